@@ -1,0 +1,111 @@
+// qk_internal.h — plan structures shared by the host runtime (qk_runtime.cpp)
+// and the sm_100a kernels (qk_kernels.cu).
+//
+// A gate block (circuit.py:166-168, executed by simulator.py:338-357) is
+// compiled on the host into one or more PASSES. A pass is one HBM sweep: every
+// CTA stages one 2^C-amplitude chunk (the address bits Q of the pass) in
+// registers/shared memory, applies the pass's ops, and writes it back. Inside
+// a pass the chunk is processed in PHASES: each thread owns 2^M amplitudes
+// whose chunk-local indices differ in the M "register qubits" of the phase;
+// non-diagonal gates need their target among the register qubits, diagonal
+// gates (RZ, RZZ, CP, D<k>) never do — runs of them are fused into one phase
+// table per run and applied as a single complex multiply per amplitude.
+#pragma once
+#include <stdint.h>
+
+namespace qk {
+
+constexpr int kMaxC = 13;        // 2^13 complex128 = 128 KiB of shared memory per CTA
+constexpr int kMaxM = 4;         // register qubits per thread (16 amplitudes)
+constexpr int kMaxOuter = 48;    // address bits outside the chunk
+constexpr int kSqsW = 4;         // SQS tile: runs of 2^4 amplitudes (256 B)
+
+enum OpCode : int32_t {
+  OP_H = 0,      // Hadamard butterfly on register slot r0 (1/sqrt2 deferred to the pass scale)
+  OP_X = 1,      // register swap on slot r0
+  OP_MAT = 2,    // dense 2x2 complex matrix coef[0..7] on slot r0
+  OP_CX = 3,     // controlled X: target slot r0; control = slot r1 (ctrl_reg=1) or chunk-local position ctrl
+  OP_SWAP = 4,   // swap register slots r0, r1
+  OP_DIAG = 5,   // multiply by tables[table + (pt | pr[j])]
+  OP_SCALE = 6,  // multiply by coef[0]
+};
+
+struct OpDesc {
+  int32_t code;
+  int32_t r0, r1;
+  int32_t ctrl;       // chunk-local control position (OP_CX with ctrl_reg == 0)
+  int32_t ctrl_reg;   // 1 if the control is register slot r1
+  int32_t coef;       // offset into the coefficient pool (doubles)
+  int64_t table;      // offset (complex entries) into the diagonal table pool
+  uint16_t tcontrib[16];  // thread bit k -> table index contribution
+  uint16_t pr[16];        // register amplitude j -> table index contribution
+};
+
+struct PhaseDesc {
+  int32_t op_begin, op_end;
+  int32_t tbits;          // C - M
+  int32_t pad;
+  uint8_t tpos[16];       // thread bit k -> chunk-local position
+  uint16_t rloc[16];      // register amplitude j -> chunk-local index
+  uint64_t taddr[16];     // thread bit k -> address offset (amplitudes)
+  uint64_t raddr[16];     // register amplitude j -> address offset (amplitudes)
+};
+
+struct PassDesc {
+  int32_t C, M;
+  int32_t phase0, nphases;
+  int32_t nouter;               // number of outer address bits
+  int32_t pad;
+  uint64_t ncta;                // 2^nouter (per launch, may be split)
+  uint8_t opos[kMaxOuter];      // outer bit k of the CTA index -> address bit
+};
+
+// Diagonal table builder: table entry x = prod over gates of entry[sub_g(x)]
+struct TableGate {
+  int32_t nt;
+  int32_t slot[13];       // table-index bit holding targets[j]; targets[0] = entry MSB
+  int64_t entries;        // offset (complex) into the entry pool
+};
+struct TableDesc {
+  int64_t out;            // offset (complex) of the table in the table pool
+  int32_t bits;           // table has 2^bits entries
+  int32_t g0, ng;         // gate range in the TableGate array
+  double scale;           // folded pass scale (H normalisation)
+};
+
+// SQS / single-device CSQS bit-permutation: new[i] = old[bitswap(i, A, B)]
+struct SqsDesc {
+  int32_t nv;                 // tile bits (first kSqsW are address bits 0..w-1)
+  int32_t w;
+  int32_t nouter;
+  int32_t nvp;                // in-tile pairs
+  int32_t nop;                // outer pairs
+  int32_t ident;              // in-tile permutation is the identity
+  uint8_t vpos[16];           // tile bit -> address bit
+  uint8_t opos[kMaxOuter];    // outer bit -> address bit
+  uint8_t va[16], vb[16];     // in-tile pairs (tile bit indices)
+  uint8_t oa[kMaxOuter], ob[kMaxOuter];  // outer pairs (outer bit indices)
+};
+
+}  // namespace qk
+
+// ---- kernel launchers (qk_kernels.cu), all asynchronous on `stream` ----
+struct CUstream_st;
+namespace qk {
+int launch_block_pass(double* state, const PassDesc* h_pass, const PassDesc* d_pass,
+                      const PhaseDesc* d_phases, const OpDesc* d_ops, const double* d_coef,
+                      const double* d_tables, uint64_t first, CUstream_st* stream);
+int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
+                        const double* d_entries, double* d_pool, CUstream_st* stream);
+int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);
+int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p, const int* q,
+                     int np, const int* a, const int* b, int k, CUstream_st* stream);
+int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* stream);
+int launch_sumsq(const double* state, uint64_t n_amps, double* d_partial, double* d_out,
+                 CUstream_st* stream);
+int launch_gather(const double* state, const uint64_t* d_idx, uint64_t count, double* d_out,
+                  CUstream_st* stream);
+int launch_gather_logical(const double* state, const int* perm, int n, uint64_t start,
+                          uint64_t count, double* d_out, CUstream_st* stream);
+int launch_fill_zero_one(double* state, uint64_t n_amps, int set_first, CUstream_st* stream);
+}  // namespace qk

@@ -1,0 +1,536 @@
+// qk_kernels.cu — hand-written sm_100a kernels of the AIC simulation path.
+//
+//   k_block_pass   gate-block pass (simulator.py:338-376): one CTA
+//                  per 2^C-amplitude chunk, register-tiled phases, swizzled
+//                  shared-memory re-layouts between phases, 128-bit global
+//                  loads/stores, diagonal runs as one table multiply.
+//   k_build_tables diagonal-run phase tables (fusion of RZ/RZZ/CP/D<k> runs,
+//                  the runtime counterpart of optimizer.py:184-276).
+//   k_sqs          in-place bit permutation new[i] = old[bitswap(i, A, B)]
+//                  (SURVEY K2/K3 single device; simulator.py:159-235) in one
+//                  HBM pass over 256-B runs.
+//   k_sqs_range    the reference's pair walk restricted to a thread range
+//                  (simulator.py:117-176 with start/stop), for unit parity.
+//   k_swap_seg     segment exchange for multi-process CSQS over NVLink P2P.
+//   k_sumsq / k_gather  norm and readback (simulator.py:393-419).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "qk_internal.h"
+
+namespace qk {
+
+// ---------------------------------------------------------------------------
+// helpers
+
+__device__ __forceinline__ uint32_t swz(uint32_t i) {
+  // XOR-fold of the 3-bit groups of i into the 16-B slot within a 128-B bank
+  // row: a quarter-warp whose lane bits sit on positions distinct mod 3
+  // (the planner guarantees it) hits 8 distinct slots -> conflict-free.
+  return i ^ (((i >> 3) ^ (i >> 6) ^ (i >> 9) ^ (i >> 12)) & 7u);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ double2 ld_g(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_g(double2* p, double2 v) {
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// register-slot gate kernels (compile-time slots, runtime dispatch)
+
+template <int M, int R>
+__device__ __forceinline__ void h_slot(double2 (&v)[1 << M]) {
+#pragma unroll
+  for (int j = 0; j < (1 << M); ++j) {
+    if (j & (1 << R)) continue;
+    const double2 a = v[j], b = v[j | (1 << R)];
+    v[j] = make_double2(a.x + b.x, a.y + b.y);
+    v[j | (1 << R)] = make_double2(a.x - b.x, a.y - b.y);
+  }
+}
+
+template <int M, int R>
+__device__ __forceinline__ void x_slot(double2 (&v)[1 << M]) {
+#pragma unroll
+  for (int j = 0; j < (1 << M); ++j) {
+    if (j & (1 << R)) continue;
+    const double2 a = v[j];
+    v[j] = v[j | (1 << R)];
+    v[j | (1 << R)] = a;
+  }
+}
+
+template <int M, int R>
+__device__ __forceinline__ void mat_slot(double2 (&v)[1 << M], const double* __restrict__ m) {
+  const double m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
+  const double m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
+#pragma unroll
+  for (int j = 0; j < (1 << M); ++j) {
+    if (j & (1 << R)) continue;
+    const double2 a = v[j], b = v[j | (1 << R)];
+    double2 n0, n1;
+    n0.x = fma(m00r, a.x, fma(-m00i, a.y, fma(m01r, b.x, -m01i * b.y)));
+    n0.y = fma(m00r, a.y, fma(m00i, a.x, fma(m01r, b.y, m01i * b.x)));
+    n1.x = fma(m10r, a.x, fma(-m10i, a.y, fma(m11r, b.x, -m11i * b.y)));
+    n1.y = fma(m10r, a.y, fma(m10i, a.x, fma(m11r, b.y, m11i * b.x)));
+    v[j] = n0;
+    v[j | (1 << R)] = n1;
+  }
+}
+
+// controlled X, target slot R; control: register slot rc (creg) or thread flag tcond
+template <int M, int R>
+__device__ __forceinline__ void cx_slot(double2 (&v)[1 << M], int creg, int rc, int tcond) {
+#pragma unroll
+  for (int j = 0; j < (1 << M); ++j) {
+    if (j & (1 << R)) continue;
+    const int cond = creg ? ((j >> rc) & 1) : tcond;
+    const double2 a = v[j], b = v[j | (1 << R)];
+    v[j] = cond ? b : a;
+    v[j | (1 << R)] = cond ? a : b;
+  }
+}
+
+template <int M, int A, int B>
+__device__ __forceinline__ void swap_slots(double2 (&v)[1 << M]) {
+#pragma unroll
+  for (int j = 0; j < (1 << M); ++j) {
+    if (!((j >> A) & 1) || ((j >> B) & 1)) continue;  // bit A set, bit B clear
+    const int k = j ^ (1 << A) ^ (1 << B);
+    const double2 t = v[j];
+    v[j] = v[k];
+    v[k] = t;
+  }
+}
+
+#define QK_DISPATCH_SLOT(FN, r, ...)                     \
+  switch (r) {                                           \
+    case 0: FN<M, 0>(__VA_ARGS__); break;                \
+    case 1: if constexpr (M > 1) FN<M, 1>(__VA_ARGS__); break; \
+    case 2: if constexpr (M > 2) FN<M, 2>(__VA_ARGS__); break; \
+    case 3: if constexpr (M > 3) FN<M, 3>(__VA_ARGS__); break; \
+    default: break;                                      \
+  }
+
+template <int M>
+__device__ __forceinline__ void swap_dispatch(double2 (&v)[1 << M], int a, int b) {
+  const int key = a * 4 + b;  // a < b
+  switch (key) {
+    case 1: if constexpr (M > 1) swap_slots<M, 0, 1>(v); break;
+    case 2: if constexpr (M > 2) swap_slots<M, 0, 2>(v); break;
+    case 3: if constexpr (M > 3) swap_slots<M, 0, 3>(v); break;
+    case 6: if constexpr (M > 2) swap_slots<M, 1, 2>(v); break;
+    case 7: if constexpr (M > 3) swap_slots<M, 1, 3>(v); break;
+    case 11: if constexpr (M > 3) swap_slots<M, 2, 3>(v); break;
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1/K4: gate-block pass
+
+template <int M, int MAXT>
+__global__ void __launch_bounds__(MAXT) k_block_pass(double2* __restrict__ state,
+                                                    const PassDesc* __restrict__ P,
+                                                    const PhaseDesc* __restrict__ PH,
+                                                    const OpDesc* __restrict__ OPS,
+                                                    const double* __restrict__ coef,
+                                                    const double2* __restrict__ tabs,
+                                                    uint64_t cta_base) {
+  extern __shared__ double2 sm[];
+  constexpr int NA = 1 << M;
+  const uint32_t tid = threadIdx.x;
+  const uint64_t X = cta_base + blockIdx.x;
+  const int nouter = P->nouter;
+  uint64_t obase = 0;
+  for (int k = 0; k < nouter; ++k) obase |= ((X >> k) & 1ull) << P->opos[k];
+
+  double2 v[NA];
+  const int np = P->nphases;
+  const PhaseDesc* D = PH + P->phase0;
+  for (int ph = 0; ph < np; ++ph, ++D) {
+    const int T = D->tbits;
+    uint32_t loct = 0;
+    uint64_t addrt = obase;
+    for (int k = 0; k < T; ++k) {
+      if ((tid >> k) & 1u) {
+        loct |= 1u << D->tpos[k];
+        addrt += D->taddr[k];
+      }
+    }
+    if (ph == 0) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) v[j] = ld_g(state + addrt + D->raddr[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) v[j] = sm[swz(loct | D->rloc[j])];
+    }
+    const int oe = D->op_end;
+    for (int o = D->op_begin; o < oe; ++o) {
+      const OpDesc* op = OPS + o;
+      const int code = op->code;
+      const int r0 = op->r0;
+      if (code == OP_H) {
+        QK_DISPATCH_SLOT(h_slot, r0, v)
+      } else if (code == OP_DIAG) {
+        uint32_t pt = 0;
+        for (int k = 0; k < T; ++k)
+          if ((tid >> k) & 1u) pt |= op->tcontrib[k];
+        const double2* tab = tabs + op->table;
+#pragma unroll
+        for (int j = 0; j < NA; ++j) v[j] = cmul(v[j], tab[pt | op->pr[j]]);
+      } else if (code == OP_MAT) {
+        const double* m = coef + op->coef;
+        QK_DISPATCH_SLOT(mat_slot, r0, v, m)
+      } else if (code == OP_X) {
+        QK_DISPATCH_SLOT(x_slot, r0, v)
+      } else if (code == OP_CX) {
+        const int creg = op->ctrl_reg;
+        const int rc = op->r1;
+        const int tcond = creg ? 0 : (int)((loct >> op->ctrl) & 1u);
+        QK_DISPATCH_SLOT(cx_slot, r0, v, creg, rc, tcond)
+      } else if (code == OP_SWAP) {
+        swap_dispatch<M>(v, r0, op->r1);
+      } else if (code == OP_SCALE) {
+        const double s = coef[op->coef];
+#pragma unroll
+        for (int j = 0; j < NA; ++j) v[j] = make_double2(v[j].x * s, v[j].y * s);
+      }
+    }
+    if (ph == np - 1) {
+#pragma unroll
+      for (int j = 0; j < NA; ++j) st_g(state + addrt + D->raddr[j], v[j]);
+    } else {
+      if (ph > 0) __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NA; ++j) sm[swz(loct | D->rloc[j])] = v[j];
+      __syncthreads();
+    }
+  }
+}
+
+int launch_block_pass(double* state, const PassDesc* h, const PassDesc* d_pass,
+                      const PhaseDesc* d_phases, const OpDesc* d_ops, const double* d_coef,
+                      const double* d_tables, uint64_t first, CUstream_st* stream) {
+  const int C = h->C, M = h->M;
+  const unsigned threads = 1u << (C - M);
+  const size_t smem = h->nphases > 1 ? ((size_t)16 << C) : 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    const int mx = 16 << kMaxC;
+    cudaFuncSetAttribute(k_block_pass<1, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_block_pass<2, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_block_pass<3, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_block_pass<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    cudaFuncSetAttribute(k_block_pass<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+    attr_set = true;
+  }
+  const uint64_t total = h->ncta;
+  const uint64_t max_grid = 1ull << 30;
+  for (uint64_t base = 0; base < total; base += max_grid) {
+    const unsigned grid = (unsigned)((total - base) < max_grid ? (total - base) : max_grid);
+    auto* st = reinterpret_cast<double2*>(state);
+    auto* tb = reinterpret_cast<const double2*>(d_tables);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const uint64_t b0 = first + base;
+    switch (M) {
+      case 1: k_block_pass<1, 512><<<grid, threads, smem, s>>>(st, d_pass, d_phases, d_ops, d_coef, tb, b0); break;
+      case 2: k_block_pass<2, 512><<<grid, threads, smem, s>>>(st, d_pass, d_phases, d_ops, d_coef, tb, b0); break;
+      case 3: k_block_pass<3, 512><<<grid, threads, smem, s>>>(st, d_pass, d_phases, d_ops, d_coef, tb, b0); break;
+      case 4:
+        if (threads <= 256)
+          k_block_pass<4, 256><<<grid, threads, smem, s>>>(st, d_pass, d_phases, d_ops, d_coef, tb, b0);
+        else
+          k_block_pass<4, 512><<<grid, threads, smem, s>>>(st, d_pass, d_phases, d_ops, d_coef, tb, b0);
+        break;
+      default: return -1;
+    }
+  }
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// diagonal-run tables
+
+__global__ void k_build_tables(const TableDesc* __restrict__ T, const TableGate* __restrict__ G,
+                               const double2* __restrict__ E, double2* __restrict__ pool) {
+  const TableDesc d = T[blockIdx.y];
+  const uint64_t n = 1ull << d.bits;
+  for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    double2 acc = make_double2(d.scale, 0.0);
+    for (int g = d.g0; g < d.g0 + d.ng; ++g) {
+      const TableGate& tg = G[g];
+      uint32_t sub = 0;
+      for (int j = 0; j < tg.nt; ++j) sub |= (uint32_t)((x >> tg.slot[j]) & 1) << (tg.nt - 1 - j);
+      acc = cmul(acc, E[tg.entries + sub]);
+    }
+    pool[d.out + x] = acc;
+  }
+}
+
+int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
+                        const double* d_entries, double* d_pool, CUstream_st* stream) {
+  if (ntables <= 0) return 0;
+  for (int base = 0; base < ntables; base += 65535) {
+    const int nt = (ntables - base) < 65535 ? (ntables - base) : 65535;
+    dim3 grid(16, nt);
+    k_build_tables<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        d_tables + base, d_gates, reinterpret_cast<const double2*>(d_entries),
+        reinterpret_cast<double2*>(d_pool));
+  }
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K2/K3 (single device): in-place bit permutation, one warp per tile pair
+
+constexpr int kSqsWarps = 8;
+
+__global__ void __launch_bounds__(256) k_sqs(double2* __restrict__ state,
+                                             const SqsDesc* __restrict__ S, uint64_t unit_base) {
+  extern __shared__ double2 sm[];
+  const int nv = S->nv;
+  const uint32_t tile = 1u << nv;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t X = unit_base + (uint64_t)blockIdx.x * kSqsWarps + warp;
+  const int nouter = S->nouter;
+  if (X >> nouter) return;
+  uint64_t Y = X;
+  for (int p = 0; p < S->nop; ++p) {
+    const uint64_t d = ((X >> S->oa[p]) ^ (X >> S->ob[p])) & 1ull;
+    Y ^= (d << S->oa[p]) | (d << S->ob[p]);
+  }
+  if (Y < X) return;
+  const bool same = (Y == X);
+  if (same && S->ident) return;
+  uint64_t bx = 0, by = 0;
+  for (int k = 0; k < nouter; ++k) {
+    bx |= ((X >> k) & 1ull) << S->opos[k];
+    by |= ((Y >> k) & 1ull) << S->opos[k];
+  }
+  double2* sx = sm + (size_t)warp * 2 * tile;
+  double2* sy = sx + tile;
+  const int w = S->w;
+  const uint32_t wmask = (1u << w) - 1;
+  for (uint32_t e = lane; e < tile; e += 32) {
+    uint64_t off = e & wmask;
+    for (int b = w; b < nv; ++b) off |= (uint64_t)((e >> b) & 1u) << S->vpos[b];
+    sx[e] = ld_g(state + bx + off);
+    if (!same) sy[e] = ld_g(state + by + off);
+  }
+  __syncwarp();
+  const int nvp = S->nvp;
+  for (uint32_t e = lane; e < tile; e += 32) {
+    uint64_t off = e & wmask;
+    for (int b = w; b < nv; ++b) off |= (uint64_t)((e >> b) & 1u) << S->vpos[b];
+    uint32_t pe = e;
+    for (int p = 0; p < nvp; ++p) {
+      const uint32_t d = ((pe >> S->va[p]) ^ (pe >> S->vb[p])) & 1u;
+      pe ^= (d << S->va[p]) | (d << S->vb[p]);
+    }
+    if (same) {
+      st_g(state + bx + off, sx[pe]);
+    } else {
+      st_g(state + bx + off, sy[pe]);
+      st_g(state + by + off, sx[pe]);
+    }
+  }
+}
+
+int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream) {
+  const uint64_t units = 1ull << h->nouter;
+  const size_t smem = (size_t)kSqsWarps * 2 * (16u << h->nv);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_sqs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSqsWarps * 2 * (16 << (2 * kSqsW)));
+    attr_set = true;
+  }
+  const uint64_t per_launch = (1ull << 30) * kSqsWarps;
+  for (uint64_t base = 0; base < units; base += per_launch) {
+    const uint64_t u = (units - base) < per_launch ? (units - base) : per_launch;
+    const unsigned grid = (unsigned)((u + kSqsWarps - 1) / kSqsWarps);
+    k_sqs<<<grid, 32 * kSqsWarps, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<double2*>(state), d, base);
+  }
+  return (int)cudaGetLastError();
+}
+
+// reference pair walk over t in [start, stop): m = bitshift(t), n = bitswap(m), swap iff m > n
+struct PairArgs {
+  int np, k;
+  int p[16], q[16];
+  int a[64], b[64];
+};
+
+__global__ void k_sqs_range(double2* __restrict__ state, uint64_t start, uint64_t stop,
+                            PairArgs pa) {
+  for (uint64_t t = start + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < stop;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t m = t;
+    for (int i = 0; i < pa.np; ++i) {
+      const uint64_t d = ((m >> pa.p[i]) ^ (m >> pa.q[i])) & 1ull;
+      m ^= (d << pa.p[i]) | (d << pa.q[i]);
+    }
+    uint64_t n = m;
+    for (int i = 0; i < pa.k; ++i) {
+      const uint64_t d = ((n >> pa.a[i]) ^ (n >> pa.b[i])) & 1ull;
+      n ^= (d << pa.a[i]) | (d << pa.b[i]);
+    }
+    if (m > n) {
+      const double2 x = state[m];
+      state[m] = state[n];
+      state[n] = x;
+    }
+  }
+}
+
+int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p, const int* q,
+                     int np, const int* a, const int* b, int k, CUstream_st* stream) {
+  if (stop <= start) return 0;
+  PairArgs pa{};
+  pa.np = np;
+  pa.k = k;
+  for (int i = 0; i < np; ++i) { pa.p[i] = p[i]; pa.q[i] = q[i]; }
+  for (int i = 0; i < k; ++i) { pa.a[i] = a[i]; pa.b[i] = b[i]; }
+  const uint64_t n = stop - start;
+  const unsigned grid = (unsigned)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
+  k_sqs_range<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<double2*>(state), start, stop, pa);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// segment exchange (either pointer may be a peer mapping over NVLink)
+
+__global__ void k_swap_seg(double2* __restrict__ a, double2* __restrict__ b, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 x = ld_g(a + i);
+    const double2 y = ld_g(b + i);
+    st_g(a + i, y);
+    st_g(b + i, x);
+  }
+}
+
+int launch_swap_segments(double* a, double* b, uint64_t n, CUstream_st* stream) {
+  if (!n) return 0;
+  const uint64_t blocks = (n + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  k_swap_seg<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), n);
+  return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// norm: deterministic two-level reduction of sum |a|^2
+
+constexpr int kSumBlocks = 148 * 8;
+
+__global__ void __launch_bounds__(256) k_sumsq(const double2* __restrict__ s, uint64_t n,
+                                               double* __restrict__ partial) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 v = s[i];
+    acc = fma(v.x, v.x, fma(v.y, v.y, acc));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void k_sum_final(const double* __restrict__ partial, int n, double* __restrict__ out) {
+  __shared__ double red[256];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+int launch_sumsq(const double* state, uint64_t n, double* d_partial, double* d_out,
+                 CUstream_st* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_sumsq<<<kSumBlocks, 256, 0, s>>>(reinterpret_cast<const double2*>(state), n, d_partial);
+  k_sum_final<<<1, 256, 0, s>>>(d_partial, kSumBlocks, d_out);
+  return (int)cudaGetLastError();
+}
+
+__global__ void k_gather(const double2* __restrict__ s, const uint64_t* __restrict__ idx,
+                         uint64_t n, double2* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = s[idx[i]];
+}
+
+int launch_gather(const double* state, const uint64_t* d_idx, uint64_t count, double* d_out,
+                  CUstream_st* stream) {
+  if (!count) return 0;
+  const uint64_t blocks = (count + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  k_gather<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const double2*>(state), d_idx, count, reinterpret_cast<double2*>(d_out));
+  return (int)cudaGetLastError();
+}
+
+struct PermArgs {
+  int n;
+  int perm[64];
+};
+
+// logical index l -> physical p: bit pos of p = bit perm[pos] of l (simulator.py:415-417)
+__global__ void k_gather_logical(const double2* __restrict__ s, PermArgs pa, uint64_t start,
+                                 uint64_t n, double2* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t l = start + i;
+    uint64_t p = 0;
+    for (int pos = 0; pos < pa.n; ++pos) p |= ((l >> pa.perm[pos]) & 1ull) << pos;
+    out[i] = s[p];
+  }
+}
+
+int launch_gather_logical(const double* state, const int* perm, int n, uint64_t start,
+                          uint64_t count, double* d_out, CUstream_st* stream) {
+  if (!count) return 0;
+  PermArgs pa{};
+  pa.n = n;
+  for (int i = 0; i < n; ++i) pa.perm[i] = perm[i];
+  const uint64_t blocks = (count + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  k_gather_logical<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const double2*>(state), pa, start, count, reinterpret_cast<double2*>(d_out));
+  return (int)cudaGetLastError();
+}
+
+int launch_fill_zero_one(double* state, uint64_t n, int set_first, CUstream_st* stream) {
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(state, 0, n * 16, s);
+  if (e != cudaSuccess) return (int)e;
+  if (set_first) {
+    static const double one[2] = {1.0, 0.0};
+    e = cudaMemcpyAsync(state, one, 16, cudaMemcpyHostToDevice, s);
+  }
+  return (int)e;
+}
+
+}  // namespace qk

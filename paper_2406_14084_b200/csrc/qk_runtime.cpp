@@ -1,0 +1,1675 @@
+// qk_runtime.cpp — host runtime behind the C ABI in include/qkb200.h.
+//
+// Owns the HBM-resident complex128 state, parses the optimized circuit format
+// (circuit.py:245-397), compiles every instruction into device plans once per
+// load (gate blocks -> passes/phases/ops + diagonal tables; SQS/CSQS -> tile
+// permutation descriptors), and replays them with asynchronous launches on one
+// stream per handle (Simulator.run, simulator.py:529-555).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qkb200.h"
+#include "qk_internal.h"
+
+using namespace qk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                          \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess)                                                      \
+      return fail(QK_ECUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(_e), \
+                  __FILE__, __LINE__, cudaGetErrorString(_e));                  \
+  } while (0)
+
+const double kSqrt1_2 = 1.0 / std::sqrt(2.0);   // simulator.py:34
+const double kDefaultAngle = 3.14159265358979323846 / 4.0;  // circuit.py:21
+
+const char* kKindName[] = {"H", "X", "U", "CX", "CP", "SWAP", "RX", "RY", "RZ", "RZZ", "D"};
+const int kArity[] = {1, 1, 1, 2, 2, 2, 1, 1, 1, 2, -1};
+const int kNParams[] = {0, 0, 3, 0, 1, 0, 1, 1, 1, 1, -1};
+
+bool is_diag(int kind) { return kind == QK_RZ || kind == QK_RZZ || kind == QK_CP || kind == QK_D; }
+
+struct GateH {
+  int kind = 0;
+  std::vector<int> t;
+  std::vector<double> p;  // angles; D: re,im pairs
+  long gid = 0;
+};
+
+struct InstrH {
+  int type = 0;  // QK_INS_*
+  std::vector<GateH> gates;
+  std::vector<int> a, b;
+};
+
+// ---------------------------------------------------------------------------
+// parser: restates circuit.py:245-287, 332-397 (messages included)
+
+struct Tok {
+  std::string s;
+};
+
+bool parse_int(const std::string& s, long* out) {
+  // Python int(): optional sign, digits, surrounding whitespace already stripped
+  if (s.empty()) return false;
+  size_t i = 0;
+  if (s[0] == '+' || s[0] == '-') i = 1;
+  if (i >= s.size()) return false;
+  for (size_t j = i; j < s.size(); ++j)
+    if (!isdigit((unsigned char)s[j]) && s[j] != '_') return false;
+  errno = 0;
+  std::string t;
+  for (char ch : s)
+    if (ch != '_') t.push_back(ch);
+  *out = strtol(t.c_str(), nullptr, 10);
+  return errno == 0;
+}
+
+bool parse_float(const std::string& s, double* out) {
+  if (s.empty()) return false;
+  char* end = nullptr;
+  *out = strtod(s.c_str(), &end);
+  return end && *end == '\0';
+}
+
+std::string pyrepr(const std::string& s) { return "'" + s + "'"; }
+
+struct Parser {
+  int n, c, local;
+  std::string msg;
+  int line_no = 0;
+  int code = QK_OK;
+
+  int err(int ln, const std::string& m) {
+    line_no = ln;
+    msg = "line " + std::to_string(ln) + ": " + m;
+    code = QK_EPARSE;
+    return code;
+  }
+  int verr(const std::string& m) {
+    msg = m;
+    code = QK_EINVAL;
+    return code;
+  }
+
+  int gate_line(const std::vector<std::string>& tk, int ln, GateH* g) {
+    const std::string& k0 = tk[0];
+    int kind = -1, darity = -1;
+    if (k0.size() > 1 && k0[0] == 'D' &&
+        std::all_of(k0.begin() + 1, k0.end(), [](char ch) { return isdigit((unsigned char)ch); })) {
+      kind = QK_D;
+      darity = atoi(k0.c_str() + 1);
+    } else {
+      for (int i = 0; i < 10; ++i)
+        if (k0 == kKindName[i]) kind = i;
+      if (kind < 0) return err(ln, "unknown gate symbol " + pyrepr(k0));
+    }
+    g->kind = kind;
+    if (kind == QK_D) {
+      const long want = 1 + darity + 2 * (1L << std::min(darity, 30));
+      if ((long)tk.size() != want)
+        return err(ln, "D" + std::to_string(darity) + " line needs " + std::to_string(want) +
+                           " tokens, got " + std::to_string(tk.size()));
+      for (int j = 0; j < darity; ++j) {
+        long v;
+        if (!parse_int(tk[1 + j], &v))
+          return err(ln, "invalid literal for int() with base 10: " + pyrepr(tk[1 + j]));
+        g->t.push_back((int)v);
+      }
+      for (size_t j = 1 + darity; j < tk.size(); ++j) {
+        double v;
+        if (!parse_float(tk[j], &v)) return err(ln, "could not convert string to float: " + pyrepr(tk[j]));
+        g->p.push_back(v);
+      }
+      g->gid = -1;
+    } else {
+      const int ar = kArity[kind], np = kNParams[kind];
+      std::vector<std::string> ptok;
+      if ((int)tk.size() == 1 + ar + 1) {
+      } else if ((int)tk.size() == 1 + ar + 1 + np) {
+        ptok.assign(tk.begin() + 1 + ar + 1, tk.end());
+      } else {
+        return err(ln, std::string("wrong token count for ") + kKindName[kind] + ": got " +
+                           std::to_string(tk.size()));
+      }
+      for (int j = 0; j < ar; ++j) {
+        long v;
+        if (!parse_int(tk[1 + j], &v))
+          return err(ln, "invalid literal for int() with base 10: " + pyrepr(tk[1 + j]));
+        g->t.push_back((int)v);
+      }
+      long gid;
+      if (!parse_int(tk[1 + ar], &gid))
+        return err(ln, "invalid literal for int() with base 10: " + pyrepr(tk[1 + ar]));
+      g->gid = gid;
+      if (ptok.empty()) {
+        g->p.assign(np, kDefaultAngle);
+      } else {
+        for (auto& s : ptok) {
+          double v;
+          if (!parse_float(s, &v)) return err(ln, "could not convert string to float: " + pyrepr(s));
+          g->p.push_back(v);
+        }
+      }
+    }
+    for (int q : g->t)
+      if (q < 0 || q >= n)
+        return err(ln, "qubit index out of range: " + std::to_string(q) + " (N=" + std::to_string(n) + ")");
+    for (size_t i = 0; i < g->t.size(); ++i)
+      for (size_t j = i + 1; j < g->t.size(); ++j)
+        if (g->t[i] == g->t[j])
+          return err(ln, std::string("duplicate target qubits in ") + kKindName[kind]);
+    if (g->gid < 0 && kind != QK_D) return err(ln, "negative gate id " + std::to_string(g->gid));
+    if (kind == QK_D && darity < 2) return verr("fused diagonal needs at least 2 qubits");
+    return QK_OK;
+  }
+
+  int run(const char* text, size_t len, std::vector<InstrH>* out) {
+    std::vector<std::pair<int, std::vector<std::string>>> lines;
+    size_t pos = 0;
+    int ln = 0;
+    while (pos <= len) {
+      size_t e = pos;
+      while (e < len && text[e] != '\n') ++e;
+      ++ln;
+      std::string line(text + pos, e - pos);
+      if (!line.empty() && line.back() == '\r') line.pop_back();
+      const size_t hash = line.find('#');
+      if (hash != std::string::npos) line.resize(hash);
+      std::vector<std::string> tk;
+      size_t i = 0;
+      while (i < line.size()) {
+        while (i < line.size() && isspace((unsigned char)line[i])) ++i;
+        size_t j = i;
+        while (j < line.size() && !isspace((unsigned char)line[j])) ++j;
+        if (j > i) tk.emplace_back(line.substr(i, j - i));
+        i = j;
+      }
+      if (!tk.empty()) lines.emplace_back(ln, std::move(tk));
+      if (e >= len) break;
+      pos = e + 1;
+    }
+    size_t i = 0;
+    while (i < lines.size()) {
+      const int lno = lines[i].first;
+      const auto& tk = lines[i].second;
+      if (tk.size() != 1) {
+        std::string j;
+        for (size_t q = 0; q < tk.size(); ++q) j += (q ? " " : "") + tk[q];
+        return err(lno, "expected a record count, got " + pyrepr(j));
+      }
+      long count;
+      if (!parse_int(tk[0], &count)) return err(lno, "expected a record count, got " + pyrepr(tk[0]));
+      if (count < 1) return err(lno, "record count must be positive");
+      if (i + 1 + (size_t)count > lines.size())
+        return err(lno, "record claims " + std::to_string(count) + " lines but file ends early");
+      const std::string& first = lines[i + 1].second[0];
+      if (first == "SQS" || first == "CSQS") {
+        if (count != 1) return err(lno, "swap records hold exactly one line");
+        const int l2 = lines[i + 1].first;
+        const auto& st = lines[i + 1].second;
+        if (st.size() < 2) return err(l2, first + " needs a pair count");
+        long m;
+        if (!parse_int(st[1], &m)) return err(l2, "invalid literal for int() with base 10: " + pyrepr(st[1]));
+        std::vector<int> ops;
+        for (size_t q = 2; q < st.size(); ++q) {
+          long v;
+          if (!parse_int(st[q], &v)) return err(l2, "invalid literal for int() with base 10: " + pyrepr(st[q]));
+          ops.push_back((int)v);
+        }
+        if ((long)st.size() != 2 + 2 * m)
+          return err(l2, first + " " + std::to_string(m) + " needs exactly " + std::to_string(2 + 2 * m) +
+                             " tokens, got " + std::to_string(st.size()));
+        InstrH ins;
+        ins.type = first == "SQS" ? QK_INS_SQS : QK_INS_CSQS;
+        ins.a.assign(ops.begin(), ops.begin() + m);
+        ins.b.assign(ops.begin() + m, ops.end());
+        if (ins.type == QK_INS_SQS) {
+          for (int x : ins.a)
+            for (int y : ins.b)
+              if (x == y) return verr("swap sets must be disjoint");
+          for (int q : ins.a)
+            if (q < 0 || q >= local) return err(l2, "SQS index " + std::to_string(q) + " outside local range");
+          for (int q : ins.b)
+            if (q < 0 || q >= local) return err(l2, "SQS index " + std::to_string(q) + " outside local range");
+        } else {
+          for (int q : ins.a)
+            if (q < 0 || q >= local)
+              return err(l2, "CSQS local index " + std::to_string(q) + " outside local range");
+          for (int q : ins.b)
+            if (q < local || q >= n)
+              return err(l2, "CSQS rank index " + std::to_string(q) + " outside rank range");
+        }
+        out->push_back(std::move(ins));
+      } else {
+        InstrH ins;
+        ins.type = QK_INS_BLOCK;
+        for (long q = 0; q < count; ++q) {
+          const int l2 = lines[i + 1 + q].first;
+          GateH g;
+          if (gate_line(lines[i + 1 + q].second, l2, &g)) return code;
+          if (c > 0)
+            for (int t : g.t)
+              if (t >= c)
+                return err(l2, "gate target " + std::to_string(t) + " >= chunk qubits C=" + std::to_string(c));
+          ins.gates.push_back(std::move(g));
+        }
+        out->push_back(std::move(ins));
+      }
+      i += 1 + count;
+    }
+    return QK_OK;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// gate constants (circuit.py:420-463; simulator.py:242-310)
+
+typedef std::complex<double> cplx;
+
+cplx cexpi(double x) { return cplx(std::cos(x), std::sin(x)); }
+
+// diagonal entries; targets[0] = MSB of the entry index
+std::vector<cplx> diag_entries(const GateH& g) {
+  const double th = g.p.empty() ? 0.0 : g.p[0];
+  switch (g.kind) {
+    case QK_RZ: return {cexpi(-0.5 * th), cexpi(0.5 * th)};
+    case QK_RZZ: {
+      const cplx em = cexpi(-0.5 * th), ep = cexpi(0.5 * th);
+      return {em, ep, ep, em};
+    }
+    case QK_CP: return {1.0, 1.0, 1.0, cexpi(th)};
+    default: {
+      std::vector<cplx> e;
+      for (size_t i = 0; i + 1 < g.p.size(); i += 2) e.emplace_back(g.p[i], g.p[i + 1]);
+      return e;
+    }
+  }
+}
+
+// 2x2 matrix (row-major m00 m01 m10 m11) of U, RX, RY
+void mat2(const GateH& g, cplx m[4]) {
+  if (g.kind == QK_U) {
+    const double th = g.p[0], ph = g.p[1], lam = g.p[2];
+    const double ct = std::cos(th / 2), st = std::sin(th / 2);
+    m[0] = ct;
+    m[1] = -cexpi(lam) * st;
+    m[2] = cexpi(ph) * st;
+    m[3] = cexpi(ph + lam) * ct;
+  } else if (g.kind == QK_RX) {
+    const double c = std::cos(g.p[0] / 2), s = std::sin(g.p[0] / 2);
+    m[0] = c;
+    m[1] = cplx(0, -s);
+    m[2] = cplx(0, -s);
+    m[3] = c;
+  } else {  // RY
+    const double c = std::cos(g.p[0] / 2), s = std::sin(g.p[0] / 2);
+    m[0] = c;
+    m[1] = -s;
+    m[2] = s;
+    m[3] = c;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plans
+
+struct HostPlan {
+  std::vector<PassDesc> passes;
+  std::vector<PhaseDesc> phases;
+  std::vector<OpDesc> ops;
+  std::vector<double> coef;
+  std::vector<TableDesc> tables;
+  std::vector<TableGate> tgates;
+  std::vector<double> entries;  // complex pairs
+  int64_t pool = 0;             // table pool size (complex entries)
+  std::vector<SqsDesc> sqs;
+  void clear() { *this = HostPlan(); }
+};
+
+struct InstrPlan {
+  int type;
+  int pass0 = 0, npass = 0;  // block
+  int sqs = -1;              // SQS / single-device CSQS
+  int csqs_s = 0;            // multi-process CSQS
+  std::vector<int> a, b;
+  double bytes = 0;          // algorithmic HBM bytes
+};
+
+int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+// thread-bit order: lane bits 0..2 on positions distinct mod 3 (swizzle-friendly)
+std::vector<int> order_tpos(const std::vector<int>& T) {
+  if (T.size() < 3) return T;
+  std::vector<int> first;
+  for (int p : T) {
+    bool ok = true;
+    for (int q : first)
+      if (q % 3 == p % 3) ok = false;
+    if (ok) first.push_back(p);
+    if (first.size() == 3) break;
+  }
+  if (first.size() < 3) return T;
+  std::vector<int> out = first;
+  for (int p : T)
+    if (std::find(first.begin(), first.end(), p) == first.end()) out.push_back(p);
+  return out;
+}
+
+struct Item {
+  int type;  // 0 gate, 1 diag run
+  const GateH* g;
+  int run;
+};
+
+// Compile the gates of one pass over chunk address bits Q (ascending) of a
+// vector of `nbits` address bits.
+int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std::vector<int>& Q,
+                 int nbits, uint64_t ncta_override, std::string& emsg) {
+  const int C = (int)Q.size();
+  const int M = std::min(kMaxM, C);
+  int loc[64];
+  for (int& x : loc) x = -1;
+  for (int l = 0; l < C; ++l) loc[Q[l]] = l;
+
+  // 1. diagonal runs (diagonal gates commute with each other and with any gate
+  //    on disjoint qubits: a diagonal gate joins the latest run unless a
+  //    non-diagonal gate emitted after that run touches one of its qubits)
+  std::vector<Item> items;
+  std::vector<std::vector<const GateH*>> runs;
+  std::vector<uint32_t> run_support;
+  int last_run = -1;
+  uint32_t blocked = 0;
+  int nh = 0;
+  for (const GateH* g : gates) {
+    uint32_t tm = 0;
+    for (int t : g->t) {
+      if (t >= 64 || loc[t] < 0) {
+        emsg = "gate target outside pass chunk";
+        return QK_ESIM;
+      }
+      tm |= 1u << loc[t];
+    }
+    if (is_diag(g->kind)) {
+      if (last_run >= 0 && !(tm & blocked)) {
+        runs[last_run].push_back(g);
+        run_support[last_run] |= tm;
+      } else {
+        runs.push_back({g});
+        run_support.push_back(tm);
+        last_run = (int)runs.size() - 1;
+        blocked = 0;
+        items.push_back({1, nullptr, last_run});
+      }
+    } else {
+      items.push_back({0, g, -1});
+      blocked |= tm;
+      if (g->kind == QK_H) ++nh;
+    }
+  }
+  // 2. register needs per item
+  auto needs = [&](const Item& it) -> std::vector<int> {
+    if (it.type == 1) return {};
+    const GateH* g = it.g;
+    if (g->kind == QK_CX) return {loc[g->t[1]]};
+    std::vector<int> r;
+    for (int t : g->t) r.push_back(loc[t]);
+    return r;
+  };
+  // 3. phases
+  struct PhaseB {
+    std::vector<int> R;
+    std::vector<int> items;
+  };
+  std::vector<PhaseB> phs;
+  for (size_t i = 0; i < items.size(); ++i) {
+    std::vector<int> need = needs(items[i]);
+    bool fits = !phs.empty();
+    if (fits)
+      for (int q : need)
+        if (std::find(phs.back().R.begin(), phs.back().R.end(), q) == phs.back().R.end()) fits = false;
+    if (!fits) {
+      PhaseB pb;
+      pb.R = need;
+      for (size_t j = i + 1; j < items.size() && (int)pb.R.size() < M; ++j)
+        for (int q : needs(items[j]))
+          if ((int)pb.R.size() < M && std::find(pb.R.begin(), pb.R.end(), q) == pb.R.end())
+            pb.R.push_back(q);
+      for (int q = C - 1; q >= 0 && (int)pb.R.size() < M; --q)  // fill with high positions
+        if (std::find(pb.R.begin(), pb.R.end(), q) == pb.R.end()) pb.R.push_back(q);
+      phs.push_back(pb);
+    }
+    phs.back().items.push_back((int)i);
+  }
+  if (phs.empty()) {  // no gates at all: nothing to do
+    return QK_OK;
+  }
+  // 4. tables for runs (built on device at load), H scale folded into the first table
+  const double scale = (nh % 2 == 0) ? std::ldexp(1.0, -nh / 2) : std::ldexp(kSqrt1_2, -(nh - 1) / 2);
+  bool scale_folded = (nh == 0);
+  std::vector<int64_t> run_table(runs.size());
+  for (size_t r = 0; r < runs.size(); ++r) {
+    const uint32_t S = run_support[r];
+    int bidx[32];
+    int nb = 0;
+    for (int p = 0; p < C; ++p)
+      if (S >> p & 1) bidx[p] = nb++;
+    TableDesc td{};
+    td.out = hp.pool;
+    td.bits = nb;
+    td.g0 = (int)hp.tgates.size();
+    td.ng = (int)runs[r].size();
+    td.scale = 1.0;
+    if (!scale_folded) {
+      td.scale = scale;
+      scale_folded = true;
+    }
+    for (const GateH* g : runs[r]) {
+      TableGate tg{};
+      tg.nt = (int)g->t.size();
+      for (int j = 0; j < tg.nt; ++j) tg.slot[j] = bidx[loc[g->t[j]]];
+      tg.entries = (int64_t)hp.entries.size() / 2;
+      std::vector<cplx> e = diag_entries(*g);
+      if (g->kind == QK_D) {
+        for (auto& x : e)
+          if (std::fabs(std::abs(x) - 1.0) > 1e-9) {
+            emsg = "non-unitary fused gate";
+            return QK_EINVAL;
+          }
+      }
+      for (auto& x : e) {
+        hp.entries.push_back(x.real());
+        hp.entries.push_back(x.imag());
+      }
+      hp.tgates.push_back(tg);
+    }
+    run_table[r] = hp.pool;
+    hp.pool += (int64_t)1 << nb;
+    hp.tables.push_back(td);
+  }
+  // 5. emit phases and ops
+  PassDesc pd{};
+  pd.C = C;
+  pd.M = M;
+  pd.phase0 = (int)hp.phases.size();
+  pd.nphases = (int)phs.size();
+  std::vector<int> O;
+  for (int p = 0; p < nbits; ++p)
+    if (std::find(Q.begin(), Q.end(), p) == Q.end()) O.push_back(p);
+  if ((int)O.size() > kMaxOuter) {
+    emsg = "too many outer bits";
+    return QK_ESIM;
+  }
+  pd.nouter = (int)O.size();
+  for (size_t k = 0; k < O.size(); ++k) pd.opos[k] = (uint8_t)O[k];
+  pd.ncta = ncta_override ? ncta_override : (1ull << O.size());
+  for (size_t ph = 0; ph < phs.size(); ++ph) {
+    const PhaseB& pb = phs[ph];
+    std::vector<int> T;
+    for (int p = 0; p < C; ++p)
+      if (std::find(pb.R.begin(), pb.R.end(), p) == pb.R.end()) T.push_back(p);
+    T = order_tpos(T);
+    PhaseDesc D{};
+    D.tbits = C - M;
+    for (int k = 0; k < D.tbits; ++k) {
+      D.tpos[k] = (uint8_t)T[k];
+      D.taddr[k] = 1ull << Q[T[k]];
+    }
+    for (int j = 0; j < (1 << M); ++j) {
+      uint32_t rl = 0;
+      uint64_t ra = 0;
+      for (int s = 0; s < M; ++s)
+        if (j >> s & 1) {
+          rl |= 1u << pb.R[s];
+          ra |= 1ull << Q[pb.R[s]];
+        }
+      D.rloc[j] = (uint16_t)rl;
+      D.raddr[j] = ra;
+    }
+    D.op_begin = (int)hp.ops.size();
+    auto slot = [&](int lpos) {
+      for (int s = 0; s < M; ++s)
+        if (pb.R[s] == lpos) return s;
+      return -1;
+    };
+    for (int ii : pb.items) {
+      const Item& it = items[ii];
+      OpDesc op{};
+      if (it.type == 1) {
+        const uint32_t S = run_support[it.run];
+        int bidx[32];
+        int nb = 0;
+        for (int p = 0; p < C; ++p)
+          if (S >> p & 1) bidx[p] = nb++;
+        op.code = OP_DIAG;
+        op.table = run_table[it.run];
+        for (int k = 0; k < D.tbits; ++k) op.tcontrib[k] = (S >> T[k] & 1) ? (uint16_t)(1u << bidx[T[k]]) : 0;
+        for (int j = 0; j < (1 << M); ++j) {
+          uint32_t v = 0;
+          for (int s = 0; s < M; ++s)
+            if ((j >> s & 1) && (S >> pb.R[s] & 1)) v |= 1u << bidx[pb.R[s]];
+          op.pr[j] = (uint16_t)v;
+        }
+      } else {
+        const GateH* g = it.g;
+        switch (g->kind) {
+          case QK_H: op.code = OP_H; op.r0 = slot(loc[g->t[0]]); break;
+          case QK_X: op.code = OP_X; op.r0 = slot(loc[g->t[0]]); break;
+          case QK_U:
+          case QK_RX:
+          case QK_RY: {
+            op.code = OP_MAT;
+            op.r0 = slot(loc[g->t[0]]);
+            cplx m[4];
+            mat2(*g, m);
+            op.coef = (int)hp.coef.size();
+            for (auto& x : m) {
+              hp.coef.push_back(x.real());
+              hp.coef.push_back(x.imag());
+            }
+            break;
+          }
+          case QK_CX: {
+            op.code = OP_CX;
+            op.r0 = slot(loc[g->t[1]]);
+            const int cs = slot(loc[g->t[0]]);
+            if (cs >= 0) {
+              op.ctrl_reg = 1;
+              op.r1 = cs;
+            } else {
+              op.ctrl = loc[g->t[0]];
+            }
+            break;
+          }
+          case QK_SWAP: {
+            op.code = OP_SWAP;
+            const int s0 = slot(loc[g->t[0]]), s1 = slot(loc[g->t[1]]);
+            op.r0 = std::min(s0, s1);
+            op.r1 = std::max(s0, s1);
+            break;
+          }
+          default:
+            emsg = "no kernel for gate kind";
+            return QK_ESIM;
+        }
+      }
+      hp.ops.push_back(op);
+    }
+    if (ph + 1 == phs.size() && !scale_folded) {
+      OpDesc op{};
+      op.code = OP_SCALE;
+      op.coef = (int)hp.coef.size();
+      hp.coef.push_back(scale);
+      hp.ops.push_back(op);
+      scale_folded = true;
+    }
+    D.op_end = (int)hp.ops.size();
+    hp.phases.push_back(D);
+  }
+  hp.passes.push_back(pd);
+  return QK_OK;
+}
+
+// Chunk-address sets for a block: one pass with Q = [0, C) when every target
+// fits kMaxC (chunk-local path, simulator.py:481-492); otherwise gates are
+// grouped into memory-level passes whose Q = targets + lowest free bits
+// (simulator.py:494-511, same per-amplitude gate order).
+int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& ip,
+                  std::string& emsg, int cmin = 10) {
+  int maxt = -1;
+  for (auto& g : ins.gates)
+    for (int t : g.t) maxt = std::max(maxt, t);
+  ip.pass0 = (int)hp.passes.size();
+  if (maxt < 0) return QK_OK;
+  if (maxt >= L) {
+    emsg = "gate target " + std::to_string(maxt) + " beyond local range";
+    return QK_ESIM;
+  }
+  const int low_keep = std::min(3, L);
+  if (maxt < kMaxC) {
+    int C = std::max(maxt + 1, std::min(L, cmin));
+    C = std::min(C, std::min(L, kMaxC));
+    if (C > 12 && maxt < 12) C = 12;
+    std::vector<int> Q;
+    for (int p = 0; p < C; ++p) Q.push_back(p);
+    std::vector<const GateH*> gs;
+    for (auto& g : ins.gates) gs.push_back(&g);
+    int rc = compile_pass(hp, gs, Q, nbits, 0, emsg);
+    if (rc) return rc;
+  } else {
+    size_t i = 0;
+    while (i < ins.gates.size()) {
+      uint64_t U = 0;
+      std::vector<const GateH*> gs;
+      while (i < ins.gates.size()) {
+        uint64_t tm = 0;
+        for (int t : ins.gates[i].t) tm |= 1ull << t;
+        if (!gs.empty() && popc(U | tm) > kMaxC - low_keep) break;
+        U |= tm;
+        gs.push_back(&ins.gates[i]);
+        ++i;
+      }
+      const int C = std::min(L, std::max(popc(U) + low_keep, std::min(L, cmin)));
+      std::vector<int> Q;
+      for (int p = 0; p < L; ++p)
+        if (U >> p & 1) Q.push_back(p);
+      for (int p = 0; p < L && (int)Q.size() < std::min(C, kMaxC); ++p)
+        if (!(U >> p & 1)) Q.push_back(p);
+      std::sort(Q.begin(), Q.end());
+      int rc = compile_pass(hp, gs, Q, nbits, 0, emsg);
+      if (rc) return rc;
+    }
+  }
+  ip.npass = (int)hp.passes.size() - ip.pass0;
+  ip.bytes = 32.0 * std::ldexp(1.0, nbits) * ip.npass;
+  return QK_OK;
+}
+
+// new[i] = old[bitswap(i, A, B)] over a vector of nbits address bits
+int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>& B0, int nbits) {
+  std::vector<int> A = A0, B = B0;
+  std::sort(A.begin(), A.end());
+  std::sort(B.begin(), B.end());
+  const int w = std::min(kSqsW, nbits);
+  std::vector<int> V;
+  for (int p = 0; p < w; ++p) V.push_back(p);
+  for (size_t k = 0; k < A.size(); ++k) {
+    if (A[k] < w && B[k] >= w) V.push_back(B[k]);
+    if (B[k] < w && A[k] >= w) V.push_back(A[k]);
+  }
+  std::sort(V.begin() + w, V.end());
+  SqsDesc sd{};
+  sd.w = w;
+  sd.nv = (int)V.size();
+  for (int b = 0; b < sd.nv; ++b) sd.vpos[b] = (uint8_t)V[b];
+  std::vector<int> O;
+  for (int p = 0; p < nbits; ++p)
+    if (std::find(V.begin(), V.end(), p) == V.end()) O.push_back(p);
+  sd.nouter = (int)O.size();
+  for (size_t k = 0; k < O.size(); ++k) sd.opos[k] = (uint8_t)O[k];
+  auto vidx = [&](int p) { return (int)(std::find(V.begin(), V.end(), p) - V.begin()); };
+  auto oidx = [&](int p) { return (int)(std::find(O.begin(), O.end(), p) - O.begin()); };
+  for (size_t k = 0; k < A.size(); ++k) {
+    const bool ain = std::find(V.begin(), V.end(), A[k]) != V.end();
+    if (ain) {
+      sd.va[sd.nvp] = (uint8_t)vidx(A[k]);
+      sd.vb[sd.nvp] = (uint8_t)vidx(B[k]);
+      ++sd.nvp;
+    } else {
+      sd.oa[sd.nop] = (uint8_t)oidx(A[k]);
+      sd.ob[sd.nop] = (uint8_t)oidx(B[k]);
+      ++sd.nop;
+    }
+  }
+  sd.ident = sd.nvp == 0;
+  hp.sqs.push_back(sd);
+  return (int)hp.sqs.size() - 1;
+}
+
+// reference shift_pairs (simulator.py:91-106): iteration-order remap for ranges
+void shift_pairs(const std::vector<int>& a_bits, const std::vector<int>& b_bits, int cl, int n_local,
+                 std::vector<int>& P, std::vector<int>& Qo) {
+  std::vector<int> a = a_bits, b = b_bits;
+  std::sort(a.begin(), a.end());
+  std::sort(b.begin(), b.end());
+  int na = 0, nb = 0;
+  for (int x : a) na += x < cl;
+  for (int x : b) nb += x < cl;
+  const int d = std::abs(na - nb);
+  P.clear();
+  Qo.clear();
+  if (d == 0) return;
+  const std::vector<int>& donors = na > nb ? b_bits : a_bits;
+  std::vector<int> dout;
+  for (int x : donors)
+    if (x >= cl) dout.push_back(x);
+  std::sort(dout.begin(), dout.end());
+  std::vector<int> p0;
+  for (int x = cl; x < cl + d; ++x)
+    if (x < n_local) p0.push_back(x);
+  std::vector<int> q0(dout.begin(), dout.begin() + std::min(dout.size(), p0.size()));
+  p0.resize(q0.size());
+  for (size_t i = 0; i < p0.size(); ++i)
+    if (std::find(q0.begin(), q0.end(), p0[i]) == q0.end()) P.push_back(p0[i]);
+  for (size_t i = 0; i < q0.size(); ++i)
+    if (std::find(p0.begin(), p0.end(), q0[i]) == p0.end()) Qo.push_back(q0[i]);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handle
+
+struct qk_sim {
+  int n = 0, r = 0, b = 0, device = 0;
+  int rank_lo = 0, count = 1;
+  int L = 0, nbits = 0;  // local qubits, address bits held by this handle
+  double* state = nullptr;
+  size_t amps = 0;
+  cudaStream_t stream = nullptr;
+  // program
+  std::vector<InstrH> prog;
+  std::vector<InstrPlan> iplan;
+  HostPlan hp;
+  std::vector<int> final_perm;
+  // device plan
+  void* blob = nullptr;
+  size_t blob_bytes = 0;
+  PassDesc* d_pass = nullptr;
+  PhaseDesc* d_phase = nullptr;
+  OpDesc* d_ops = nullptr;
+  double* d_coef = nullptr;
+  SqsDesc* d_sqs = nullptr;
+  double* d_pool = nullptr;
+  size_t pool_bytes = 0;
+  // scratch
+  double* d_partial = nullptr;
+  double* d_scalar = nullptr;
+  void* d_scratch = nullptr;
+  size_t scratch_bytes = 0;
+  // timing
+  std::vector<cudaEvent_t> events;
+  int per_launch = 0;
+  double stat_ms[3] = {0, 0, 0};
+  double stat_launch[3] = {0, 0, 0};
+  double stat_bytes[3] = {0, 0, 0};
+  // multi-process
+  qk_barrier_fn barrier = nullptr;
+  void* barrier_ctx = nullptr;
+  std::vector<double*> peers;  // by shard index
+  int nshards = 1, shard = 0;
+};
+
+namespace {
+
+int ensure_scratch(qk_sim* s, size_t bytes) {
+  if (s->scratch_bytes >= bytes) return QK_OK;
+  if (s->d_scratch) cudaFree(s->d_scratch);
+  s->d_scratch = nullptr;
+  s->scratch_bytes = 0;
+  CUDA_TRY(cudaMalloc(&s->d_scratch, bytes));
+  s->scratch_bytes = bytes;
+  return QK_OK;
+}
+
+template <class T>
+size_t push_section(std::vector<char>& buf, const std::vector<T>& v) {
+  size_t off = (buf.size() + 255) & ~(size_t)255;
+  buf.resize(off + v.size() * sizeof(T));
+  if (!v.empty()) memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+int upload_plan(qk_sim* s) {
+  HostPlan& hp = s->hp;
+  std::vector<char> buf;
+  const size_t o_pass = push_section(buf, hp.passes);
+  const size_t o_phase = push_section(buf, hp.phases);
+  const size_t o_ops = push_section(buf, hp.ops);
+  const size_t o_coef = push_section(buf, hp.coef);
+  const size_t o_sqs = push_section(buf, hp.sqs);
+  const size_t o_tab = push_section(buf, hp.tables);
+  const size_t o_tg = push_section(buf, hp.tgates);
+  const size_t o_ent = push_section(buf, hp.entries);
+  buf.resize(buf.size() + 256);
+  if (s->blob_bytes < buf.size()) {
+    if (s->blob) cudaFree(s->blob);
+    s->blob = nullptr;
+    s->blob_bytes = 0;
+    CUDA_TRY(cudaMalloc(&s->blob, buf.size()));
+    s->blob_bytes = buf.size();
+  }
+  char* base = (char*)s->blob;
+  CUDA_TRY(cudaMemcpyAsync(base, buf.data(), buf.size(), cudaMemcpyHostToDevice, s->stream));
+  s->d_pass = (PassDesc*)(base + o_pass);
+  s->d_phase = (PhaseDesc*)(base + o_phase);
+  s->d_ops = (OpDesc*)(base + o_ops);
+  s->d_coef = (double*)(base + o_coef);
+  s->d_sqs = (SqsDesc*)(base + o_sqs);
+  const size_t pool_bytes = (size_t)std::max<int64_t>(hp.pool, 1) * 16;
+  if (s->pool_bytes < pool_bytes) {
+    if (s->d_pool) cudaFree(s->d_pool);
+    s->d_pool = nullptr;
+    s->pool_bytes = 0;
+    CUDA_TRY(cudaMalloc(&s->d_pool, pool_bytes));
+    s->pool_bytes = pool_bytes;
+  }
+  if (!hp.tables.empty()) {
+    int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
+                                 (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
+                                 s->d_pool, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "table build launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+void replay_perm(qk_sim* s) {
+  s->final_perm.resize(s->n);
+  for (int i = 0; i < s->n; ++i) s->final_perm[i] = i;
+  for (auto& ins : s->prog) {
+    if (ins.type == QK_INS_BLOCK) continue;
+    std::vector<int> a = ins.a, b = ins.b;
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    for (size_t k = 0; k < a.size() && k < b.size(); ++k) std::swap(s->final_perm[a[k]], s->final_perm[b[k]]);
+  }
+}
+
+int check_csqs(const qk_sim* s, const std::vector<int>& local_set, const std::vector<int>& rank_set) {
+  // simulator.py:184-194
+  const int local = s->L, S = (int)local_set.size();
+  std::vector<int> srt = local_set;
+  std::sort(srt.begin(), srt.end());
+  bool top = true;
+  for (int i = 0; i < S; ++i)
+    if (srt[i] != local - S + i) top = false;
+  if (!top) {
+    std::string l = "(";
+    for (int i = 0; i < S; ++i) l += std::to_string(local_set[i]) + (S == 1 ? "," : (i + 1 < S ? ", " : ""));
+    l += ")";
+    return fail(QK_ESIM, "cross-rank local set %s is not top-of-local", l.c_str());
+  }
+  if ((int)rank_set.size() != S) return fail(QK_ESIM, "cross-rank swap sets differ in size");
+  for (int q : rank_set)
+    if (q < local || q >= s->n) return fail(QK_ESIM, "rank bit %d outside [%d, %d)", q, local, s->n);
+  if (s->b < S) return fail(QK_ESIM, "buffer of 2^%d too small for %d swap pairs", s->b, S);
+  return QK_OK;
+}
+
+int compile_program(qk_sim* s) {
+  s->hp.clear();
+  s->iplan.clear();
+  std::string emsg;
+  for (auto& ins : s->prog) {
+    InstrPlan ip;
+    ip.type = ins.type;
+    if (ins.type == QK_INS_BLOCK) {
+      int rc = compile_block(s->hp, ins, s->L, s->nbits, ip, emsg);
+      if (rc) return fail(rc, "%s", emsg.c_str());
+    } else if (ins.type == QK_INS_SQS) {
+      for (int q : ins.a)
+        if (q < 0 || q >= s->L)
+          return fail(QK_EINVAL, "swap bit %d out of range for %d local qubits", q, s->L);
+      for (int q : ins.b)
+        if (q < 0 || q >= s->L)
+          return fail(QK_EINVAL, "swap bit %d out of range for %d local qubits", q, s->L);
+      ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, ins.a, ins.b, s->nbits);
+      ip.bytes = 32.0 * std::ldexp(1.0, s->nbits) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
+    } else {
+      int rc = check_csqs(s, ins.a, ins.b);
+      if (rc) return rc;
+      // rank bits held inside this handle become plain address bits
+      const int held_rank_bits = s->nbits - s->L;
+      bool local_only = true;
+      for (int q : ins.b)
+        if (q - s->L >= held_rank_bits) local_only = false;
+      ip.a = ins.a;
+      ip.b = ins.b;
+      ip.csqs_s = (int)ins.a.size();
+      if (local_only) {
+        ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, ins.a, ins.b, s->nbits);
+      } else {
+        ip.sqs = -2;  // cross-process exchange
+      }
+      ip.bytes = 32.0 * std::ldexp(1.0, s->nbits) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
+    }
+    s->iplan.push_back(std::move(ip));
+  }
+  replay_perm(s);
+  return upload_plan(s);
+}
+
+int ensure_events(qk_sim* s, size_t n) {
+  while (s->events.size() < n) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    s->events.push_back(e);
+  }
+  return QK_OK;
+}
+
+int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
+  PassDesc h = s->hp.passes[p];
+  if (count_override) h.ncta = count_override;
+  int rc = launch_block_pass(s->state, &h, s->d_pass + p, s->d_phase, s->d_ops, s->d_coef, s->d_pool, first,
+                             (CUstream_st*)s->stream);
+  if (rc) return fail(QK_ECUDA, "block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+  return QK_OK;
+}
+
+int exchange_cross(qk_sim* s, const InstrPlan& ip);
+
+int run_instr(qk_sim* s, const InstrPlan& ip) {
+  if (ip.type == QK_INS_BLOCK) {
+    for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
+      int rc = launch_pass(s, p);
+      if (rc) return rc;
+    }
+    return QK_OK;
+  }
+  if (ip.sqs >= 0) {
+    int rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "sqs launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+    return QK_OK;
+  }
+  if (ip.sqs == -2) return exchange_cross(s, ip);
+  return QK_OK;
+}
+
+// Multi-process CSQS (simulator.py:179-235 semantics; output independent of
+// B): the swapped rank bits select peer shards. For every pair of shards
+// (x, y) in a group, segment y of x and segment x of y are exchanged; the
+// lower shard of a pair moves the first half of the segment, the higher one
+// the second half, so both NVLink directions carry equal traffic.
+int exchange_cross(qk_sim* s, const InstrPlan& ip) {
+  if (s->nshards <= 1 || (int)s->peers.size() < s->nshards)
+    return fail(QK_ESIM, "cross-rank swap needs the peer shards' state (qk_ipc_open)");
+  const int S = ip.csqs_s;
+  const int held = s->nbits - s->L;  // rank bits inside a shard
+  std::vector<int> loc = ip.a, rk = ip.b;
+  std::sort(loc.begin(), loc.end());
+  std::sort(rk.begin(), rk.end());
+  // pairs whose rank bit is inside the shard: plain local permutation first
+  std::vector<int> in_a, in_b, out_a, out_b;
+  for (int k = 0; k < S; ++k) {
+    if (rk[k] - s->L < held) {
+      in_a.push_back(loc[k]);
+      in_b.push_back(rk[k]);
+    } else {
+      out_a.push_back(loc[k]);
+      out_b.push_back(rk[k]);
+    }
+  }
+  if (s->barrier) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
+  }
+  // shard-bit positions of the out-of-shard rank bits
+  const int so = (int)out_a.size();
+  std::vector<int> sbit(so);
+  for (int k = 0; k < so; ++k) sbit[k] = out_b[k] - s->L - held;
+  // local bits out_a are positions < L inside each partition; segment index =
+  // value of those bits. For each partition held and each peer pattern y != x:
+  const uint64_t part = 1ull << s->L;
+  for (int pi = 0; pi < s->count; ++pi) {
+    const int me = s->shard;
+    int x = 0;
+    for (int k = 0; k < so; ++k) x |= ((me >> sbit[k]) & 1) << k;
+    for (int y = 0; y < (1 << so); ++y) {
+      if (y == x) continue;
+      int peer = me;
+      for (int k = 0; k < so; ++k) {
+        peer &= ~(1 << sbit[k]);
+        peer |= ((y >> k) & 1) << sbit[k];
+      }
+      // amplitudes of my partition pi whose out_a bits == y <-> peer partition pi whose bits == x.
+      // out_a are the top local bits (checked by check_csqs) when in_a is empty; general case
+      // handled by enumerating contiguous runs below the lowest swapped bit.
+      const int lo = *std::min_element(out_a.begin(), out_a.end());
+      const uint64_t run = 1ull << lo;
+      const uint64_t nruns = part >> (lo + so);
+      const uint64_t half = run / 2 ? run / 2 : run;
+      const bool first_half = me < peer;
+      for (uint64_t rr = 0; rr < nruns; ++rr) {
+        uint64_t base = rr << (lo + so);
+        uint64_t my_off = base, peer_off = base;
+        for (int k = 0; k < so; ++k) {
+          my_off |= (uint64_t)((y >> k) & 1) << out_a[k];
+          peer_off |= (uint64_t)((x >> k) & 1) << out_a[k];
+        }
+        double* mine = s->state + 2 * (pi * part + my_off);
+        double* theirs = s->peers[peer] + 2 * (pi * part + peer_off);
+        uint64_t off = 0, len = run;
+        if (run > 1) {
+          off = first_half ? 0 : half;
+          len = half;
+        } else if (!first_half) {
+          continue;
+        }
+        int rc = launch_swap_segments(mine + 2 * off, theirs + 2 * off, len, (CUstream_st*)s->stream);
+        if (rc) return fail(QK_ECUDA, "peer exchange failed");
+      }
+    }
+  }
+  if (s->barrier) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
+  }
+  if (!in_a.empty()) {
+    HostPlan tmp;
+    compile_sqs(tmp, in_a, in_b, s->nbits);
+    SqsDesc* d = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(SqsDesc), s->stream));
+    CUDA_TRY(cudaMemcpyAsync(d, &tmp.sqs[0], sizeof(SqsDesc), cudaMemcpyHostToDevice, s->stream));
+    launch_sqs(s->state, &tmp.sqs[0], d, (CUstream_st*)s->stream);
+    CUDA_TRY(cudaFreeAsync(d, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
+  return QK_OK;
+}
+
+int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out) {
+  if (!out) return fail(QK_EINVAL, "null output handle");
+  *out = nullptr;
+  if (n < 0 || r < 0 || r > n) return fail(QK_EINVAL, "need 0 <= R <= N, got R=%d, N=%d", r, n);
+  if (b < 0 || b > n - r) return fail(QK_EINVAL, "need B <= N-R, got B=%d, N-R=%d", b, n - r);
+  if (count < 1 || (count & (count - 1)) || rank_lo < 0 || rank_lo % count || rank_lo + count > (1 << r))
+    return fail(QK_EINVAL, "bad shard [%d, %d) of %d ranks", rank_lo, rank_lo + count, 1 << r);
+  const double required = std::ldexp(16.0, n);
+  const int hb = __builtin_ctz((unsigned)count);
+  const int nbits = n - r + hb;
+  if (n > 62) return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
+  CUDA_TRY(cudaSetDevice(device));
+  size_t free_b = 0, total_b = 0;
+  CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const size_t need = (size_t)16 << nbits;
+  if (nbits > 40 || (double)need > 0.97 * (double)free_b)
+    return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
+  qk_sim* s = new qk_sim();
+  s->n = n;
+  s->r = r;
+  s->b = b;
+  s->device = device;
+  s->rank_lo = rank_lo;
+  s->count = count;
+  s->L = n - r;
+  s->nbits = nbits;
+  s->amps = (size_t)1 << nbits;
+  s->nshards = (1 << r) / count;
+  s->shard = rank_lo / count;
+  cudaError_t e = cudaMalloc(&s->state, need);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete s;
+    return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
+  }
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaMalloc(&s->d_partial, 148 * 8 * sizeof(double) + 256));
+  s->d_scalar = s->d_partial + 148 * 8;
+  int rc = launch_fill_zero_one(s->state, s->amps, rank_lo == 0, (CUstream_st*)s->stream);
+  if (rc) return fail(QK_ECUDA, "state init failed");
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  s->peers.assign(s->nshards, nullptr);
+  s->peers[s->shard] = s->state;
+  *out = s;
+  return QK_OK;
+}
+
+std::vector<InstrH> unpack(const int32_t* w, size_t nw, const double* p, size_t np, int* rc_out,
+                           std::string& emsg) {
+  std::vector<InstrH> out;
+  size_t i = 0, pi = 0;
+  *rc_out = QK_OK;
+  auto bad = [&](const char* m) {
+    emsg = m;
+    *rc_out = QK_EINVAL;
+    return std::vector<InstrH>();
+  };
+  while (i < nw) {
+    InstrH ins;
+    ins.type = w[i++];
+    if (ins.type == -1) break;  // gate-id side channel of qk_parse_text
+    if (i >= nw) return bad("truncated packed program");
+    const int cnt = w[i++];
+    if (ins.type == QK_INS_BLOCK) {
+      for (int g = 0; g < cnt; ++g) {
+        if (i + 2 > nw) return bad("truncated packed gate");
+        GateH gh;
+        gh.kind = w[i++];
+        const int nt = w[i++];
+        if (gh.kind < 0 || gh.kind > QK_D || nt < 1 || nt > 24 || i + nt + 1 > nw)
+          return bad("bad packed gate");
+        for (int k = 0; k < nt; ++k) gh.t.push_back(w[i++]);
+        const int npar = w[i++];
+        if (pi + npar > np) return bad("packed params exhausted");
+        gh.p.assign(p + pi, p + pi + npar);
+        pi += npar;
+        if (gh.kind == QK_D && npar != (2 << nt)) return bad("D gate needs 2^k complex entries");
+        ins.gates.push_back(std::move(gh));
+      }
+    } else if (ins.type == QK_INS_SQS || ins.type == QK_INS_CSQS) {
+      if (i + 2 * (size_t)cnt > nw) return bad("truncated swap record");
+      ins.a.assign(w + i, w + i + cnt);
+      ins.b.assign(w + i + cnt, w + i + 2 * cnt);
+      i += 2 * cnt;
+    } else {
+      return bad("unknown packed record");
+    }
+    out.push_back(std::move(ins));
+  }
+  return out;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int qk_version(void) { return 1; }
+const char* qk_last_error(void) { return g_err.c_str(); }
+
+int qk_device_count(int* count) {
+  if (!count) return fail(QK_EINVAL, "null pointer");
+  cudaError_t e = cudaGetDeviceCount(count);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return fail(QK_ECUDA, "no CUDA device: %s", cudaGetErrorString(e));
+  }
+  return QK_OK;
+}
+
+int qk_create(int n, int r, int b, int device, qk_sim** out) {
+  return create_common(n, r, b, device, 0, 1 << std::max(0, std::min(r, 30)), out);
+}
+
+int qk_create_shard(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out) {
+  return create_common(n, r, b, device, rank_lo, count, out);
+}
+
+int qk_destroy(qk_sim* s) {
+  if (!s) return QK_OK;
+  cudaSetDevice(s->device);
+  if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto e : s->events) cudaEventDestroy(e);
+  for (size_t i = 0; i < s->peers.size(); ++i)
+    if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
+  if (s->state) cudaFree(s->state);
+  if (s->blob) cudaFree(s->blob);
+  if (s->d_pool) cudaFree(s->d_pool);
+  if (s->d_partial) cudaFree(s->d_partial);
+  if (s->d_scratch) cudaFree(s->d_scratch);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return QK_OK;
+}
+
+int qk_reset(qk_sim* s) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc = launch_fill_zero_one(s->state, s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
+  if (rc) return fail(QK_ECUDA, "reset failed");
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_layout(const qk_sim* s, int* n, int* r, int* b, int* rank_lo, int* count) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  if (n) *n = s->n;
+  if (r) *r = s->r;
+  if (b) *b = s->b;
+  if (rank_lo) *rank_lo = s->rank_lo;
+  if (count) *count = s->count;
+  return QK_OK;
+}
+
+int qk_load_text(qk_sim* s, const char* text, size_t len, int c, int* n_instr) {
+  if (!s || (!text && len)) return fail(QK_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(s->device));
+  Parser ps;
+  ps.n = s->n;
+  ps.local = s->L;
+  ps.c = c;
+  std::vector<InstrH> prog;
+  if (ps.run(text, len, &prog)) return fail(ps.code, "%s", ps.msg.c_str());
+  s->prog = std::move(prog);
+  int rc = compile_program(s);
+  if (rc) return rc;
+  if (n_instr) *n_instr = (int)s->prog.size();
+  return QK_OK;
+}
+
+int qk_load_packed(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc;
+  std::string emsg;
+  std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
+  if (rc) return fail(rc, "%s", emsg.c_str());
+  s->prog = std::move(prog);
+  return compile_program(s);
+}
+
+int qk_program_info(const qk_sim* s, int* n_instr, int* n_blocks, int* n_sqs, int* n_csqs, int32_t* perm) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  int nb = 0, ns = 0, nc = 0;
+  for (auto& i : s->prog) {
+    nb += i.type == QK_INS_BLOCK;
+    ns += i.type == QK_INS_SQS;
+    nc += i.type == QK_INS_CSQS;
+  }
+  if (n_instr) *n_instr = (int)s->prog.size();
+  if (n_blocks) *n_blocks = nb;
+  if (n_sqs) *n_sqs = ns;
+  if (n_csqs) *n_csqs = nc;
+  if (perm)
+    for (int i = 0; i < s->n; ++i) perm[i] = i < (int)s->final_perm.size() ? s->final_perm[i] : i;
+  return QK_OK;
+}
+
+int qk_set_profiling(qk_sim* s, int per_launch) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  s->per_launch = per_launch;
+  return QK_OK;
+}
+
+int qk_run(qk_sim* s, double* timings) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(s->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t ni = s->iplan.size();
+  int rc = ensure_events(s, 2 * ni + 2);
+  if (rc) return rc;
+  for (size_t i = 0; i < ni; ++i) {
+    CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
+    rc = run_instr(s, s->iplan[i]);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  double cls[3] = {0, 0, 0};
+  for (size_t i = 0; i < ni; ++i) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
+    const int c = s->iplan[i].type;
+    cls[c] += ms;
+    s->stat_ms[c] += ms;
+    s->stat_bytes[c] += s->iplan[i].bytes;
+    s->stat_launch[c] += c == QK_INS_BLOCK ? s->iplan[i].npass : (s->iplan[i].sqs != -1 ? 1 : 0);
+  }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (timings) {
+    timings[0] = cls[0] * 1e-3;
+    timings[1] = cls[1] * 1e-3;
+    timings[2] = cls[2] * 1e-3;
+    timings[3] = wall;
+  }
+  return QK_OK;
+}
+
+int qk_kernel_stats(qk_sim* s, double* out, int reset) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  if (out)
+    for (int c = 0; c < 3; ++c) {
+      out[2 * c] = s->stat_ms[c];
+      out[2 * c + 1] = s->stat_launch[c];
+      out[6 + c] = s->stat_bytes[c];
+    }
+  if (reset)
+    for (int c = 0; c < 3; ++c) s->stat_ms[c] = s->stat_launch[c] = s->stat_bytes[c] = 0;
+  return QK_OK;
+}
+
+int qk_sumsq(qk_sim* s, double* sumsq) {
+  if (!s || !sumsq) return fail(QK_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc = launch_sumsq(s->state, s->amps, s->d_partial, s->d_scalar, (CUstream_st*)s->stream);
+  if (rc) return fail(QK_ECUDA, "norm launch failed");
+  CUDA_TRY(cudaMemcpyAsync(sumsq, s->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_read_physical(qk_sim* s, int part, uint64_t off, uint64_t count, double* reim) {
+  if (!s || (!reim && count)) return fail(QK_EINVAL, "null argument");
+  const uint64_t psize = 1ull << s->L;
+  if (part < 0 || part >= s->count || off + count > psize || off > psize)
+    return fail(QK_EINVAL, "read outside partition");
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (count)
+    CUDA_TRY(cudaMemcpyAsync(reim, s->state + 2 * (part * psize + off), count * 16, cudaMemcpyDeviceToHost,
+                             s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_write_physical(qk_sim* s, int part, uint64_t off, uint64_t count, const double* reim) {
+  if (!s || (!reim && count)) return fail(QK_EINVAL, "null argument");
+  const uint64_t psize = 1ull << s->L;
+  if (part < 0 || part >= s->count || off + count > psize || off > psize)
+    return fail(QK_EINVAL, "write outside partition");
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (count)
+    CUDA_TRY(cudaMemcpyAsync(s->state + 2 * (part * psize + off), reim, count * 16, cudaMemcpyHostToDevice,
+                             s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_gather(qk_sim* s, const uint64_t* idx, uint64_t count, double* reim) {
+  if (!s || (count && (!idx || !reim))) return fail(QK_EINVAL, "null argument");
+  if (!count) return QK_OK;
+  const uint64_t lo = (uint64_t)s->rank_lo << s->L;
+  for (uint64_t i = 0; i < count; ++i)
+    if (idx[i] < lo || idx[i] - lo >= s->amps) return fail(QK_EINVAL, "index %llu not held by this handle",
+                                                          (unsigned long long)idx[i]);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const uint64_t chunk = 1u << 22;
+  int rc = ensure_scratch(s, chunk * 24);
+  if (rc) return rc;
+  uint64_t* d_idx = (uint64_t*)s->d_scratch;
+  double* d_out = (double*)((char*)s->d_scratch + chunk * 8);
+  std::vector<uint64_t> rel(std::min(count, chunk));
+  for (uint64_t b = 0; b < count; b += chunk) {
+    const uint64_t m = std::min(chunk, count - b);
+    for (uint64_t i = 0; i < m; ++i) rel[i] = idx[b + i] - lo;
+    CUDA_TRY(cudaMemcpyAsync(d_idx, rel.data(), m * 8, cudaMemcpyHostToDevice, s->stream));
+    rc = launch_gather(s->state, d_idx, m, d_out, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "gather failed");
+    CUDA_TRY(cudaMemcpyAsync(reim + 2 * b, d_out, m * 16, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
+  return QK_OK;
+}
+
+int qk_read_logical(qk_sim* s, const int32_t* perm, const uint64_t* lidx, uint64_t count, double* reim) {
+  if (!s || !perm || (count && (!lidx || !reim))) return fail(QK_EINVAL, "null argument");
+  std::vector<uint64_t> phys(count);
+  for (uint64_t i = 0; i < count; ++i) {
+    if (s->n < 64 && (lidx[i] >> s->n)) return fail(QK_EINVAL, "logical index %llu out of range",
+                                                    (unsigned long long)lidx[i]);
+    uint64_t p = 0;
+    for (int pos = 0; pos < s->n; ++pos) p |= ((lidx[i] >> perm[pos]) & 1ull) << pos;
+    phys[i] = p;
+  }
+  return qk_gather(s, phys.data(), count, reim);
+}
+
+int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64_t count, double* reim) {
+  if (!s || !perm || (count && !reim)) return fail(QK_EINVAL, "null argument");
+  if (s->count != (1 << s->r)) return fail(QK_EINVAL, "logical range readback needs the whole state");
+  if (s->n < 64 && (start + count > (1ull << s->n) || start > (1ull << s->n)))
+    return fail(QK_EINVAL, "logical range out of bounds");
+  CUDA_TRY(cudaSetDevice(s->device));
+  const uint64_t chunk = 1u << 22;
+  int rc = ensure_scratch(s, chunk * 16);
+  if (rc) return rc;
+  std::vector<int> pm(perm, perm + s->n);
+  for (uint64_t b = 0; b < count; b += chunk) {
+    const uint64_t m = std::min(chunk, count - b);
+    rc = launch_gather_logical(s->state, pm.data(), s->n, start + b, m, (double*)s->d_scratch,
+                               (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "logical gather failed");
+    CUDA_TRY(cudaMemcpyAsync(reim + 2 * b, s->d_scratch, m * 16, cudaMemcpyDeviceToHost, s->stream));
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+  }
+  return QK_OK;
+}
+
+int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t* words, size_t* nwords,
+                  double* params, size_t* nparams, int* err_line) {
+  if (!nwords || !nparams || (!text && len)) return fail(QK_EINVAL, "null argument");
+  Parser ps;
+  ps.n = n;
+  ps.local = local;
+  ps.c = c;
+  std::vector<InstrH> prog;
+  if (ps.run(text, len, &prog)) {
+    if (err_line) *err_line = ps.line_no;
+    return fail(ps.code, "%s", ps.msg.c_str());
+  }
+  std::vector<int32_t> w;
+  std::vector<double> p;
+  for (auto& ins : prog) {
+    w.push_back(ins.type);
+    if (ins.type == QK_INS_BLOCK) {
+      w.push_back((int32_t)ins.gates.size());
+      for (auto& g : ins.gates) {
+        w.push_back(g.kind);
+        w.push_back((int32_t)g.t.size());
+        for (int t : g.t) w.push_back(t);
+        w.push_back((int32_t)g.p.size());
+        p.insert(p.end(), g.p.begin(), g.p.end());
+        // gate id rides after the packed program: kept in a side channel below
+      }
+    } else {
+      w.push_back((int32_t)ins.a.size());
+      w.insert(w.end(), ins.a.begin(), ins.a.end());
+      w.insert(w.end(), ins.b.begin(), ins.b.end());
+    }
+  }
+  // gate ids (one per gate, in order) are appended after the program words,
+  // preceded by a sentinel record type -1 and their count
+  std::vector<int32_t> ids;
+  for (auto& ins : prog)
+    if (ins.type == QK_INS_BLOCK)
+      for (auto& g : ins.gates) ids.push_back((int32_t)g.gid);
+  w.push_back(-1);
+  w.push_back((int32_t)ids.size());
+  w.insert(w.end(), ids.begin(), ids.end());
+  if (words) {
+    if (*nwords < w.size() || *nparams < p.size()) return fail(QK_EINVAL, "buffers too small");
+    memcpy(words, w.data(), w.size() * 4);
+    if (!p.empty()) memcpy(params, p.data(), p.size() * 8);
+  }
+  *nwords = w.size();
+  *nparams = p.size();
+  return QK_OK;
+}
+
+int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, const double* params,
+                   size_t nparams, int c, uint64_t row_start, uint64_t row_stop) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
+  if (c < 1 || c > s->L) return fail(QK_EINVAL, "bad chunk width %d", c);
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc;
+  std::string emsg;
+  std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
+  if (rc) return fail(rc, "%s", emsg.c_str());
+  if (prog.size() != 1 || prog[0].type != QK_INS_BLOCK) return fail(QK_EINVAL, "expected one gate block");
+  static const char* names[] = {"H", "X", "U", "CX", "CP", "SWAP", "RX", "RY", "RZ", "RZZ", "D"};
+  for (auto& g : prog[0].gates)
+    for (int t : g.t)
+      if (t >= c) {
+        std::string tg = "(";
+        for (size_t k = 0; k < g.t.size(); ++k)
+          tg += std::to_string(g.t[k]) + (g.t.size() == 1 ? "," : (k + 1 < g.t.size() ? ", " : ""));
+        tg += ")";
+        return fail(QK_ESIM, "gate %s %s does not fit width %d", names[g.kind], tg.c_str(), c);
+      }
+  const uint64_t rows = 1ull << (s->L - c);
+  if (row_stop > rows) row_stop = rows;
+  if (row_start >= row_stop) return QK_OK;
+  // chunk = [0, c) of the partition, outer = [c, L): CTA index == row
+  HostPlan keep = std::move(s->hp);
+  s->hp.clear();
+  std::vector<int> Q;
+  for (int p = 0; p < c; ++p) Q.push_back(p);
+  std::vector<const GateH*> gs;
+  for (auto& g : prog[0].gates) gs.push_back(&g);
+  rc = compile_pass(s->hp, gs, Q, s->L, 0, emsg);
+  if (rc) {
+    s->hp = std::move(keep);
+    return fail(rc, "%s", emsg.c_str());
+  }
+  rc = upload_plan(s);
+  if (!rc && !s->hp.passes.empty()) {
+    double* saved = s->state;
+    s->state = s->state + 2 * ((uint64_t)part << s->L);
+    rc = launch_pass(s, 0, row_start, row_stop - row_start);
+    s->state = saved;
+    if (!rc) {
+      cudaError_t e = cudaStreamSynchronize(s->stream);
+      if (e != cudaSuccess) rc = fail(QK_ECUDA, "%s", cudaGetErrorString(e));
+    }
+  }
+  s->hp = std::move(keep);
+  int rc2 = upload_plan(s);
+  return rc ? rc : rc2;
+}
+
+int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc;
+  std::string emsg;
+  std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
+  if (rc) return fail(rc, "%s", emsg.c_str());
+  if (prog.size() != 1 || prog[0].type != QK_INS_BLOCK) return fail(QK_EINVAL, "expected one gate block");
+  HostPlan keep = std::move(s->hp);
+  s->hp.clear();
+  InstrPlan ip;
+  // force the memory-level grouping by compiling gate by gate as singleton blocks
+  rc = QK_OK;
+  for (auto& g : prog[0].gates) {
+    InstrH one;
+    one.type = QK_INS_BLOCK;
+    one.gates.push_back(g);
+    rc = compile_block(s->hp, one, s->L, s->nbits, ip, emsg);
+    if (rc) break;
+  }
+  if (rc) {
+    s->hp = std::move(keep);
+    return fail(rc, "%s", emsg.c_str());
+  }
+  rc = upload_plan(s);
+  for (size_t p = 0; !rc && p < s->hp.passes.size(); ++p) rc = launch_pass(s, (int)p);
+  if (!rc) {
+    cudaError_t e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) rc = fail(QK_ECUDA, "%s", cudaGetErrorString(e));
+  }
+  s->hp = std::move(keep);
+  int rc2 = upload_plan(s);
+  return rc ? rc : rc2;
+}
+
+int qk_sqs(qk_sim* s, int part, const int32_t* out_set, const int32_t* in_set, int k, int cl,
+           uint64_t start, uint64_t stop) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
+  std::vector<int> a(out_set, out_set + k), b(in_set, in_set + k);
+  for (int q : a)
+    if (q < 0 || q >= s->L) return fail(QK_EINVAL, "swap bit %d out of range for %d local qubits", q, s->L);
+  for (int q : b)
+    if (q < 0 || q >= s->L) return fail(QK_EINVAL, "swap bit %d out of range for %d local qubits", q, s->L);
+  for (int x : a)
+    for (int y : b)
+      if (x == y) return fail(QK_EINVAL, "bit sets overlap");
+  CUDA_TRY(cudaSetDevice(s->device));
+  const uint64_t size = 1ull << s->L;
+  if (stop > size) stop = size;
+  double* base = s->state + 2 * ((uint64_t)part << s->L);
+  if (k == 0 || start >= stop) return QK_OK;
+  if (start == 0 && stop == size) {
+    HostPlan tmp;
+    compile_sqs(tmp, a, b, s->L);
+    int rc = ensure_scratch(s, sizeof(SqsDesc));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(s->d_scratch, &tmp.sqs[0], sizeof(SqsDesc), cudaMemcpyHostToDevice, s->stream));
+    rc = launch_sqs(base, &tmp.sqs[0], (const SqsDesc*)s->d_scratch, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "sqs launch failed");
+  } else {
+    std::vector<int> P, Qo;
+    shift_pairs(a, b, cl, s->L, P, Qo);
+    std::vector<int> sa = a, sb = b;
+    std::sort(sa.begin(), sa.end());
+    std::sort(sb.begin(), sb.end());
+    std::vector<int> sp = P, sq = Qo;
+    std::sort(sp.begin(), sp.end());
+    std::sort(sq.begin(), sq.end());
+    int rc = launch_sqs_range(base, start, stop, sp.data(), sq.data(), (int)sp.size(), sa.data(), sb.data(), k,
+                              (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "sqs range launch failed");
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_csqs(qk_sim* s, const int32_t* local_set, const int32_t* rank_set, int S) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  std::vector<int> a(local_set, local_set + S), b(rank_set, rank_set + S);
+  int rc = check_csqs(s, a, b);
+  if (rc) return rc;
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (S == 0) return QK_OK;
+  InstrPlan ip;
+  ip.type = QK_INS_CSQS;
+  ip.a = a;
+  ip.b = b;
+  ip.csqs_s = S;
+  const int held = s->nbits - s->L;
+  bool local_only = true;
+  for (int q : b)
+    if (q - s->L >= held) local_only = false;
+  if (!local_only) {
+    rc = exchange_cross(s, ip);
+    if (rc) return rc;
+  } else {
+    HostPlan tmp;
+    compile_sqs(tmp, a, b, s->nbits);
+    rc = ensure_scratch(s, sizeof(SqsDesc));
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(s->d_scratch, &tmp.sqs[0], sizeof(SqsDesc), cudaMemcpyHostToDevice, s->stream));
+    rc = launch_sqs(s->state, &tmp.sqs[0], (const SqsDesc*)s->d_scratch, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "csqs launch failed");
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_ipc_handle(qk_sim* s, void* handle64) {
+  if (!s || !handle64) return fail(QK_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(s->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, s->state));
+  memcpy(handle64, &h, sizeof h);
+  return QK_OK;
+}
+
+int qk_ipc_open(qk_sim* s, int peer, const void* handle64) {
+  if (!s || !handle64) return fail(QK_EINVAL, "null argument");
+  if (peer < 0 || peer >= s->nshards) return fail(QK_EINVAL, "bad peer shard %d", peer);
+  if (peer == s->shard) return QK_OK;
+  CUDA_TRY(cudaSetDevice(s->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  s->peers[peer] = (double*)p;
+  return QK_OK;
+}
+
+int qk_set_barrier(qk_sim* s, qk_barrier_fn fn, void* ctx) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  s->barrier = fn;
+  s->barrier_ctx = ctx;
+  return QK_OK;
+}
+
+int qk_sync(qk_sim* s) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  CUDA_TRY(cudaSetDevice(s->device));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+}  // extern "C"
