@@ -175,6 +175,11 @@ int qk_ipc_open(qk_sim* sim, int peer_shard, const void* handle64);
 typedef int (*qk_barrier_fn)(void* ctx);
 int qk_set_barrier(qk_sim* sim, qk_barrier_fn fn, void* ctx);
 
+/* Device-side markers on the handle's stream (CUDA events, slots 0..7), for
+ * timing a bracket of several calls on the launching stream. */
+int qk_mark(qk_sim* sim, int slot);
+int qk_mark_elapsed(qk_sim* sim, int slot_a, int slot_b, double* ms);
+
 /* Synchronize the handle's streams. */
 int qk_sync(qk_sim* sim);
 

@@ -62,6 +62,8 @@ _SIGS = {
     "qk_ipc_handle": (c_int, [c_void, c_void]),
     "qk_ipc_open": (c_int, [c_void, c_int, c_void]),
     "qk_set_barrier": (c_int, [c_void, BARRIER_FN, c_void]),
+    "qk_mark": (c_int, [c_void, c_int]),
+    "qk_mark_elapsed": (c_int, [c_void, c_int, c_int, P(c_dbl)]),
     "qk_sync": (c_int, [c_void]),
 }
 
@@ -294,3 +296,11 @@ class Handle:
 
     def sync(self):
         check(lib().qk_sync(self.ptr))
+
+    def mark(self, slot: int):
+        check(lib().qk_mark(self.ptr, slot))
+
+    def mark_elapsed_ms(self, a: int, b: int) -> float:
+        v = c_dbl(0.0)
+        check(lib().qk_mark_elapsed(self.ptr, a, b, ctypes.byref(v)))
+        return v.value

@@ -11,6 +11,7 @@
 // gates (RZ, RZZ, CP, D<k>) never do — runs of them are fused into one phase
 // table per run and applied as a single complex multiply per amplitude.
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 
 namespace qk {
@@ -18,7 +19,7 @@ namespace qk {
 constexpr int kMaxC = 13;        // 2^13 complex128 = 128 KiB of shared memory per CTA
 constexpr int kMaxM = 4;         // register qubits per thread (16 amplitudes)
 constexpr int kMaxOuter = 48;    // address bits outside the chunk
-constexpr int kSqsW = 4;         // SQS tile: runs of 2^4 amplitudes (256 B)
+constexpr int kSqsW = 5;         // SQS tile: runs of 2^5 amplitudes (512 B)
 
 enum OpCode : int32_t {
   OP_H = 0,      // Hadamard butterfly on register slot r0 (1/sqrt2 deferred to the pass scale)
@@ -81,10 +82,39 @@ struct SqsDesc {
   int32_t nvp;                // in-tile pairs
   int32_t nop;                // outer pairs
   int32_t ident;              // in-tile permutation is the identity
-  uint8_t vpos[16];           // tile bit -> address bit
+  uint8_t vpos[16];           // tile bit -> address bit (nv <= 10)
   uint8_t opos[kMaxOuter];    // outer bit -> address bit
   uint8_t va[16], vb[16];     // in-tile pairs (tile bit indices)
   uint8_t oa[kMaxOuter], ob[kMaxOuter];  // outer pairs (outer bit indices)
+};
+
+// ---- persistent TMA gate-block pass (contiguous chunks, C in [9, 12], M = 4) ----
+constexpr int kTMaxPh = 12;
+constexpr int kTMaxOps = 64;
+constexpr int kTMaxCoef = 128;
+
+struct TOp {
+  int8_t code, r0, r1, creg;
+  int16_t ctrl, coef;
+  int32_t table;
+  uint16_t tcontrib[12];
+  uint16_t pr[16];
+};
+
+struct TPhase {
+  int16_t op_begin, op_end;
+  uint8_t tpos[12];
+  uint16_t rloc[16];
+};
+
+struct alignas(64) TmaParams {
+  CUtensorMap map;              // 2-D view {16 doubles, rows} of the state, SWIZZLE_128B
+  const double* tabs;           // diagonal table pool
+  uint64_t nchunks;
+  int32_t C, nphases, box_rows, ntma, ng, stages;
+  TPhase ph[kTMaxPh];
+  TOp ops[kTMaxOps];
+  double coef[kTMaxCoef];
 };
 
 }  // namespace qk
@@ -95,6 +125,8 @@ namespace qk {
 int launch_block_pass(double* state, const PassDesc* h_pass, const PassDesc* d_pass,
                       const PhaseDesc* d_phases, const OpDesc* d_ops, const double* d_coef,
                       const double* d_tables, uint64_t first, CUstream_st* stream);
+int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream);
+int tma_smem_bytes(int C, int* ng, int* stages);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);

@@ -138,7 +138,7 @@ __device__ __forceinline__ void swap_dispatch(double2 (&v)[1 << M], int a, int b
 // K1/K4: gate-block pass
 
 template <int M, int MAXT>
-__global__ void __launch_bounds__(MAXT) k_block_pass(double2* __restrict__ state,
+__global__ void __launch_bounds__(MAXT, 512 / MAXT + 1) k_block_pass(double2* __restrict__ state,
                                                     const PassDesc* __restrict__ P,
                                                     const PhaseDesc* __restrict__ PH,
                                                     const OpDesc* __restrict__ OPS,
@@ -291,77 +291,118 @@ int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate*
 }
 
 // ---------------------------------------------------------------------------
-// K2/K3 (single device): in-place bit permutation, one warp per tile pair
+// K2/K3 (single device): in-place bit permutation new[i] = old[bitswap(i, A, B)].
+// The planner splits the address bits into a tile set V (the low w bits, the
+// partners of any of them, and fillers up to 2^8..2^10 amplitudes) and the
+// outer bits O. Pairs inside V permute within a tile; pairs inside O map tile
+// X to tile Y = pi(X). A CTA moves one canonical tile pair (X <= Y) per loop
+// iteration: every thread issues all its loads (runs of 2^w amplitudes are
+// contiguous across lanes), then writes the swapped/permuted values back —
+// through shared memory only when the in-tile permutation is not the identity.
 
-constexpr int kSqsWarps = 8;
+__device__ __forceinline__ uint64_t warp_or64(uint64_t v) {
+  const uint32_t lo = __reduce_or_sync(0xffffffffu, (uint32_t)v);
+  const uint32_t hi = __reduce_or_sync(0xffffffffu, (uint32_t)(v >> 32));
+  return ((uint64_t)hi << 32) | lo;
+}
 
-__global__ void __launch_bounds__(256) k_sqs(double2* __restrict__ state,
-                                             const SqsDesc* __restrict__ S, uint64_t unit_base) {
+__global__ void __launch_bounds__(256) k_sqs(double2* __restrict__ state, const __grid_constant__ SqsDesc S) {
   extern __shared__ double2 sm[];
-  const int nv = S->nv;
+  const int nv = S.nv, w = S.w;
   const uint32_t tile = 1u << nv;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t X = unit_base + (uint64_t)blockIdx.x * kSqsWarps + warp;
-  const int nouter = S->nouter;
-  if (X >> nouter) return;
-  uint64_t Y = X;
-  for (int p = 0; p < S->nop; ++p) {
-    const uint64_t d = ((X >> S->oa[p]) ^ (X >> S->ob[p])) & 1ull;
-    Y ^= (d << S->oa[p]) | (d << S->ob[p]);
-  }
-  if (Y < X) return;
-  const bool same = (Y == X);
-  if (same && S->ident) return;
-  uint64_t bx = 0, by = 0;
-  for (int k = 0; k < nouter; ++k) {
-    bx |= ((X >> k) & 1ull) << S->opos[k];
-    by |= ((Y >> k) & 1ull) << S->opos[k];
-  }
-  double2* sx = sm + (size_t)warp * 2 * tile;
-  double2* sy = sx + tile;
-  const int w = S->w;
+  const uint64_t nunits = 1ull << S.nouter;
+  const int lane = threadIdx.x & 31;
+  const uint32_t e0 = threadIdx.x;
+  const int per = tile > 256 ? (int)(tile >> 8) : 1;
+  const bool active = e0 < tile;
   const uint32_t wmask = (1u << w) - 1;
-  for (uint32_t e = lane; e < tile; e += 32) {
-    uint64_t off = e & wmask;
-    for (int b = w; b < nv; ++b) off |= (uint64_t)((e >> b) & 1u) << S->vpos[b];
-    sx[e] = ld_g(state + bx + off);
-    if (!same) sy[e] = ld_g(state + by + off);
+  uint64_t off[4];
+  uint32_t pe[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const uint32_t e = e0 + 256u * m;
+    uint64_t o = e & wmask;
+    for (int b = w; b < nv; ++b) o |= (uint64_t)((e >> b) & 1u) << S.vpos[b];
+    off[m] = o;
+    uint32_t q = e;
+    for (int k = 0; k < S.nvp; ++k) {
+      const uint32_t d = ((q >> S.va[k]) ^ (q >> S.vb[k])) & 1u;
+      q ^= (d << S.va[k]) | (d << S.vb[k]);
+    }
+    pe[m] = q;
   }
-  __syncwarp();
-  const int nvp = S->nvp;
-  for (uint32_t e = lane; e < tile; e += 32) {
-    uint64_t off = e & wmask;
-    for (int b = w; b < nv; ++b) off |= (uint64_t)((e >> b) & 1u) << S->vpos[b];
-    uint32_t pe = e;
-    for (int p = 0; p < nvp; ++p) {
-      const uint32_t d = ((pe >> S->va[p]) ^ (pe >> S->vb[p])) & 1u;
-      pe ^= (d << S->va[p]) | (d << S->vb[p]);
+  for (uint64_t X = blockIdx.x; X < nunits; X += gridDim.x) {
+    uint64_t c = 0;
+    if (lane < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane]) ^ (X >> S.ob[lane])) & 1ull;
+      c = (d << S.oa[lane]) | (d << S.ob[lane]);
     }
-    if (same) {
-      st_g(state + bx + off, sx[pe]);
-    } else {
-      st_g(state + bx + off, sy[pe]);
-      st_g(state + by + off, sx[pe]);
+    if (lane + 32 < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane + 32]) ^ (X >> S.ob[lane + 32])) & 1ull;
+      c |= (d << S.oa[lane + 32]) | (d << S.ob[lane + 32]);
     }
+    const uint64_t Y = X ^ warp_or64(c);
+    if (Y < X) continue;
+    const bool same = (Y == X);
+    if (same && S.ident) continue;
+    uint64_t cx = 0, cy = 0;
+    if (lane < S.nouter) {
+      cx = ((X >> lane) & 1ull) << S.opos[lane];
+      cy = ((Y >> lane) & 1ull) << S.opos[lane];
+    }
+    if (lane + 32 < S.nouter) {
+      cx |= ((X >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+      cy |= ((Y >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+    }
+    const uint64_t bx = warp_or64(cx), by = warp_or64(cy);
+    double2 a[4], b[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m < per && active) {
+        a[m] = ld_g(state + bx + off[m]);
+        if (!same) b[m] = ld_g(state + by + off[m]);
+      }
+    }
+    if (S.ident) {
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (m < per && active) {
+          st_g(state + bx + off[m], b[m]);
+          st_g(state + by + off[m], a[m]);
+        }
+      }
+      continue;
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m < per && active) {
+        sm[e0 + 256u * m] = a[m];
+        if (!same) sm[tile + e0 + 256u * m] = b[m];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m < per && active) {
+        if (same) {
+          st_g(state + bx + off[m], sm[pe[m]]);
+        } else {
+          st_g(state + bx + off[m], sm[tile + pe[m]]);
+          st_g(state + by + off[m], sm[pe[m]]);
+        }
+      }
+    }
+    __syncthreads();
   }
 }
 
-int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream) {
+int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* /*d*/, CUstream_st* stream) {
   const uint64_t units = 1ull << h->nouter;
-  const size_t smem = (size_t)kSqsWarps * 2 * (16u << h->nv);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_sqs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSqsWarps * 2 * (16 << (2 * kSqsW)));
-    attr_set = true;
-  }
-  const uint64_t per_launch = (1ull << 30) * kSqsWarps;
-  for (uint64_t base = 0; base < units; base += per_launch) {
-    const uint64_t u = (units - base) < per_launch ? (units - base) : per_launch;
-    const unsigned grid = (unsigned)((u + kSqsWarps - 1) / kSqsWarps);
-    k_sqs<<<grid, 32 * kSqsWarps, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-        reinterpret_cast<double2*>(state), d, base);
-  }
+  const size_t smem = h->ident ? 0 : (size_t)2 * (16u << h->nv);
+  uint64_t grid = 148ull * 6;
+  if (grid > units) grid = units;
+  k_sqs<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<double2*>(state), *h);
   return (int)cudaGetLastError();
 }
 
@@ -522,15 +563,14 @@ int launch_gather_logical(const double* state, const int* perm, int n, uint64_t 
   return (int)cudaGetLastError();
 }
 
+__global__ void k_set_one(double2* s) { s[0] = make_double2(1.0, 0.0); }
+
 int launch_fill_zero_one(double* state, uint64_t n, int set_first, CUstream_st* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(state, 0, n * 16, s);
   if (e != cudaSuccess) return (int)e;
-  if (set_first) {
-    static const double one[2] = {1.0, 0.0};
-    e = cudaMemcpyAsync(state, one, 16, cudaMemcpyHostToDevice, s);
-  }
-  return (int)e;
+  if (set_first) k_set_one<<<1, 1, 0, s>>>(reinterpret_cast<double2*>(state));
+  return (int)cudaGetLastError();
 }
 
 }  // namespace qk

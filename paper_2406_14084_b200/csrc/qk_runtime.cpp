@@ -5,6 +5,8 @@
 // load (gate blocks -> passes/phases/ops + diagonal tables; SQS/CSQS -> tile
 // permutation descriptors), and replays them with asynchronous launches on one
 // stream per handle (Simulator.run, simulator.py:529-555).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -695,12 +697,28 @@ int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>
   std::vector<int> A = A0, B = B0;
   std::sort(A.begin(), A.end());
   std::sort(B.begin(), B.end());
+  int partner[64];
+  for (int& x : partner) x = -1;
+  for (size_t k = 0; k < A.size(); ++k) {
+    partner[A[k]] = B[k];
+    partner[B[k]] = A[k];
+  }
   const int w = std::min(kSqsW, nbits);
   std::vector<int> V;
+  auto inV = [&](int p) { return std::find(V.begin(), V.end(), p) != V.end(); };
   for (int p = 0; p < w; ++p) V.push_back(p);
-  for (size_t k = 0; k < A.size(); ++k) {
-    if (A[k] < w && B[k] >= w) V.push_back(B[k]);
-    if (B[k] < w && A[k] >= w) V.push_back(A[k]);
+  for (int p = 0; p < w; ++p)
+    if (partner[p] >= w) V.push_back(partner[p]);
+  // fillers: grow the tile to >= 2^8 amplitudes (<= 2^10), keeping pairs whole
+  const int target = std::min(nbits, 8);
+  for (int q = w; q < nbits && (int)V.size() < target; ++q) {
+    if (inV(q)) continue;
+    if (partner[q] < 0) {
+      V.push_back(q);
+    } else if (!inV(partner[q]) && V.size() + 2 <= 10) {
+      V.push_back(q);
+      V.push_back(partner[q]);
+    }
   }
   std::sort(V.begin() + w, V.end());
   SqsDesc sd{};
@@ -709,14 +727,13 @@ int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>
   for (int b = 0; b < sd.nv; ++b) sd.vpos[b] = (uint8_t)V[b];
   std::vector<int> O;
   for (int p = 0; p < nbits; ++p)
-    if (std::find(V.begin(), V.end(), p) == V.end()) O.push_back(p);
+    if (!inV(p)) O.push_back(p);
   sd.nouter = (int)O.size();
   for (size_t k = 0; k < O.size(); ++k) sd.opos[k] = (uint8_t)O[k];
   auto vidx = [&](int p) { return (int)(std::find(V.begin(), V.end(), p) - V.begin()); };
   auto oidx = [&](int p) { return (int)(std::find(O.begin(), O.end(), p) - O.begin()); };
   for (size_t k = 0; k < A.size(); ++k) {
-    const bool ain = std::find(V.begin(), V.end(), A[k]) != V.end();
-    if (ain) {
+    if (inV(A[k])) {
       sd.va[sd.nvp] = (uint8_t)vidx(A[k]);
       sd.vb[sd.nvp] = (uint8_t)vidx(B[k]);
       ++sd.nvp;
@@ -794,10 +811,18 @@ struct qk_sim {
   size_t scratch_bytes = 0;
   // timing
   std::vector<cudaEvent_t> events;
+  cudaEvent_t marks[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int per_launch = 0;
   double stat_ms[3] = {0, 0, 0};
   double stat_launch[3] = {0, 0, 0};
   double stat_bytes[3] = {0, 0, 0};
+  // persistent TMA passes
+  int num_sms = 148;
+  bool allow_tma = true;
+  CUtensorMap maps[6];
+  bool map_ok[6] = {false, false, false, false, false, false};
+  std::vector<TmaParams> tma;
+  std::vector<int> pass_tma;
   // multi-process
   qk_barrier_fn barrier = nullptr;
   void* barrier_ctx = nullptr;
@@ -823,6 +848,92 @@ size_t push_section(std::vector<char>& buf, const std::vector<T>& v) {
   buf.resize(off + v.size() * sizeof(T));
   if (!v.empty()) memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
   return off;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D view of the state: rows of 8 amplitudes (16 doubles = 128 B), SWIZZLE_128B
+const CUtensorMap* state_map(qk_sim* s, int box_rows) {
+  const int slot = __builtin_ctz((unsigned)box_rows) - 3;  // 8..256 -> 0..5
+  if (slot < 0 || slot > 5) return nullptr;
+  if (!s->map_ok[slot]) {
+    auto fn = encode_fn();
+    if (!fn || s->nbits < 3) return nullptr;
+    cuuint64_t dims[2] = {16, (cuuint64_t)1 << (s->nbits - 3)};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(&s->maps[slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, s->state, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return nullptr;
+    s->map_ok[slot] = true;
+  }
+  return &s->maps[slot];
+}
+
+bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp) {
+  if (getenv("QK_NO_TMA")) return false;
+  if (pd.M != 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || s->nbits > 34) return false;
+  if (pd.nouter != s->nbits - pd.C) return false;
+  for (int k = 0; k < pd.nouter; ++k)
+    if (pd.opos[k] != pd.C + k) return false;
+  const HostPlan& hp = s->hp;
+  const int ob = hp.phases[pd.phase0].op_begin;
+  const int oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
+  if (oe - ob > kTMaxOps) return false;
+  const int box_rows = std::min(256, 1 << (pd.C - 3));
+  const CUtensorMap* map = state_map(s, box_rows);
+  if (!map) return false;
+  memset(&tp, 0, sizeof tp);
+  tp.map = *map;
+  tp.tabs = s->d_pool;
+  tp.nchunks = 1ull << (s->nbits - pd.C);
+  tp.C = pd.C;
+  tp.nphases = pd.nphases;
+  tp.box_rows = box_rows;
+  tp.ntma = (1 << (pd.C - 3)) / box_rows;
+  if (tma_smem_bytes(pd.C, &tp.ng, &tp.stages) < 0) return false;
+  int ncoef = 0;
+  for (int ph = 0; ph < pd.nphases; ++ph) {
+    const PhaseDesc& D = hp.phases[pd.phase0 + ph];
+    TPhase& T = tp.ph[ph];
+    T.op_begin = (int16_t)(D.op_begin - ob);
+    T.op_end = (int16_t)(D.op_end - ob);
+    for (int k = 0; k < 12; ++k) T.tpos[k] = D.tpos[k];
+    for (int j = 0; j < 16; ++j) T.rloc[j] = D.rloc[j];
+  }
+  for (int o = ob; o < oe; ++o) {
+    const OpDesc& op = hp.ops[o];
+    TOp& t = tp.ops[o - ob];
+    t.code = (int8_t)op.code;
+    t.r0 = (int8_t)op.r0;
+    t.r1 = (int8_t)op.r1;
+    t.creg = (int8_t)op.ctrl_reg;
+    t.ctrl = (int16_t)op.ctrl;
+    if (op.table > INT32_MAX) return false;
+    t.table = (int32_t)op.table;
+    for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
+    for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
+    const int nc = op.code == OP_MAT ? 8 : (op.code == OP_SCALE ? 1 : 0);
+    if (nc) {
+      if (ncoef + nc > kTMaxCoef) return false;
+      for (int q = 0; q < nc; ++q) tp.coef[ncoef + q] = hp.coef[op.coef + q];
+      t.coef = (int16_t)ncoef;
+      ncoef += nc;
+    }
+  }
+  return true;
 }
 
 int upload_plan(qk_sim* s) {
@@ -858,6 +969,15 @@ int upload_plan(qk_sim* s) {
     s->pool_bytes = 0;
     CUDA_TRY(cudaMalloc(&s->d_pool, pool_bytes));
     s->pool_bytes = pool_bytes;
+  }
+  s->tma.clear();
+  s->pass_tma.assign(hp.passes.size(), -1);
+  for (size_t p = 0; p < hp.passes.size(); ++p) {
+    TmaParams tp;
+    if (make_tma(s, hp.passes[p], tp)) {
+      s->pass_tma[p] = (int)s->tma.size();
+      s->tma.push_back(tp);
+    }
   }
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
@@ -955,6 +1075,11 @@ int ensure_events(qk_sim* s, size_t n) {
 }
 
 int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
+  if (s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0) {
+    int rc = launch_block_tma(&s->tma[s->pass_tma[p]], s->num_sms, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "tma block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+    return QK_OK;
+  }
   PassDesc h = s->hp.passes[p];
   if (count_override) h.ncta = count_override;
   int rc = launch_block_pass(s->state, &h, s->d_pass + p, s->d_phase, s->d_ops, s->d_coef, s->d_pool, first,
@@ -1110,6 +1235,7 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
     return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
   }
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaMalloc(&s->d_partial, 148 * 8 * sizeof(double) + 256));
   s->d_scalar = s->d_partial + 148 * 8;
   int rc = launch_fill_zero_one(s->state, s->amps, rank_lo == 0, (CUstream_st*)s->stream);
@@ -1200,6 +1326,8 @@ int qk_destroy(qk_sim* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto e : s->events) cudaEventDestroy(e);
+  for (auto e : s->marks)
+    if (e) cudaEventDestroy(e);
   for (size_t i = 0; i < s->peers.size(); ++i)
     if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
   if (s->state) cudaFree(s->state);
@@ -1515,7 +1643,9 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
   if (!rc && !s->hp.passes.empty()) {
     double* saved = s->state;
     s->state = s->state + 2 * ((uint64_t)part << s->L);
+    s->allow_tma = false;
     rc = launch_pass(s, 0, row_start, row_stop - row_start);
+    s->allow_tma = true;
     s->state = saved;
     if (!rc) {
       cudaError_t e = cudaStreamSynchronize(s->stream);
@@ -1662,6 +1792,24 @@ int qk_set_barrier(qk_sim* s, qk_barrier_fn fn, void* ctx) {
   if (!s) return fail(QK_EINVAL, "null handle");
   s->barrier = fn;
   s->barrier_ctx = ctx;
+  return QK_OK;
+}
+
+int qk_mark(qk_sim* s, int slot) {
+  if (!s || slot < 0 || slot >= 8) return fail(QK_EINVAL, "bad marker slot");
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (!s->marks[slot]) CUDA_TRY(cudaEventCreate(&s->marks[slot]));
+  CUDA_TRY(cudaEventRecord(s->marks[slot], s->stream));
+  return QK_OK;
+}
+
+int qk_mark_elapsed(qk_sim* s, int a, int b, double* ms) {
+  if (!s || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !s->marks[a] || !s->marks[b])
+    return fail(QK_EINVAL, "bad marker slots");
+  CUDA_TRY(cudaEventSynchronize(s->marks[b]));
+  float f = 0;
+  CUDA_TRY(cudaEventElapsedTime(&f, s->marks[a], s->marks[b]));
+  *ms = f;
   return QK_OK;
 }
 

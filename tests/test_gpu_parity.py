@@ -186,6 +186,8 @@ KINDS = ["H", "X", "U", "CX", "CP", "SWAP", "RX", "RY", "RZ", "RZZ", "D"]
 
 def _random_gate(rng, c, gid):
     kind = KINDS[rng.integers(0, len(KINDS))]
+    if kind == "D" and c < 2:
+        kind = "RZ"
     if kind == "D":
         k = int(rng.integers(2, min(c, 6) + 1))
         t = tuple(int(x) for x in np.sort(rng.choice(c, size=k, replace=False)))
@@ -229,7 +231,7 @@ def test_random_streams_vs_oracle(gpu, seed):
     L = n - r
     c = int(rng.integers(1, min(L, 13) + 1))
     b = int(rng.integers(min(r, L), L + 1)) if r else L
-    layout = LayoutParams(n=n, c=L, r=r, b=b)
+    layout = LayoutParams(n=n, c=L, r=r, cl=min(2, L), b=b)
     ins = _random_stream(rng, n, r, c, int(rng.integers(1, 16)))
     opt = OptimizedCircuit(n, layout, ins)
     text = serialize_optimized(opt)
