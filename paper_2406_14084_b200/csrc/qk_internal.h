@@ -93,10 +93,16 @@ constexpr int kTMaxPh = 12;
 constexpr int kTMaxOps = 64;
 constexpr int kTMaxCoef = 128;
 
+// step of a TMA phase program. OP_H/OP_X/OP_MAT never appear as steps:
+// consecutive one-qubit gates on distinct register slots are fused into one
+// STEP_1Q (slot s gets kind st[s]: 0 none, 1 H butterfly, 2 X, 3 matrix coef[cf[s]]).
+constexpr int STEP_1Q = 16;
 struct TOp {
   int8_t code, r0, r1, creg;
   int16_t ctrl, coef;
   int32_t table;
+  int8_t st[4];
+  int16_t cf[4];
   uint16_t tcontrib[12];
   uint16_t pr[16];
 };
@@ -110,8 +116,16 @@ struct TPhase {
 struct alignas(64) TmaParams {
   CUtensorMap map;              // 2-D view {16 doubles, rows} of the state, SWIZZLE_128B
   const double* tabs;           // diagonal table pool
+  double* state;                // buffer read by the TMA loads (and written when not permuted)
+  double* out;                  // buffer the last phase writes (== state unless permuted)
   uint64_t nchunks;
-  int32_t C, nphases, box_rows, ntma, ng, stages;
+  int32_t C, M, nphases, box_rows, ntma, ng, stages;
+  int32_t direct_store;         // 1: last phase stores with STG.128, 0: TMA bulk store
+  int32_t permuted;             // 1: last phase scatters to the post-SQS positions (out-of-place)
+  int32_t nbits;
+  uint8_t dpos[64];             // destination bit of every source address bit (permuted)
+  uint64_t ldst_t[12];          // last phase: thread bit k -> destination offset
+  uint64_t ldst_r[16];          // last phase: register amplitude j -> destination offset
   TPhase ph[kTMaxPh];
   TOp ops[kTMaxOps];
   double coef[kTMaxCoef];
@@ -126,7 +140,7 @@ int launch_block_pass(double* state, const PassDesc* h_pass, const PassDesc* d_p
                       const PhaseDesc* d_phases, const OpDesc* d_ops, const double* d_coef,
                       const double* d_tables, uint64_t first, CUstream_st* stream);
 int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream);
-int tma_smem_bytes(int C, int* ng, int* stages);
+int tma_smem_bytes(int C, int M, int* ng, int* stages);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);

@@ -376,19 +376,20 @@ __global__ void __launch_bounds__(256) k_sqs(double2* __restrict__ state, const 
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       if (m < per && active) {
-        sm[e0 + 256u * m] = a[m];
-        if (!same) sm[tile + e0 + 256u * m] = b[m];
+        sm[swz(e0 + 256u * m)] = a[m];
+        if (!same) sm[tile + swz(e0 + 256u * m)] = b[m];
       }
     }
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       if (m < per && active) {
+        const uint32_t q = swz(pe[m]);
         if (same) {
-          st_g(state + bx + off[m], sm[pe[m]]);
+          st_g(state + bx + off[m], sm[q]);
         } else {
-          st_g(state + bx + off[m], sm[tile + pe[m]]);
-          st_g(state + by + off[m], sm[pe[m]]);
+          st_g(state + bx + off[m], sm[tile + q]);
+          st_g(state + by + off[m], sm[q]);
         }
       }
     }

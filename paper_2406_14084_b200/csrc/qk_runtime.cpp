@@ -357,6 +357,9 @@ struct HostPlan {
 struct InstrPlan {
   int type;
   int pass0 = 0, npass = 0;  // block
+  std::vector<int> dest;     // block: destination bit of each source bit (fused SQS), empty if none
+  int permuted = 0;          // block: last pass scatters out-of-place (set at upload)
+  int fused_by = -1;         // SQS/CSQS: index of the block whose last pass absorbs it
   int sqs = -1;              // SQS / single-device CSQS
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
@@ -392,9 +395,10 @@ struct Item {
 // Compile the gates of one pass over chunk address bits Q (ascending) of a
 // vector of `nbits` address bits.
 int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std::vector<int>& Q,
-                 int nbits, uint64_t ncta_override, std::string& emsg) {
+                 int nbits, uint64_t ncta_override, std::string& emsg, const std::vector<int>* dest = nullptr) {
   const int C = (int)Q.size();
-  const int M = std::min(kMaxM, C);
+  int M = std::min(kMaxM, C);
+  if (C >= 9 && C <= 12 && Q.back() == C - 1 && getenv("QK_M")) M = std::max(3, std::min(4, atoi(getenv("QK_M"))));
   int loc[64];
   for (int& x : loc) x = -1;
   for (int l = 0; l < C; ++l) loc[Q[l]] = l;
@@ -535,7 +539,12 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     std::vector<int> T;
     for (int p = 0; p < C; ++p)
       if (std::find(pb.R.begin(), pb.R.end(), p) == pb.R.end()) T.push_back(p);
-    T = order_tpos(T);
+    if (dest && ph + 1 == phs.size()) {
+      // last phase of a fused pass: lanes on the source bits that land lowest
+      std::stable_sort(T.begin(), T.end(), [&](int x, int y) { return (*dest)[Q[x]] < (*dest)[Q[y]]; });
+    } else {
+      T = order_tpos(T);
+    }
     PhaseDesc D{};
     D.tbits = C - M;
     for (int k = 0; k < D.tbits; ++k) {
@@ -641,8 +650,21 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
 // fits kMaxC (chunk-local path, simulator.py:481-492); otherwise gates are
 // grouped into memory-level passes whose Q = targets + lowest free bits
 // (simulator.py:494-511, same per-amplitude gate order).
+// chunk width of a block's single pass (0 if the block needs memory-level passes)
+int block_chunk_width(const InstrH& ins, int L, int cmin = 10) {
+  int maxt = -1;
+  for (auto& g : ins.gates)
+    for (int t : g.t) maxt = std::max(maxt, t);
+  if (maxt < 0 || maxt >= kMaxC || maxt >= L) return 0;
+  int C = std::max(maxt + 1, std::min(L, cmin));
+  C = std::min(C, std::min(L, kMaxC));
+  if (C > 12 && maxt < 12) C = 12;
+  return C;
+}
+
 int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& ip,
                   std::string& emsg, int cmin = 10) {
+  const std::vector<int>* dest = ip.dest.empty() ? nullptr : &ip.dest;
   int maxt = -1;
   for (auto& g : ins.gates)
     for (int t : g.t) maxt = std::max(maxt, t);
@@ -654,14 +676,12 @@ int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& 
   }
   const int low_keep = std::min(3, L);
   if (maxt < kMaxC) {
-    int C = std::max(maxt + 1, std::min(L, cmin));
-    C = std::min(C, std::min(L, kMaxC));
-    if (C > 12 && maxt < 12) C = 12;
+    const int C = block_chunk_width(ins, L, cmin);
     std::vector<int> Q;
     for (int p = 0; p < C; ++p) Q.push_back(p);
     std::vector<const GateH*> gs;
     for (auto& g : ins.gates) gs.push_back(&g);
-    int rc = compile_pass(hp, gs, Q, nbits, 0, emsg);
+    int rc = compile_pass(hp, gs, Q, nbits, 0, emsg, dest);
     if (rc) return rc;
   } else {
     size_t i = 0;
@@ -709,8 +729,8 @@ int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>
   for (int p = 0; p < w; ++p) V.push_back(p);
   for (int p = 0; p < w; ++p)
     if (partner[p] >= w) V.push_back(partner[p]);
-  // fillers: grow the tile to >= 2^8 amplitudes (<= 2^10), keeping pairs whole
-  const int target = std::min(nbits, 8);
+  // fillers: grow the tile to 2^10 amplitudes, keeping pairs whole
+  const int target = std::min(nbits, 10);
   for (int q = w; q < nbits && (int)V.size() < target; ++q) {
     if (inV(q)) continue;
     if (partner[q] < 0) {
@@ -786,7 +806,9 @@ struct qk_sim {
   int n = 0, r = 0, b = 0, device = 0;
   int rank_lo = 0, count = 1;
   int L = 0, nbits = 0;  // local qubits, address bits held by this handle
-  double* state = nullptr;
+  double* state = nullptr;      // == bufs[cur]
+  double* bufs[2] = {nullptr, nullptr};  // bufs[1]: out-of-place target of fused passes
+  int cur = 0;
   size_t amps = 0;
   cudaStream_t stream = nullptr;
   // program
@@ -819,8 +841,8 @@ struct qk_sim {
   // persistent TMA passes
   int num_sms = 148;
   bool allow_tma = true;
-  CUtensorMap maps[6];
-  bool map_ok[6] = {false, false, false, false, false, false};
+  CUtensorMap maps[2][6];
+  bool map_ok[2][6] = {{false, false, false, false, false, false}, {false, false, false, false, false, false}};
   std::vector<TmaParams> tma;
   std::vector<int> pass_tma;
   // multi-process
@@ -863,75 +885,107 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D view of the state: rows of 8 amplitudes (16 doubles = 128 B), SWIZZLE_128B
-const CUtensorMap* state_map(qk_sim* s, int box_rows) {
+const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
   const int slot = __builtin_ctz((unsigned)box_rows) - 3;  // 8..256 -> 0..5
-  if (slot < 0 || slot > 5) return nullptr;
-  if (!s->map_ok[slot]) {
+  if (slot < 0 || slot > 5 || !s->bufs[buf]) return nullptr;
+  if (!s->map_ok[buf][slot]) {
     auto fn = encode_fn();
     if (!fn || s->nbits < 3) return nullptr;
     cuuint64_t dims[2] = {16, (cuuint64_t)1 << (s->nbits - 3)};
     cuuint64_t strides[1] = {128};
     cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
     cuuint32_t es[2] = {1, 1};
-    CUresult r = fn(&s->maps[slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, s->state, dims, strides, box, es,
+    CUresult r = fn(&s->maps[buf][slot], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, s->bufs[buf], dims, strides, box, es,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return nullptr;
-    s->map_ok[slot] = true;
+    s->map_ok[buf][slot] = true;
   }
-  return &s->maps[slot];
+  return &s->maps[buf][slot];
 }
 
-bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp) {
+bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<int>* dest) {
   if (getenv("QK_NO_TMA")) return false;
-  if (pd.M != 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || s->nbits > 34) return false;
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || s->nbits > 34) return false;
   if (pd.nouter != s->nbits - pd.C) return false;
   for (int k = 0; k < pd.nouter; ++k)
     if (pd.opos[k] != pd.C + k) return false;
   const HostPlan& hp = s->hp;
-  const int ob = hp.phases[pd.phase0].op_begin;
-  const int oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
-  if (oe - ob > kTMaxOps) return false;
   const int box_rows = std::min(256, 1 << (pd.C - 3));
-  const CUtensorMap* map = state_map(s, box_rows);
-  if (!map) return false;
+  if (!state_map(s, 0, box_rows)) return false;
   memset(&tp, 0, sizeof tp);
-  tp.map = *map;
   tp.tabs = s->d_pool;
+  tp.direct_store = (getenv("QK_TMA_STORE") && !dest) ? 0 : 1;
+  tp.nbits = s->nbits;
+  if (dest) {
+    tp.permuted = 1;
+    for (int q = 0; q < s->nbits; ++q) tp.dpos[q] = (uint8_t)(*dest)[q];
+    const PhaseDesc& D = s->hp.phases[pd.phase0 + pd.nphases - 1];
+    for (int k = 0; k < D.tbits; ++k) tp.ldst_t[k] = 1ull << (*dest)[D.tpos[k]];
+    for (int j = 0; j < (1 << pd.M); ++j) {
+      uint64_t o = 0;
+      for (int b = 0; b < pd.C; ++b)
+        if (D.rloc[j] >> b & 1) o |= 1ull << (*dest)[b];
+      tp.ldst_r[j] = o;
+    }
+  }
   tp.nchunks = 1ull << (s->nbits - pd.C);
   tp.C = pd.C;
+  tp.M = pd.M;
   tp.nphases = pd.nphases;
   tp.box_rows = box_rows;
   tp.ntma = (1 << (pd.C - 3)) / box_rows;
-  if (tma_smem_bytes(pd.C, &tp.ng, &tp.stages) < 0) return false;
-  int ncoef = 0;
+  if (tma_smem_bytes(pd.C, pd.M, &tp.ng, &tp.stages) < 0) return false;
+  int ncoef = 0, nsteps = 0;
   for (int ph = 0; ph < pd.nphases; ++ph) {
     const PhaseDesc& D = hp.phases[pd.phase0 + ph];
     TPhase& T = tp.ph[ph];
-    T.op_begin = (int16_t)(D.op_begin - ob);
-    T.op_end = (int16_t)(D.op_end - ob);
     for (int k = 0; k < 12; ++k) T.tpos[k] = D.tpos[k];
     for (int j = 0; j < 16; ++j) T.rloc[j] = D.rloc[j];
-  }
-  for (int o = ob; o < oe; ++o) {
-    const OpDesc& op = hp.ops[o];
-    TOp& t = tp.ops[o - ob];
-    t.code = (int8_t)op.code;
-    t.r0 = (int8_t)op.r0;
-    t.r1 = (int8_t)op.r1;
-    t.creg = (int8_t)op.ctrl_reg;
-    t.ctrl = (int16_t)op.ctrl;
-    if (op.table > INT32_MAX) return false;
-    t.table = (int32_t)op.table;
-    for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
-    for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
-    const int nc = op.code == OP_MAT ? 8 : (op.code == OP_SCALE ? 1 : 0);
-    if (nc) {
-      if (ncoef + nc > kTMaxCoef) return false;
-      for (int q = 0; q < nc; ++q) tp.coef[ncoef + q] = hp.coef[op.coef + q];
-      t.coef = (int16_t)ncoef;
-      ncoef += nc;
+    T.op_begin = (int16_t)nsteps;
+    TOp* cur1q = nullptr;  // open STEP_1Q (one-qubit gates on distinct slots commute)
+    for (int o = D.op_begin; o < D.op_end; ++o) {
+      const OpDesc& op = hp.ops[o];
+      const bool one_q = op.code == OP_H || op.code == OP_X || op.code == OP_MAT;
+      if (one_q && cur1q && cur1q->st[op.r0] == 0) {
+        // joins the open step
+      } else {
+        if (nsteps >= kTMaxOps) return false;
+        TOp& t = tp.ops[nsteps++];
+        memset(&t, 0, sizeof t);
+        cur1q = nullptr;
+        if (one_q) {
+          t.code = STEP_1Q;
+          cur1q = &t;
+        } else {
+          t.code = (int8_t)op.code;
+          t.r0 = (int8_t)op.r0;
+          t.r1 = (int8_t)op.r1;
+          t.creg = (int8_t)op.ctrl_reg;
+          t.ctrl = (int16_t)op.ctrl;
+          if (op.table > INT32_MAX) return false;
+          t.table = (int32_t)op.table;
+          for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
+          for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
+          if (op.code == OP_SCALE) {
+            if (ncoef + 1 > kTMaxCoef) return false;
+            tp.coef[ncoef] = hp.coef[op.coef];
+            t.coef = (int16_t)ncoef++;
+          }
+        }
+      }
+      if (one_q) {
+        const int sl = op.r0;
+        cur1q->st[sl] = op.code == OP_H ? 1 : (op.code == OP_X ? 2 : 3);
+        if (op.code == OP_MAT) {
+          if (ncoef + 8 > kTMaxCoef) return false;
+          for (int q = 0; q < 8; ++q) tp.coef[ncoef + q] = hp.coef[op.coef + q];
+          cur1q->cf[sl] = (int16_t)ncoef;
+          ncoef += 8;
+        }
+      }
     }
+    T.op_end = (int16_t)nsteps;
   }
   return true;
 }
@@ -972,13 +1026,21 @@ int upload_plan(qk_sim* s) {
   }
   s->tma.clear();
   s->pass_tma.assign(hp.passes.size(), -1);
+  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr);
+  for (auto& ip : s->iplan) {
+    ip.permuted = 0;
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) pass_dest[ip.pass0 + ip.npass - 1] = &ip.dest;
+  }
   for (size_t p = 0; p < hp.passes.size(); ++p) {
     TmaParams tp;
-    if (make_tma(s, hp.passes[p], tp)) {
+    if (make_tma(s, hp.passes[p], tp, pass_dest[p])) {
       s->pass_tma[p] = (int)s->tma.size();
       s->tma.push_back(tp);
     }
   }
+  for (auto& ip : s->iplan)
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty())
+      ip.permuted = s->pass_tma[ip.pass0 + ip.npass - 1] >= 0;
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
                                  (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
@@ -1026,10 +1088,56 @@ int compile_program(qk_sim* s) {
   s->hp.clear();
   s->iplan.clear();
   std::string emsg;
-  for (auto& ins : s->prog) {
+  // fusion pre-scan: with a second buffer, every run of SQS (and on-device
+  // CSQS) right after a gate block becomes that block's output permutation
+  std::vector<std::vector<int>> dest(s->prog.size());
+  std::vector<int> fused_by(s->prog.size(), -1);
+  if (s->bufs[1] && !getenv("QK_NO_FUSE")) {
+    const int held_rank_bits = s->nbits - s->L;
+    for (size_t i = 0; i < s->prog.size(); ++i) {
+      if (s->prog[i].type != QK_INS_BLOCK || s->prog[i].gates.empty()) continue;
+      std::vector<int> pos(s->nbits), fuse_pos;
+      for (int q = 0; q < s->nbits; ++q) pos[q] = q;
+      size_t j = i + 1;
+      for (; j < s->prog.size(); ++j) {
+        const InstrH& nx = s->prog[j];
+        if (nx.type == QK_INS_BLOCK || nx.a.empty()) break;
+        bool ok = true;
+        for (int q : nx.a) ok = ok && q >= 0 && q < s->nbits;
+        for (int q : nx.b) ok = ok && q >= 0 && q < s->nbits && (nx.type == QK_INS_SQS || q - s->L < held_rank_bits);
+        if (nx.type == QK_INS_SQS)
+          for (int q : nx.b) ok = ok && q < s->L;
+        if (nx.type == QK_INS_CSQS && check_csqs(s, nx.a, nx.b) != QK_OK) ok = false;
+        if (!ok) break;
+        std::vector<int> a = nx.a, b = nx.b;
+        std::sort(a.begin(), a.end());
+        std::sort(b.begin(), b.end());
+        for (int q = 0; q < s->nbits; ++q)
+          for (size_t k = 0; k < a.size(); ++k) {
+            if (pos[q] == a[k]) { pos[q] = b[k]; break; }
+            if (pos[q] == b[k]) { pos[q] = a[k]; break; }
+          }
+        // keep the fusion only while the 5 lowest destination bits still come
+        // from chunk bits: every warp then stores whole 512-B runs. Swaps that
+        // move low bits out of the chunk are left to the tiled SQS kernel.
+        bool coalesced = true;
+        const int cw = block_chunk_width(s->prog[i], s->L);
+        for (int q = 0; q < s->nbits; ++q)
+          if (pos[q] < 5 && q >= cw) coalesced = false;
+        if (!coalesced) break;
+        fused_by[j] = (int)i;
+        fuse_pos = pos;
+      }
+      if (j > i + 1 && !fuse_pos.empty()) dest[i] = fuse_pos;
+    }
+  }
+  for (size_t ii = 0; ii < s->prog.size(); ++ii) {
+    auto& ins = s->prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
+    ip.fused_by = fused_by[ii];
     if (ins.type == QK_INS_BLOCK) {
+      ip.dest = dest[ii];
       int rc = compile_block(s->hp, ins, s->L, s->nbits, ip, emsg);
       if (rc) return fail(rc, "%s", emsg.c_str());
     } else if (ins.type == QK_INS_SQS) {
@@ -1062,6 +1170,28 @@ int compile_program(qk_sim* s) {
     s->iplan.push_back(std::move(ip));
   }
   replay_perm(s);
+  if (getenv("QK_DUMP_PLAN")) {
+    int bi = 0;
+    for (auto& ip : s->iplan) {
+      if (ip.type == QK_INS_BLOCK) {
+        for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
+          const PassDesc& pd = s->hp.passes[p];
+          int cnt[8] = {0};
+          for (int ph = 0; ph < pd.nphases; ++ph) {
+            const PhaseDesc& D = s->hp.phases[pd.phase0 + ph];
+            for (int o = D.op_begin; o < D.op_end; ++o) cnt[s->hp.ops[o].code]++;
+          }
+          fprintf(stderr, "block %d pass %d: C=%d M=%d phases=%d H=%d X=%d MAT=%d CX=%d SWAP=%d DIAG=%d SCALE=%d\n", bi,
+                  p, pd.C, pd.M, pd.nphases, cnt[0], cnt[1], cnt[2], cnt[3], cnt[4], cnt[5], cnt[6]);
+        }
+        ++bi;
+      } else if (ip.sqs >= 0) {
+        const SqsDesc& d = s->hp.sqs[ip.sqs];
+        fprintf(stderr, "swap: nv=%d w=%d nouter=%d in-tile=%d outer=%d\n", d.nv, d.w, d.nouter, d.nvp, d.nop);
+      }
+    }
+    for (auto& t : s->hp.tables) fprintf(stderr, "table: bits=%d gates=%d\n", t.bits, t.ng);
+  }
   return upload_plan(s);
 }
 
@@ -1076,8 +1206,18 @@ int ensure_events(qk_sim* s, size_t n) {
 
 int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
   if (s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0) {
-    int rc = launch_block_tma(&s->tma[s->pass_tma[p]], s->num_sms, (CUstream_st*)s->stream);
+    TmaParams& tp = s->tma[s->pass_tma[p]];
+    const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
+    if (!map) return fail(QK_ECUDA, "tensor map unavailable");
+    tp.map = *map;
+    tp.state = s->bufs[s->cur];
+    tp.out = tp.permuted ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
+    int rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "tma block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+    if (tp.permuted) {
+      s->cur ^= 1;
+      s->state = s->bufs[s->cur];
+    }
     return QK_OK;
   }
   PassDesc h = s->hp.passes[p];
@@ -1090,7 +1230,12 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
 
 int exchange_cross(qk_sim* s, const InstrPlan& ip);
 
+bool fused_away(const qk_sim* s, const InstrPlan& ip) {
+  return ip.fused_by >= 0 && s->iplan[ip.fused_by].permuted;
+}
+
 int run_instr(qk_sim* s, const InstrPlan& ip) {
+  if (ip.type != QK_INS_BLOCK && fused_away(s, ip)) return QK_OK;
   if (ip.type == QK_INS_BLOCK) {
     for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
       int rc = launch_pass(s, p);
@@ -1228,11 +1373,19 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   s->amps = (size_t)1 << nbits;
   s->nshards = (1 << r) / count;
   s->shard = rank_lo / count;
-  cudaError_t e = cudaMalloc(&s->state, need);
+  cudaError_t e = cudaMalloc(&s->bufs[0], need);
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete s;
     return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
+  }
+  s->state = s->bufs[0];
+  // second buffer for out-of-place fused block+SQS passes when it fits comfortably
+  if (count == (1 << r) && !getenv("QK_INPLACE") && 2.0 * (double)need <= 0.90 * (double)free_b) {
+    if (cudaMalloc(&s->bufs[1], need) != cudaSuccess) {
+      cudaGetLastError();
+      s->bufs[1] = nullptr;
+    }
   }
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -1330,7 +1483,8 @@ int qk_destroy(qk_sim* s) {
     if (e) cudaEventDestroy(e);
   for (size_t i = 0; i < s->peers.size(); ++i)
     if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
-  if (s->state) cudaFree(s->state);
+  if (s->bufs[0]) cudaFree(s->bufs[0]);
+  if (s->bufs[1]) cudaFree(s->bufs[1]);
   if (s->blob) cudaFree(s->blob);
   if (s->d_pool) cudaFree(s->d_pool);
   if (s->d_partial) cudaFree(s->d_partial);
@@ -1343,6 +1497,8 @@ int qk_destroy(qk_sim* s) {
 int qk_reset(qk_sim* s) {
   if (!s) return fail(QK_EINVAL, "null handle");
   CUDA_TRY(cudaSetDevice(s->device));
+  s->cur = 0;
+  s->state = s->bufs[0];
   int rc = launch_fill_zero_one(s->state, s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
   CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -1430,6 +1586,7 @@ int qk_run(qk_sim* s, double* timings) {
     const int c = s->iplan[i].type;
     cls[c] += ms;
     s->stat_ms[c] += ms;
+    if (fused_away(s, s->iplan[i])) continue;
     s->stat_bytes[c] += s->iplan[i].bytes;
     s->stat_launch[c] += c == QK_INS_BLOCK ? s->iplan[i].npass : (s->iplan[i].sqs != -1 ? 1 : 0);
   }

@@ -14,17 +14,16 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "qk_internal.h"
 
 namespace qk {
 namespace {
 
-constexpr int M = 4;
-constexpr int NA = 1 << M;
-constexpr int kConsumers = 256;
-constexpr int kThreads = 32 + kConsumers;
-constexpr uint32_t kSmemBudget = 196 * 1024;
+constexpr int kConsumers4 = 256;   // M = 4: 16 amplitudes per thread
+constexpr int kConsumers3 = 512;   // M = 3: 8 amplitudes per thread
+constexpr uint32_t kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -60,6 +59,9 @@ __device__ __forceinline__ void tma_store(const CUtensorMap* map, int c0, int c1
                "r"(c0), "r"(c1), "r"(su32(src))
                : "memory");
 }
+__device__ __forceinline__ void st_g_cs(double2* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -75,18 +77,25 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 
-template <int R>
-__device__ __forceinline__ void h_slot(double2 (&v)[NA]) {
+// in-place butterfly (a, b) -> (a + b, a - b) computed as s = a + b,
+// d = s - 2b (one FMA): no temporaries, so no register moves
+template <int M, int R>
+__device__ __forceinline__ void h_slot(double2 (&v)[1 << M]) {
+  constexpr int NA = 1 << M;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
     if (j & (1 << R)) continue;
-    const double2 a = v[j], b = v[j | (1 << R)];
-    v[j] = make_double2(a.x + b.x, a.y + b.y);
-    v[j | (1 << R)] = make_double2(a.x - b.x, a.y - b.y);
+    double2& a = v[j];
+    double2& b = v[j | (1 << R)];
+    a.x += b.x;
+    a.y += b.y;
+    b.x = fma(-2.0, b.x, a.x);
+    b.y = fma(-2.0, b.y, a.y);
   }
 }
-template <int R>
-__device__ __forceinline__ void x_slot(double2 (&v)[NA]) {
+template <int M, int R>
+__device__ __forceinline__ void x_slot(double2 (&v)[1 << M]) {
+  constexpr int NA = 1 << M;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
     if (j & (1 << R)) continue;
@@ -95,8 +104,9 @@ __device__ __forceinline__ void x_slot(double2 (&v)[NA]) {
     v[j | (1 << R)] = a;
   }
 }
-template <int R>
-__device__ __forceinline__ void mat_slot(double2 (&v)[NA], const double* m) {
+template <int M, int R>
+__device__ __forceinline__ void mat_slot(double2 (&v)[1 << M], const double* m) {
+  constexpr int NA = 1 << M;
   const double m00r = m[0], m00i = m[1], m01r = m[2], m01i = m[3];
   const double m10r = m[4], m10i = m[5], m11r = m[6], m11i = m[7];
 #pragma unroll
@@ -112,8 +122,9 @@ __device__ __forceinline__ void mat_slot(double2 (&v)[NA], const double* m) {
     v[j | (1 << R)] = n1;
   }
 }
-template <int R>
-__device__ __forceinline__ void cx_slot(double2 (&v)[NA], int creg, int rc, int tcond) {
+template <int M, int R>
+__device__ __forceinline__ void cx_slot(double2 (&v)[1 << M], int creg, int rc, int tcond) {
+  constexpr int NA = 1 << M;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
     if (j & (1 << R)) continue;
@@ -123,8 +134,9 @@ __device__ __forceinline__ void cx_slot(double2 (&v)[NA], int creg, int rc, int 
     v[j | (1 << R)] = cond ? a : b;
   }
 }
-template <int A, int B>
-__device__ __forceinline__ void swap_slots(double2 (&v)[NA]) {
+template <int M, int A, int B>
+__device__ __forceinline__ void swap_slots(double2 (&v)[1 << M]) {
+  constexpr int NA = 1 << M;
 #pragma unroll
   for (int j = 0; j < NA; ++j) {
     if (!((j >> A) & 1) || ((j >> B) & 1)) continue;
@@ -135,22 +147,40 @@ __device__ __forceinline__ void swap_slots(double2 (&v)[NA]) {
   }
 }
 
-#define QK_SLOT4(FN, r, ...)      \
-  switch (r) {                    \
-    case 0: FN<0>(__VA_ARGS__); break; \
-    case 1: FN<1>(__VA_ARGS__); break; \
-    case 2: FN<2>(__VA_ARGS__); break; \
-    default: FN<3>(__VA_ARGS__); break; \
+#define QK_SLOT4(FN, r, ...)                                       \
+  switch (r) {                                                     \
+    case 0: FN<M, 0>(__VA_ARGS__); break;                          \
+    case 1: FN<M, 1>(__VA_ARGS__); break;                          \
+    case 2: FN<M, 2>(__VA_ARGS__); break;                          \
+    default: if constexpr (M > 3) FN<M, 3>(__VA_ARGS__); break;    \
   }
 
-__device__ __forceinline__ void apply_ops(double2 (&v)[NA], const TmaParams& p, const TPhase& D, uint32_t tid,
+template <int M, int S>
+__device__ __forceinline__ void slot_1q(double2 (&v)[1 << M], const TOp& op, const double* coef) {
+  if constexpr (S < M) {
+    const int k = op.st[S];
+    if (k == 1) {
+      h_slot<M, S>(v);
+    } else if (k == 3) {
+      mat_slot<M, S>(v, coef + op.cf[S]);
+    } else if (k == 2) {
+      x_slot<M, S>(v);
+    }
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void apply_ops(double2 (&v)[1 << M], const TmaParams& p, const TPhase& D, uint32_t tid,
                                           int T, uint32_t loct) {
+  constexpr int NA = 1 << M;
   for (int o = D.op_begin; o < D.op_end; ++o) {
     const TOp& op = p.ops[o];
     const int code = op.code;
-    const int r0 = op.r0;
-    if (code == OP_H) {
-      QK_SLOT4(h_slot, r0, v)
+    if (code == STEP_1Q) {
+      slot_1q<M, 0>(v, op, p.coef);
+      slot_1q<M, 1>(v, op, p.coef);
+      slot_1q<M, 2>(v, op, p.coef);
+      slot_1q<M, 3>(v, op, p.coef);
     } else if (code == OP_DIAG) {
       uint32_t pt = 0;
       for (int k = 0; k < T; ++k)
@@ -158,23 +188,18 @@ __device__ __forceinline__ void apply_ops(double2 (&v)[NA], const TmaParams& p, 
       const double2* tab = reinterpret_cast<const double2*>(p.tabs) + op.table;
 #pragma unroll
       for (int j = 0; j < NA; ++j) v[j] = cmul(v[j], __ldg(tab + (pt | op.pr[j])));
-    } else if (code == OP_MAT) {
-      const double* m = p.coef + op.coef;
-      QK_SLOT4(mat_slot, r0, v, m)
-    } else if (code == OP_X) {
-      QK_SLOT4(x_slot, r0, v)
     } else if (code == OP_CX) {
       const int creg = op.creg;
       const int tcond = creg ? 0 : (int)((loct >> op.ctrl) & 1u);
-      QK_SLOT4(cx_slot, r0, v, creg, (int)op.r1, tcond)
+      QK_SLOT4(cx_slot, op.r0, v, creg, (int)op.r1, tcond)
     } else if (code == OP_SWAP) {
-      switch (r0 * 4 + op.r1) {
-        case 1: swap_slots<0, 1>(v); break;
-        case 2: swap_slots<0, 2>(v); break;
-        case 3: swap_slots<0, 3>(v); break;
-        case 6: swap_slots<1, 2>(v); break;
-        case 7: swap_slots<1, 3>(v); break;
-        default: swap_slots<2, 3>(v); break;
+      switch (op.r0 * 4 + op.r1) {
+        case 1: swap_slots<M, 0, 1>(v); break;
+        case 2: swap_slots<M, 0, 2>(v); break;
+        case 6: swap_slots<M, 1, 2>(v); break;
+        case 3: if constexpr (M > 3) swap_slots<M, 0, 3>(v); break;
+        case 7: if constexpr (M > 3) swap_slots<M, 1, 3>(v); break;
+        default: if constexpr (M > 3) swap_slots<M, 2, 3>(v); break;
       }
     } else if (code == OP_SCALE) {
       const double s = p.coef[op.coef];
@@ -184,9 +209,12 @@ __device__ __forceinline__ void apply_ops(double2 (&v)[NA], const TmaParams& p, 
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_block_tma(const __grid_constant__ TmaParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+template <int M, int NTHREADS>
+__global__ void __launch_bounds__(NTHREADS, 1) k_block_tma(const __grid_constant__ TmaParams p) {
+  constexpr int NA = 1 << M;
+  // dynamic shared memory starts 1024-B aligned (no static smem in this kernel)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw;
   const int C = p.C;
   const int T = C - M;
   const int GT = 1 << T;
@@ -236,18 +264,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_block_tma(const __grid_constant
     const uint32_t round = (uint32_t)(i / S);
     double2* sm = reinterpret_cast<double2*>(base + (size_t)s * stage_bytes);
     mbar_wait(full + s, round & 1u);
-    for (int ph = 0; ph < p.nphases; ++ph) {
+    const int last = p.nphases - 1;
+    for (int ph = 0; ph <= last; ++ph) {
       const TPhase& D = p.ph[ph];
       uint32_t loct = 0;
       for (int k = 0; k < T; ++k)
         if ((tid >> k) & 1u) loct |= 1u << D.tpos[k];
 #pragma unroll
       for (int j = 0; j < NA; ++j) v[j] = sm[swz128(loct | D.rloc[j])];
-      apply_ops(v, p, D, tid, T, loct);
+      if (ph == last && p.direct_store) {
+        // compute first: consuming the loaded registers guarantees every shared
+        // load has returned; then order them before the next TMA (async proxy)
+        // write into this stage, and release it before the global stores
+        apply_ops<M>(v, p, D, tid, T, loct);
+        fence_async_smem();
+        group_bar(bar_id, GT);
+        if (tid == 0) mbar_arrive(empty + s);
+        if (p.permuted) {
+          // fused SQS: amplitude with source index o goes to pi(o), a bit permutation
+          uint64_t dst = 0;
+          const int nout = p.nbits - C;
+          for (int k = 0; k < nout; ++k) dst |= ((chunk >> k) & 1ull) << p.dpos[C + k];
+          for (int k = 0; k < T; ++k)
+            if ((tid >> k) & 1u) dst |= p.ldst_t[k];
+          double2* g = reinterpret_cast<double2*>(p.out) + dst;
+#pragma unroll
+          for (int j = 0; j < NA; ++j) st_g_cs(g + p.ldst_r[j], v[j]);
+        } else {
+          double2* g = reinterpret_cast<double2*>(p.out) + (chunk << C);
+#pragma unroll
+          for (int j = 0; j < NA; ++j) st_g_cs(g + (loct | D.rloc[j]), v[j]);
+        }
+        break;
+      }
+      apply_ops<M>(v, p, D, tid, T, loct);
 #pragma unroll
       for (int j = 0; j < NA; ++j) sm[swz128(loct | D.rloc[j])] = v[j];
-      if (ph + 1 < p.nphases) group_bar(bar_id, GT);
+      if (ph < last) group_bar(bar_id, GT);
     }
+    if (p.direct_store) continue;
     fence_async_smem();
     group_bar(bar_id, GT);
     if (tid == 0) {
@@ -264,30 +319,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_block_tma(const __grid_constant
 
 }  // namespace
 
-int tma_smem_bytes(int C, int* ng, int* stages) {
+static int consumers_for(int C, int M) {
+  if (M == 4 && C == 12 && getenv("QK_NG2")) return 512;
+  return M == 4 ? kConsumers4 : kConsumers3;
+}
+
+int tma_smem_bytes(int C, int M, int* ng, int* stages) {
+  const int consumers = consumers_for(C, M);
   const int GT = 1 << (C - M);
-  const int NG = GT >= kConsumers ? 1 : kConsumers / GT;
+  const int NG = GT >= consumers ? 1 : consumers / GT;
   const uint32_t stage = 16u << C;
+  // each stage belongs to exactly one consumer group (S % NG == 0), so a
+  // group never waits on a stage more than one mbarrier phase ahead
   int S = (int)(kSmemBudget / stage);
   S = (S / NG) * NG;
   if (S > 4 * NG) S = 4 * NG;
   if (ng) *ng = NG;
   if (stages) *stages = S;
-  if (S < 2) return -1;
-  return (int)(S * stage + 2 * S * 8 + 1024);
+  if (S < 2 || S < NG) return -1;
+  return (int)(S * stage + 2 * S * 8);
 }
 
 int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_block_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_block_tma<4, 32 + kConsumers4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_block_tma<3, 32 + kConsumers3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_block_tma<4, 32 + 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   int ng = 0, st = 0;
-  const int smem = tma_smem_bytes(p->C, &ng, &st);
+  const int smem = tma_smem_bytes(p->C, p->M, &ng, &st);
   if (smem < 0) return -1;
   const uint64_t grid = p->nchunks < (uint64_t)num_sms ? p->nchunks : (uint64_t)num_sms;
-  k_block_tma<<<(unsigned)grid, kThreads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(*p);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (p->M == 4 && consumers_for(p->C, 4) == 512)
+    k_block_tma<4, 32 + 512><<<(unsigned)grid, 32 + 512, smem, s>>>(*p);
+  else if (p->M == 4)
+    k_block_tma<4, 32 + kConsumers4><<<(unsigned)grid, 32 + kConsumers4, smem, s>>>(*p);
+  else
+    k_block_tma<3, 32 + kConsumers3><<<(unsigned)grid, 32 + kConsumers3, smem, s>>>(*p);
   return (int)cudaGetLastError();
 }
 

@@ -310,3 +310,32 @@ def test_bv_basis_state_30_qubits(gpu):
     assert abs(abs(amps[0]) - 1.0) <= 1e-12 and np.max(np.abs(amps[1:])) <= 1e-12
     assert abs(res.amplitude((1 << 30) - 1)) <= 1e-12
     assert math.isfinite(res.timings["gate"])
+
+
+# ---------------------------------------------------------------------------
+# at scale: every execution strategy must agree (persistent-ring stage reuse,
+# fused out-of-place SQS, interpreter fallback) on reference-optimized circuits
+
+
+@pytest.mark.parametrize("name,n,c", [("qaoa24_c12_r0", 24, 12), ("qft26_c10_r0", 26, 10)])
+def test_execution_strategies_agree_at_scale(gpu, name, n, c):
+    import os
+    from conftest import ROOT
+    text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
+    outs = {}
+    for mode in ("default", "QK_NO_FUSE", "QK_NO_TMA"):
+        if mode != "default":
+            os.environ[mode] = "1"
+        try:
+            sim = Simulator(LayoutParams(n=n, c=n))
+            perm = sim.load_text(text, c)
+            for _ in range(2):            # second run reuses every ring stage again
+                sim.handle.reset()
+                res = sim.run_loaded(perm)
+            outs[mode] = res.physical_vector()
+            assert abs(res.norm() - 1.0) <= 1e-12, (mode, res.norm())
+        finally:
+            os.environ.pop(mode, None)
+    base = outs["QK_NO_TMA"]
+    for mode, vec in outs.items():
+        assert np.max(np.abs(vec - base)) <= TOL, mode
