@@ -171,6 +171,15 @@ int qk_apply_gate_full(qk_sim* sim, const int32_t* words, size_t nwords,
  * CUDA IPC handle (64 bytes), open the peers' handles, and register a host
  * barrier callback the runtime calls around every cross-rank swap. */
 int qk_ipc_handle(qk_sim* sim, void* handle64);
+/* Host-only plan of the cross-shard part of a CSQS for shard `shard` of a job
+ * with 2^r ranks held `count` per shard (no device needed; used by the
+ * exchange and by the multi-process CPU tests). Two-call protocol on *nseg:
+ * segs receives 4 uint64 per segment (my offset, peer shard, peer offset,
+ * length, in amplitudes of the shard vector); local_pairs receives the
+ * in-shard pairs (a_0..a_{m-1}, b_0..b_{m-1}), *nlocal = m. */
+int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set,
+                 const int32_t* rank_set, int s, uint64_t* segs, size_t* nseg,
+                 int32_t* local_pairs, int* nlocal);
 int qk_ipc_open(qk_sim* sim, int peer_shard, const void* handle64);
 typedef int (*qk_barrier_fn)(void* ctx);
 int qk_set_barrier(qk_sim* sim, qk_barrier_fn fn, void* ctx);

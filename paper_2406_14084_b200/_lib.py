@@ -60,6 +60,8 @@ _SIGS = {
     "qk_csqs": (c_int, [c_void, P(c_int32), P(c_int32), c_int]),
     "qk_apply_gate_full": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
     "qk_ipc_handle": (c_int, [c_void, c_void]),
+    "qk_csqs_plan": (c_int, [c_int, c_int, c_int, c_int, P(c_int32), P(c_int32), c_int, P(c_u64),
+                             P(c_size), P(c_int32), P(c_int)]),
     "qk_ipc_open": (c_int, [c_void, c_int, c_void]),
     "qk_set_barrier": (c_int, [c_void, BARRIER_FN, c_void]),
     "qk_mark": (c_int, [c_void, c_int]),
@@ -185,6 +187,22 @@ def parse_text(text: str, n: int, local: int, c: int):
                          ctypes.byref(npar), ctypes.byref(line))
     check(rc, line.value)
     return words[:nw.value], params[:npar.value]
+
+
+def csqs_plan(n: int, r: int, count: int, shard: int, local_set, rank_set):
+    """Cross-shard exchange plan -> (segments [(my_off, peer, peer_off, len)], in-shard pairs)."""
+    a = np.ascontiguousarray(local_set, dtype=np.int32)
+    b = np.ascontiguousarray(rank_set, dtype=np.int32)
+    nseg, nloc = c_size(0), c_int(0)
+    check(lib().qk_csqs_plan(n, r, count, shard, iptr(a), iptr(b), len(a), None, ctypes.byref(nseg),
+                             None, ctypes.byref(nloc)))
+    segs = np.zeros(max(1, 4 * nseg.value), dtype=np.uint64)
+    pairs = np.zeros(max(1, 2 * nloc.value), dtype=np.int32)
+    check(lib().qk_csqs_plan(n, r, count, shard, iptr(a), iptr(b), len(a), uptr(segs),
+                             ctypes.byref(nseg), iptr(pairs), ctypes.byref(nloc)))
+    seg_list = [tuple(int(x) for x in segs[4 * i:4 * i + 4]) for i in range(nseg.value)]
+    m = nloc.value
+    return seg_list, (tuple(int(x) for x in pairs[:m]), tuple(int(x) for x in pairs[m:2 * m]))
 
 
 class Handle:

@@ -1252,23 +1252,29 @@ int run_instr(qk_sim* s, const InstrPlan& ip) {
   return QK_OK;
 }
 
-// Multi-process CSQS (simulator.py:179-235 semantics; output independent of
-// B): the swapped rank bits select peer shards. For every pair of shards
-// (x, y) in a group, segment y of x and segment x of y are exchanged; the
-// lower shard of a pair moves the first half of the segment, the higher one
-// the second half, so both NVLink directions carry equal traffic.
-int exchange_cross(qk_sim* s, const InstrPlan& ip) {
-  if (s->nshards <= 1 || (int)s->peers.size() < s->nshards)
-    return fail(QK_ESIM, "cross-rank swap needs the peer shards' state (qk_ipc_open)");
-  const int S = ip.csqs_s;
-  const int held = s->nbits - s->L;  // rank bits inside a shard
-  std::vector<int> loc = ip.a, rk = ip.b;
+// Multi-process CSQS plan (simulator.py:179-235 semantics, output independent
+// of B). Pairs whose rank bit lies inside the shard are a local permutation;
+// the others select peer shards. CSQS local bits are the top S local bits
+// (checked), so the out-of-shard pairs use the top `so` local bits and every
+// exchange is one contiguous segment per partition: segment y of shard x <->
+// segment x of shard y. The lower shard of a pair moves the first half, the
+// higher one the second half, so both NVLink directions carry equal traffic and
+// every amplitude pair is swapped exactly once.
+struct Seg {
+  uint64_t my_off, peer, peer_off, len;
+};
+
+int csqs_plan(int n, int r, int count, int shard, const std::vector<int>& local_set,
+              const std::vector<int>& rank_set, std::vector<Seg>& segs, std::vector<int>& in_a,
+              std::vector<int>& in_b) {
+  const int L = n - r;
+  const int held = __builtin_ctz((unsigned)count);
+  std::vector<int> loc = local_set, rk = rank_set;
   std::sort(loc.begin(), loc.end());
   std::sort(rk.begin(), rk.end());
-  // pairs whose rank bit is inside the shard: plain local permutation first
-  std::vector<int> in_a, in_b, out_a, out_b;
-  for (int k = 0; k < S; ++k) {
-    if (rk[k] - s->L < held) {
+  std::vector<int> out_a, out_b;
+  for (size_t k = 0; k < loc.size(); ++k) {
+    if (rk[k] - L < held) {
       in_a.push_back(loc[k]);
       in_b.push_back(rk[k]);
     } else {
@@ -1276,56 +1282,55 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
       out_b.push_back(rk[k]);
     }
   }
-  if (s->barrier) {
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
-    if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
-  }
-  // shard-bit positions of the out-of-shard rank bits
   const int so = (int)out_a.size();
+  if (!so) return QK_OK;
+  for (int k = 0; k < so; ++k)
+    if (out_a[k] != L - so + k) return fail(QK_ESIM, "cross-shard local bits must be the top local bits");
   std::vector<int> sbit(so);
-  for (int k = 0; k < so; ++k) sbit[k] = out_b[k] - s->L - held;
-  // local bits out_a are positions < L inside each partition; segment index =
-  // value of those bits. For each partition held and each peer pattern y != x:
-  const uint64_t part = 1ull << s->L;
-  for (int pi = 0; pi < s->count; ++pi) {
-    const int me = s->shard;
-    int x = 0;
-    for (int k = 0; k < so; ++k) x |= ((me >> sbit[k]) & 1) << k;
+  for (int k = 0; k < so; ++k) sbit[k] = out_b[k] - L - held;
+  const uint64_t part = 1ull << L;
+  const uint64_t run = part >> so;
+  int x = 0;
+  for (int k = 0; k < so; ++k) x |= ((shard >> sbit[k]) & 1) << k;
+  for (int pi = 0; pi < count; ++pi) {
     for (int y = 0; y < (1 << so); ++y) {
       if (y == x) continue;
-      int peer = me;
+      int peer = shard;
       for (int k = 0; k < so; ++k) {
         peer &= ~(1 << sbit[k]);
         peer |= ((y >> k) & 1) << sbit[k];
       }
-      // amplitudes of my partition pi whose out_a bits == y <-> peer partition pi whose bits == x.
-      // out_a are the top local bits (checked by check_csqs) when in_a is empty; general case
-      // handled by enumerating contiguous runs below the lowest swapped bit.
-      const int lo = *std::min_element(out_a.begin(), out_a.end());
-      const uint64_t run = 1ull << lo;
-      const uint64_t nruns = part >> (lo + so);
-      const uint64_t half = run / 2 ? run / 2 : run;
-      const bool first_half = me < peer;
-      for (uint64_t rr = 0; rr < nruns; ++rr) {
-        uint64_t base = rr << (lo + so);
-        uint64_t my_off = base, peer_off = base;
-        for (int k = 0; k < so; ++k) {
-          my_off |= (uint64_t)((y >> k) & 1) << out_a[k];
-          peer_off |= (uint64_t)((x >> k) & 1) << out_a[k];
-        }
-        double* mine = s->state + 2 * (pi * part + my_off);
-        double* theirs = s->peers[peer] + 2 * (pi * part + peer_off);
-        uint64_t off = 0, len = run;
-        if (run > 1) {
-          off = first_half ? 0 : half;
-          len = half;
-        } else if (!first_half) {
-          continue;
-        }
-        int rc = launch_swap_segments(mine + 2 * off, theirs + 2 * off, len, (CUstream_st*)s->stream);
-        if (rc) return fail(QK_ECUDA, "peer exchange failed");
+      const uint64_t my_off = pi * part + (uint64_t)y * run;
+      const uint64_t peer_off = pi * part + (uint64_t)x * run;
+      if (run > 1) {
+        const uint64_t half = run / 2;
+        const uint64_t o = shard < peer ? 0 : half;
+        segs.push_back({my_off + o, (uint64_t)peer, peer_off + o, half});
+      } else if (shard < peer) {
+        segs.push_back({my_off, (uint64_t)peer, peer_off, 1});
       }
     }
+  }
+  return QK_OK;
+}
+
+int exchange_cross(qk_sim* s, const InstrPlan& ip) {
+  if (s->nshards <= 1 || (int)s->peers.size() < s->nshards)
+    return fail(QK_ESIM, "cross-rank swap needs the peer shards' state (qk_ipc_open)");
+  std::vector<Seg> segs;
+  std::vector<int> in_a, in_b;
+  int rc = csqs_plan(s->n, s->r, s->count, s->shard, ip.a, ip.b, segs, in_a, in_b);
+  if (rc) return rc;
+  for (auto& sg : segs)
+    if (!s->peers[sg.peer]) return fail(QK_ESIM, "peer shard %d not mapped (qk_ipc_open)", (int)sg.peer);
+  if (s->barrier) {
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
+  }
+  for (auto& sg : segs) {
+    rc = launch_swap_segments(s->state + 2 * sg.my_off, s->peers[sg.peer] + 2 * sg.peer_off, sg.len,
+                              (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "peer exchange failed");
   }
   if (s->barrier) {
     CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -1334,11 +1339,8 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   if (!in_a.empty()) {
     HostPlan tmp;
     compile_sqs(tmp, in_a, in_b, s->nbits);
-    SqsDesc* d = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(SqsDesc), s->stream));
-    CUDA_TRY(cudaMemcpyAsync(d, &tmp.sqs[0], sizeof(SqsDesc), cudaMemcpyHostToDevice, s->stream));
-    launch_sqs(s->state, &tmp.sqs[0], d, (CUstream_st*)s->stream);
-    CUDA_TRY(cudaFreeAsync(d, s->stream));
+    rc = launch_sqs(s->state, &tmp.sqs[0], nullptr, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "in-shard swap failed");
     CUDA_TRY(cudaStreamSynchronize(s->stream));
   }
   return QK_OK;
@@ -1920,6 +1922,36 @@ int qk_csqs(qk_sim* s, const int32_t* local_set, const int32_t* rank_set, int S)
     if (rc) return fail(QK_ECUDA, "csqs launch failed");
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set, const int32_t* rank_set, int S,
+                 uint64_t* segs, size_t* nseg, int32_t* local_pairs, int* nlocal) {
+  if (!nseg || !nlocal || (S && (!local_set || !rank_set))) return fail(QK_EINVAL, "null argument");
+  if (r < 0 || r > n || count < 1 || (count & (count - 1)) || count > (1 << r) || shard < 0 ||
+      shard >= (1 << r) / count)
+    return fail(QK_EINVAL, "bad shard layout");
+  std::vector<Seg> sg;
+  std::vector<int> in_a, in_b;
+  int rc = csqs_plan(n, r, count, shard, std::vector<int>(local_set, local_set + S),
+                     std::vector<int>(rank_set, rank_set + S), sg, in_a, in_b);
+  if (rc) return rc;
+  if (segs) {
+    if (*nseg < sg.size()) return fail(QK_EINVAL, "segment buffer too small");
+    for (size_t i = 0; i < sg.size(); ++i) {
+      segs[4 * i] = sg[i].my_off;
+      segs[4 * i + 1] = sg[i].peer;
+      segs[4 * i + 2] = sg[i].peer_off;
+      segs[4 * i + 3] = sg[i].len;
+    }
+  }
+  if (local_pairs)
+    for (size_t k = 0; k < in_a.size(); ++k) {
+      local_pairs[k] = in_a[k];
+      local_pairs[in_a.size() + k] = in_b[k];
+    }
+  *nseg = sg.size();
+  *nlocal = (int)in_a.size();
   return QK_OK;
 }
 
