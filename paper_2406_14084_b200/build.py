@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libqkb200.so")
-SOURCES = ["qk_kernels.cu", "qk_tma.cu", "qk_runtime.cpp"]
+SOURCES = ["qk_kernels.cu", "qk_tma.cu", "qk_jit.cpp", "qk_runtime.cpp"]
 HEADERS = ["qk_internal.h", os.path.join("..", "..", "include", "qkb200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -39,7 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = OUT + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "-shared", "-cudart", "static", "-o", tmp,
-           *[os.path.join(CSRC, s) for s in SOURCES]]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -14,6 +14,9 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <string>
+#include <vector>
+
 namespace qk {
 
 constexpr int kMaxC = 13;        // 2^13 complex128 = 128 KiB of shared memory per CTA
@@ -141,6 +144,11 @@ int launch_block_pass(double* state, const PassDesc* h_pass, const PassDesc* d_p
                       const double* d_tables, uint64_t first, CUstream_st* stream);
 int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream);
 int tma_smem_bytes(int C, int M, int* ng, int* stages);
+// load-time specialised passes (qk_jit.cpp)
+bool jit_available();
+bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef);
+void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles);
+int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);

@@ -845,6 +845,8 @@ struct qk_sim {
   bool map_ok[2][6] = {{false, false, false, false, false, false}, {false, false, false, false, false, false}};
   std::vector<TmaParams> tma;
   std::vector<int> pass_tma;
+  std::vector<void*> pass_jit;                 // specialised kernel per pass (or nullptr)
+  std::vector<std::vector<uint64_t>> jit_blob;  // its parameter block (map/state/out patched at launch)
   // multi-process
   qk_barrier_fn barrier = nullptr;
   void* barrier_ctx = nullptr;
@@ -1041,6 +1043,43 @@ int upload_plan(qk_sim* s) {
   for (auto& ip : s->iplan)
     if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty())
       ip.permuted = s->pass_tma[ip.pass0 + ip.npass - 1] >= 0;
+  // specialise TMA passes of large states (compile cost amortised; cached per structure)
+  s->pass_jit.assign(hp.passes.size(), nullptr);
+  s->jit_blob.assign(hp.passes.size(), {});
+  const char* jenv = getenv("QK_JIT");
+  const int jit_min = jenv ? atoi(jenv) : 20;   // QK_JIT=<min address bits>; QK_NO_JIT disables
+  if (jit_available() && s->nbits >= jit_min) {
+    std::vector<std::string> srcs;
+    std::vector<int> src_pass;
+    std::vector<std::vector<long long>> toffs;
+    std::vector<std::vector<double>> coefs;
+    for (size_t p = 0; p < hp.passes.size(); ++p) {
+      if (s->pass_tma[p] < 0) continue;
+      std::string src;
+      std::vector<long long> toff;
+      std::vector<double> coef;
+      if (!jit_source(s->tma[s->pass_tma[p]], &src, &toff, &coef)) continue;
+      srcs.push_back(std::move(src));
+      src_pass.push_back((int)p);
+      toffs.push_back(std::move(toff));
+      coefs.push_back(std::move(coef));
+    }
+    std::vector<void*> handles;
+    jit_build(srcs, &handles);
+    for (size_t i = 0; i < srcs.size(); ++i) {
+      if (!handles[i]) continue;
+      const int p = src_pass[i];
+      // QkJitParams: map[16 words] | tabs | state | out | nchunks | toff[ntab+1] | coef[ncoef+1]
+      std::vector<uint64_t> blob(16 + 4 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
+      blob[16] = (uint64_t)(uintptr_t)s->d_pool;
+      blob[19] = s->tma[s->pass_tma[p]].nchunks;
+      for (size_t k = 0; k < toffs[i].size(); ++k) blob[20 + k] = (uint64_t)toffs[i][k];
+      const size_t co = 20 + toffs[i].size() + 1;
+      for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
+      s->pass_jit[p] = handles[i];
+      s->jit_blob[p] = std::move(blob);
+    }
+  }
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
                                  (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
@@ -1212,7 +1251,16 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
     tp.map = *map;
     tp.state = s->bufs[s->cur];
     tp.out = tp.permuted ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
-    int rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
+    int rc;
+    if (p < (int)s->pass_jit.size() && s->pass_jit[p]) {
+      std::vector<uint64_t>& blob = s->jit_blob[p];
+      memcpy(blob.data(), map, 128);
+      blob[17] = (uint64_t)(uintptr_t)tp.state;
+      blob[18] = (uint64_t)(uintptr_t)tp.out;
+      rc = jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream);
+    } else {
+      rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
+    }
     if (rc) return fail(QK_ECUDA, "tma block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
     if (tp.permuted) {
       s->cur ^= 1;

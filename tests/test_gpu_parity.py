@@ -22,7 +22,7 @@ def _layout_for(c):
     return LayoutParams(n=c["n"], c=c["n"] - c["r"], r=c["r"], b=c["b"])
 
 
-def test_golden_circuits(gpu, golden):
+def test_golden_circuits(gpu, engine, golden):
     meta, arr = golden
     worst = 0.0
     for c in meta["circuits"]:
@@ -223,8 +223,21 @@ def _random_stream(rng, n, r, c, nins):
     return tuple(out)
 
 
+@pytest.fixture(params=["interp", "jit"])
+def engine(request):
+    """Run a test once with the interpreted passes and once with every TMA pass
+    specialised by the load-time JIT (QK_JIT=<min address bits>)."""
+    import os
+    if request.param == "jit":
+        os.environ["QK_JIT"] = "0"
+    else:
+        os.environ["QK_JIT"] = "99"
+    yield request.param
+    os.environ.pop("QK_JIT", None)
+
+
 @pytest.mark.parametrize("seed", range(24))
-def test_random_streams_vs_oracle(gpu, seed):
+def test_random_streams_vs_oracle(gpu, engine, seed):
     rng = np.random.default_rng(500 + seed)
     n = int(rng.integers(3, 15))
     r = int(rng.integers(0, min(3, n - 1) + 1))
@@ -250,7 +263,7 @@ def test_random_streams_vs_oracle(gpu, seed):
     assert err <= TOL, (seed, n, r, c, err)
 
 
-def test_chunk_widths_up_to_13(gpu):
+def test_chunk_widths_up_to_13(gpu, engine):
     rng = np.random.default_rng(77)
     for c in (10, 11, 12, 13):
         n = 16
@@ -323,7 +336,7 @@ def test_execution_strategies_agree_at_scale(gpu, name, n, c):
     from conftest import ROOT
     text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
     outs = {}
-    for mode in ("default", "QK_NO_FUSE", "QK_NO_TMA"):
+    for mode in ("default", "QK_NO_FUSE", "QK_NO_TMA", "QK_NO_JIT"):
         if mode != "default":
             os.environ[mode] = "1"
         try:
