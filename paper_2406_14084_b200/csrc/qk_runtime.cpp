@@ -360,6 +360,7 @@ struct InstrPlan {
   std::vector<int> dest;     // block: destination bit of each source bit (fused SQS), empty if none
   int permuted = 0;          // block: last pass scatters out-of-place (set at upload)
   int fused_by = -1;         // SQS/CSQS: index of the block whose last pass absorbs it
+  int synthetic = 0;         // block: layout-restore pass appended by the planner
   int sqs = -1;              // SQS / single-device CSQS
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
@@ -472,8 +473,11 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     }
     phs.back().items.push_back((int)i);
   }
-  if (phs.empty()) {  // no gates at all: nothing to do
-    return QK_OK;
+  if (phs.empty()) {
+    if (!dest) return QK_OK;  // no gates at all: nothing to do
+    PhaseB pb;                 // layout-only pass (restore / relabel)
+    for (int q = C - 1; q >= 0 && (int)pb.R.size() < M; --q) pb.R.push_back(q);
+    phs.push_back(pb);
   }
   // 4. tables for runs (built on device at load), H scale folded into the first table
   const double scale = (nh % 2 == 0) ? std::ldexp(1.0, -nh / 2) : std::ldexp(kSqrt1_2, -(nh - 1) / 2);
@@ -663,20 +667,20 @@ int block_chunk_width(const InstrH& ins, int L, int cmin = 10) {
 }
 
 int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& ip,
-                  std::string& emsg, int cmin = 10) {
+                  std::string& emsg, int cmin = 10, int cfix = 0) {
   const std::vector<int>* dest = ip.dest.empty() ? nullptr : &ip.dest;
   int maxt = -1;
   for (auto& g : ins.gates)
     for (int t : g.t) maxt = std::max(maxt, t);
   ip.pass0 = (int)hp.passes.size();
-  if (maxt < 0) return QK_OK;
+  if (maxt < 0 && !(dest && cfix)) return QK_OK;
   if (maxt >= L) {
     emsg = "gate target " + std::to_string(maxt) + " beyond local range";
     return QK_ESIM;
   }
   const int low_keep = std::min(3, L);
   if (maxt < kMaxC) {
-    const int C = block_chunk_width(ins, L, cmin);
+    const int C = cfix ? std::max(cfix, block_chunk_width(ins, L, cmin)) : block_chunk_width(ins, L, cmin);
     std::vector<int> Q;
     for (int p = 0; p < C; ++p) Q.push_back(p);
     std::vector<const GateH*> gs;
@@ -713,10 +717,14 @@ int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& 
 }
 
 // new[i] = old[bitswap(i, A, B)] over a vector of nbits address bits
-int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>& B0, int nbits) {
+int compile_sqs(HostPlan& hp, const std::vector<int>& A0, const std::vector<int>& B0, int nbits,
+                bool paired = false) {
+  // pairs sorted(A)[k] <-> sorted(B)[k] (simulator.py:85); `paired`: A[k] <-> B[k] as given
   std::vector<int> A = A0, B = B0;
-  std::sort(A.begin(), A.end());
-  std::sort(B.begin(), B.end());
+  if (!paired) {
+    std::sort(A.begin(), A.end());
+    std::sort(B.begin(), B.end());
+  }
   int partner[64];
   for (int& x : partner) x = -1;
   for (size_t k = 0; k < A.size(); ++k) {
@@ -1041,8 +1049,11 @@ int upload_plan(qk_sim* s) {
     }
   }
   for (auto& ip : s->iplan)
-    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty())
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) {
       ip.permuted = s->pass_tma[ip.pass0 + ip.npass - 1] >= 0;
+      // the planner already relabeled the qubits for this pass: it must run
+      if (!ip.permuted) return fail(QK_ESIM, "internal: fused pass is not executable on the TMA path");
+    }
   // specialise TMA passes of large states (compile cost amortised; cached per structure)
   s->pass_jit.assign(hp.passes.size(), nullptr);
   s->jit_blob.assign(hp.passes.size(), {});
@@ -1123,61 +1134,135 @@ int check_csqs(const qk_sim* s, const std::vector<int>& local_set, const std::ve
   return QK_OK;
 }
 
+// Conservative plan-time check that a single-pass block runs on the TMA path
+// (a fused pass must: the swaps it absorbs have no other executor).
+bool tma_plan_ok(const HostPlan& hp, int pass, int nbits) {
+  if (getenv("QK_NO_TMA")) return false;
+  const PassDesc& pd = hp.passes[pass];
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || nbits > 34) return false;
+  if (pd.nouter != nbits - pd.C) return false;
+  const int ob = hp.phases[pd.phase0].op_begin, oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
+  int ncoef = 0;
+  for (int o = ob; o < oe; ++o) ncoef += hp.ops[o].code == OP_MAT ? 8 : (hp.ops[o].code == OP_SCALE ? 1 : 0);
+  return oe - ob <= kTMaxOps && ncoef <= kTMaxCoef;
+}
+
 int compile_program(qk_sim* s) {
   s->hp.clear();
   s->iplan.clear();
   std::string emsg;
-  // fusion pre-scan: with a second buffer, every run of SQS (and on-device
-  // CSQS) right after a gate block becomes that block's output permutation
-  std::vector<std::vector<int>> dest(s->prog.size());
-  std::vector<int> fused_by(s->prog.size(), -1);
-  if (s->bufs[1] && !getenv("QK_NO_FUSE")) {
-    const int held_rank_bits = s->nbits - s->L;
-    for (size_t i = 0; i < s->prog.size(); ++i) {
-      if (s->prog[i].type != QK_INS_BLOCK || s->prog[i].gates.empty()) continue;
-      std::vector<int> pos(s->nbits), fuse_pos;
-      for (int q = 0; q < s->nbits; ++q) pos[q] = q;
-      size_t j = i + 1;
-      for (; j < s->prog.size(); ++j) {
-        const InstrH& nx = s->prog[j];
-        if (nx.type == QK_INS_BLOCK || nx.a.empty()) break;
-        bool ok = true;
-        for (int q : nx.a) ok = ok && q >= 0 && q < s->nbits;
-        for (int q : nx.b) ok = ok && q >= 0 && q < s->nbits && (nx.type == QK_INS_SQS || q - s->L < held_rank_bits);
-        if (nx.type == QK_INS_SQS)
-          for (int q : nx.b) ok = ok && q < s->L;
-        if (nx.type == QK_INS_CSQS && check_csqs(s, nx.a, nx.b) != QK_OK) ok = false;
-        if (!ok) break;
-        std::vector<int> a = nx.a, b = nx.b;
-        std::sort(a.begin(), a.end());
-        std::sort(b.begin(), b.end());
-        for (int q = 0; q < s->nbits; ++q)
-          for (size_t k = 0; k < a.size(); ++k) {
-            if (pos[q] == a[k]) { pos[q] = b[k]; break; }
-            if (pos[q] == b[k]) { pos[q] = a[k]; break; }
-          }
-        // keep the fusion only while the 5 lowest destination bits still come
-        // from chunk bits: every warp then stores whole 512-B runs. Swaps that
-        // move low bits out of the chunk are left to the tiled SQS kernel.
-        bool coalesced = true;
-        const int cw = block_chunk_width(s->prog[i], s->L);
-        for (int q = 0; q < s->nbits; ++q)
-          if (pos[q] < 5 && q >= cw) coalesced = false;
-        if (!coalesced) break;
-        fused_by[j] = (int)i;
-        fuse_pos = pos;
-      }
-      if (j > i + 1 && !fuse_pos.empty()) dest[i] = fuse_pos;
-    }
+  const int nb = s->nbits;
+  // Relabeling mode (needs the second buffer): every block runs with the same
+  // chunk width Cg over address bits [0, Cg); a plan-time map sigma (reference
+  // position -> address bit) absorbs SQS runs into the preceding block's
+  // out-of-place store. The store's destination layout keeps the next chunk
+  // contiguous and puts >= 5 qubits that stay in the chunk on the lowest
+  // address bits, so every warp still writes whole 512-B runs.
+  int Cg = 0;
+  bool relabel = s->bufs[1] && !getenv("QK_NO_FUSE") && !getenv("QK_NO_TMA");
+  for (auto& ins : s->prog) {
+    if (ins.type != QK_INS_BLOCK || ins.gates.empty()) continue;
+    const int w = block_chunk_width(ins, s->L);
+    if (!w) relabel = false;
+    Cg = std::max(Cg, w);
   }
+  if (Cg < 9 || Cg > 12 || Cg > nb) relabel = false;
+  std::vector<int> sigma(nb);
+  for (int q = 0; q < nb; ++q) sigma[q] = q;
+  std::vector<char> fused(s->prog.size(), 0);
+  auto remap = [&](const InstrH& ins) {
+    InstrH m = ins;
+    for (auto& g : m.gates)
+      for (int& t : g.t) t = sigma[t];
+    return m;
+  };
   for (size_t ii = 0; ii < s->prog.size(); ++ii) {
     auto& ins = s->prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
-    ip.fused_by = fused_by[ii];
     if (ins.type == QK_INS_BLOCK) {
-      ip.dest = dest[ii];
-      int rc = compile_block(s->hp, ins, s->L, s->nbits, ip, emsg);
+      InstrH mapped = remap(ins);
+      if (relabel && !ins.gates.empty()) {
+        // longest run of following SQS that still leaves >= 5 lane positions
+        std::vector<int> best_d;
+        size_t best_j = ii + 1;
+        std::vector<int> P(nb);  // P[q]: reference position whose data lands on q
+        for (int q = 0; q < nb; ++q) P[q] = q;
+        std::vector<int> Rlast;
+        {
+          HostPlan scratch;
+          InstrPlan sp;
+          if (compile_block(scratch, mapped, s->L, nb, sp, emsg, 10, Cg) == QK_OK && sp.npass == 1) {
+            const PassDesc& pd = scratch.passes[0];
+            const PhaseDesc& D = scratch.phases[pd.phase0 + pd.nphases - 1];
+            std::vector<char> isT(Cg, 0);
+            for (int k = 0; k < D.tbits; ++k) isT[D.tpos[k]] = 1;
+            for (int q = 0; q < Cg; ++q)
+              if (!isT[q]) Rlast.push_back(q);
+          }
+        }
+        for (size_t j = ii + 1; j < s->prog.size() && s->prog[j].type == QK_INS_SQS && !s->prog[j].a.empty(); ++j) {
+          std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
+          bool ok = true;
+          for (int q : a) ok = ok && q >= 0 && q < s->L;
+          for (int q : b) ok = ok && q >= 0 && q < s->L;
+          if (!ok) break;
+          std::sort(a.begin(), a.end());
+          std::sort(b.begin(), b.end());
+          std::vector<int> P2 = P;  // after this swap, q holds what P said pi(q) held
+          for (size_t k = 0; k < a.size(); ++k) std::swap(P2[a[k]], P2[b[k]]);
+          // source addresses of the next chunk's qubits
+          std::vector<char> in_next(nb, 0);
+          for (int q = 0; q < Cg; ++q) in_next[sigma[P2[q]]] = 1;
+          std::vector<int> stay_lane, stay_reg, incoming, rest;
+          for (int a2 = 0; a2 < nb; ++a2) {
+            if (in_next[a2] && a2 < Cg) {
+              (std::find(Rlast.begin(), Rlast.end(), a2) == Rlast.end() ? stay_lane : stay_reg).push_back(a2);
+            } else if (in_next[a2]) {
+              incoming.push_back(a2);
+            } else {
+              rest.push_back(a2);
+            }
+          }
+          if (stay_lane.size() < 3) break;   // lanes 0-2 on dest bits 0-2: full 128-B lines
+          std::vector<int> d(nb);
+          int pos = 0;
+          for (int x : stay_lane) d[x] = pos++;
+          for (int x : stay_reg) d[x] = pos++;
+          for (int x : incoming) d[x] = pos++;
+          for (int x : rest) d[x] = pos++;
+          P = P2;
+          best_d = d;
+          best_j = j + 1;
+        }
+        if (!best_d.empty()) {
+          ip.dest = best_d;
+          const size_t hp_passes = s->hp.passes.size();
+          int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, Cg);
+          if (rc) return fail(rc, "%s", emsg.c_str());
+          if (ip.npass == 1 && tma_plan_ok(s->hp, (int)hp_passes, nb)) {
+            std::vector<int> ns(nb);
+            for (int q = 0; q < nb; ++q) ns[q] = best_d[sigma[P[q]]];
+            sigma = ns;
+            for (size_t j = ii + 1; j < best_j; ++j) fused[j] = 1;
+            ip.fused_by = -1;
+            s->iplan.push_back(std::move(ip));
+            const int block_idx = (int)s->iplan.size() - 1;
+            for (size_t j = ii + 1; j < best_j; ++j) {
+              InstrPlan fp;
+              fp.type = QK_INS_SQS;
+              fp.fused_by = block_idx;
+              s->iplan.push_back(std::move(fp));
+            }
+            ii = best_j - 1;
+            continue;
+          }
+          // not fusable after all: recompile in place (drop the permuted pass)
+          s->hp.passes.resize(hp_passes);
+          ip.dest.clear();
+        }
+      }
+      int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, relabel ? Cg : 0);
       if (rc) return fail(rc, "%s", emsg.c_str());
     } else if (ins.type == QK_INS_SQS) {
       for (int q : ins.a)
@@ -1186,13 +1271,26 @@ int compile_program(qk_sim* s) {
       for (int q : ins.b)
         if (q < 0 || q >= s->L)
           return fail(QK_EINVAL, "swap bit %d out of range for %d local qubits", q, s->L);
-      ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, ins.a, ins.b, s->nbits);
-      ip.bytes = 32.0 * std::ldexp(1.0, s->nbits) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
+      std::vector<int> a, b;
+      for (int q : ins.a) a.push_back(sigma[q]);
+      for (int q : ins.b) b.push_back(sigma[q]);
+      // keep the sorted-pair semantics of the reference: pair sorted(A)[k] with sorted(B)[k]
+      std::vector<int> sa = ins.a, sb = ins.b;
+      std::sort(sa.begin(), sa.end());
+      std::sort(sb.begin(), sb.end());
+      a.clear();
+      b.clear();
+      for (size_t k = 0; k < sa.size(); ++k) {
+        a.push_back(sigma[sa[k]]);
+        b.push_back(sigma[sb[k]]);
+      }
+      ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
+      ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
     } else {
       int rc = check_csqs(s, ins.a, ins.b);
       if (rc) return rc;
       // rank bits held inside this handle become plain address bits
-      const int held_rank_bits = s->nbits - s->L;
+      const int held_rank_bits = nb - s->L;
       bool local_only = true;
       for (int q : ins.b)
         if (q - s->L >= held_rank_bits) local_only = false;
@@ -1200,12 +1298,36 @@ int compile_program(qk_sim* s) {
       ip.b = ins.b;
       ip.csqs_s = (int)ins.a.size();
       if (local_only) {
-        ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, ins.a, ins.b, s->nbits);
+        std::vector<int> sa = ins.a, sb = ins.b;
+        std::sort(sa.begin(), sa.end());
+        std::sort(sb.begin(), sb.end());
+        std::vector<int> a, b;
+        for (size_t k = 0; k < sa.size(); ++k) {
+          a.push_back(sigma[sa[k]]);
+          b.push_back(sigma[sb[k]]);
+        }
+        ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
       } else {
-        ip.sqs = -2;  // cross-process exchange
+        ip.sqs = -2;  // cross-process exchange (shard mode: sigma is the identity)
       }
-      ip.bytes = 32.0 * std::ldexp(1.0, s->nbits) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
+      ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
     }
+    s->iplan.push_back(std::move(ip));
+  }
+  // restore the reference layout at the end of the program
+  bool ident = true;
+  for (int q = 0; q < nb; ++q) ident = ident && sigma[q] == q;
+  if (!ident) {
+    std::vector<int> d(nb);
+    for (int q = 0; q < nb; ++q) d[sigma[q]] = q;
+    InstrPlan ip;
+    ip.type = QK_INS_BLOCK;
+    ip.dest = d;
+    InstrH empty;
+    empty.type = QK_INS_BLOCK;
+    int rc = compile_block(s->hp, empty, s->L, nb, ip, emsg, 10, Cg);
+    if (rc || ip.npass != 1) return fail(QK_ESIM, "internal: layout restore pass failed");
+    ip.synthetic = 1;
     s->iplan.push_back(std::move(ip));
   }
   replay_perm(s);
@@ -1230,6 +1352,12 @@ int compile_program(qk_sim* s) {
       }
     }
     for (auto& t : s->hp.tables) fprintf(stderr, "table: bits=%d gates=%d\n", t.bits, t.ng);
+    int nf = 0, ns = 0;
+    for (auto& ip : s->iplan) {
+      nf += ip.fused_by >= 0;
+      ns += ip.type == QK_INS_SQS;
+    }
+    fprintf(stderr, "relabel=%d Cg=%d fused SQS %d of %d\n", (int)relabel, Cg, nf, ns);
   }
   return upload_plan(s);
 }
