@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libqkb200.so")
-SOURCES = ["qk_kernels.cu", "qk_tma.cu", "qk_jit.cpp", "qk_runtime.cpp"]
+SOURCES = ["qk_kernels.cu", "qk_tma.cu", "qk_sqs.cu", "qk_jit.cpp", "qk_runtime.cpp"]
 HEADERS = ["qk_internal.h", os.path.join("..", "..", "include", "qkb200.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -152,6 +152,7 @@ int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, i
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);
+int launch_sqs_bulk(double* state, const SqsDesc* h, int num_sms, CUstream_st* stream);
 int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p, const int* q,
                      int np, const int* a, const int* b, int k, CUstream_st* stream);
 int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* stream);

@@ -1420,7 +1420,10 @@ int run_instr(qk_sim* s, const InstrPlan& ip) {
     return QK_OK;
   }
   if (ip.sqs >= 0) {
-    int rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
+    int rc = -2;
+    if (getenv("QK_SQS_BULK") && s->nbits >= 16)  // bulk-copy variant: 512-B copies are TMA-op bound
+      rc = launch_sqs_bulk(s->state, &s->hp.sqs[ip.sqs], s->num_sms, (CUstream_st*)s->stream);
+    if (rc == -2) rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "sqs launch failed: %s", cudaGetErrorString((cudaError_t)rc));
     return QK_OK;
   }
