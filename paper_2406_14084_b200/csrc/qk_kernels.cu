@@ -15,6 +15,7 @@
 //   k_sumsq / k_gather  norm and readback (simulator.py:393-419).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "qk_internal.h"
 
@@ -397,7 +398,103 @@ __global__ void __launch_bounds__(256) k_sqs(double2* __restrict__ state, const 
   }
 }
 
+// cp.async variant: 16-B async copies land in (swizzled) shared memory without
+// register staging, so several CTAs per SM keep ~100+ KiB of loads in flight.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_sqs_async(double2* __restrict__ state, const __grid_constant__ SqsDesc S) {
+  extern __shared__ double2 sm[];
+  const int nv = S.nv, w = S.w;
+  const uint32_t tile = 1u << nv;
+  const uint64_t nunits = 1ull << S.nouter;
+  const int lane = threadIdx.x & 31;
+  const uint32_t e0 = threadIdx.x;
+  const int per = tile > 256 ? (int)(tile >> 8) : 1;
+  const bool active = e0 < tile;
+  const uint32_t wmask = (1u << w) - 1;
+  uint64_t off[4];
+  uint32_t pe[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const uint32_t e = e0 + 256u * m;
+    uint64_t o = e & wmask;
+    for (int b = w; b < nv; ++b) o |= (uint64_t)((e >> b) & 1u) << S.vpos[b];
+    off[m] = o;
+    uint32_t q = e;
+    for (int k = 0; k < S.nvp; ++k) {
+      const uint32_t d = ((q >> S.va[k]) ^ (q >> S.vb[k])) & 1u;
+      q ^= (d << S.va[k]) | (d << S.vb[k]);
+    }
+    pe[m] = swz(q);
+  }
+  for (uint64_t X = blockIdx.x; X < nunits; X += gridDim.x) {
+    uint64_t c = 0;
+    if (lane < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane]) ^ (X >> S.ob[lane])) & 1ull;
+      c = (d << S.oa[lane]) | (d << S.ob[lane]);
+    }
+    if (lane + 32 < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane + 32]) ^ (X >> S.ob[lane + 32])) & 1ull;
+      c |= (d << S.oa[lane + 32]) | (d << S.ob[lane + 32]);
+    }
+    const uint64_t Y = X ^ warp_or64(c);
+    if (Y < X) continue;
+    const bool same = (Y == X);
+    if (same && S.ident) continue;
+    uint64_t cx = 0, cy = 0;
+    if (lane < S.nouter) {
+      cx = ((X >> lane) & 1ull) << S.opos[lane];
+      cy = ((Y >> lane) & 1ull) << S.opos[lane];
+    }
+    if (lane + 32 < S.nouter) {
+      cx |= ((X >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+      cy |= ((Y >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+    }
+    const uint64_t bx = warp_or64(cx), by = warp_or64(cy);
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m < per && active) {
+        const uint32_t e = swz(e0 + 256u * m);
+        cp_async16(sm + e, state + bx + off[m]);
+        if (!same) cp_async16(sm + tile + e, state + by + off[m]);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      if (m < per && active) {
+        if (same) {
+          st_g(state + bx + off[m], sm[pe[m]]);
+        } else {
+          st_g(state + bx + off[m], sm[tile + pe[m]]);
+          st_g(state + by + off[m], sm[pe[m]]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* /*d*/, CUstream_st* stream) {
+  if (!getenv("QK_SQS_REG")) {
+    const uint64_t units = 1ull << h->nouter;
+    const size_t smem = (size_t)2 * (16u << h->nv);
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_sqs_async, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (16 << 10));
+      attr2 = true;
+    }
+    uint64_t grid = 148ull * 7;
+    if (grid > units) grid = units;
+    k_sqs_async<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+        reinterpret_cast<double2*>(state), *h);
+    return (int)cudaGetLastError();
+  }
   const uint64_t units = 1ull << h->nouter;
   const size_t smem = h->ident ? 0 : (size_t)2 * (16u << h->nv);
   uint64_t grid = 148ull * 6;
