@@ -479,16 +479,22 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     for (int q = C - 1; q >= 0 && (int)pb.R.size() < M; --q) pb.R.push_back(q);
     phs.push_back(pb);
   }
-  // 4. tables for runs (built on device at load), H scale folded into the first table
+  // 4. tables for runs (built on device at load), H scale folded into the first
+  //    table. A run's table index bits are ordered for the phase that applies
+  //    it: the lanes' positions first, then the register slots, so the 32
+  //    lanes of a warp read one contiguous 512-B span of the table.
   const double scale = (nh % 2 == 0) ? std::ldexp(1.0, -nh / 2) : std::ldexp(kSqrt1_2, -(nh - 1) / 2);
   bool scale_folded = (nh == 0);
-  std::vector<int64_t> run_table(runs.size());
-  for (size_t r = 0; r < runs.size(); ++r) {
+  std::vector<int64_t> run_table(runs.size(), -1);
+  std::vector<std::vector<int>> run_bidx(runs.size());
+  auto build_table = [&](int r, const std::vector<int>& order) -> int {
     const uint32_t S = run_support[r];
-    int bidx[32];
+    std::vector<int> bidx(C, -1);
     int nb = 0;
+    for (int p : order)
+      if (p >= 0 && p < C && (S >> p & 1) && bidx[p] < 0) bidx[p] = nb++;
     for (int p = 0; p < C; ++p)
-      if (S >> p & 1) bidx[p] = nb++;
+      if ((S >> p & 1) && bidx[p] < 0) bidx[p] = nb++;
     TableDesc td{};
     td.out = hp.pool;
     td.bits = nb;
@@ -519,9 +525,11 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       hp.tgates.push_back(tg);
     }
     run_table[r] = hp.pool;
+    run_bidx[r] = bidx;
     hp.pool += (int64_t)1 << nb;
     hp.tables.push_back(td);
-  }
+    return QK_OK;
+  };
   // 5. emit phases and ops
   PassDesc pd{};
   pd.C = C;
@@ -577,17 +585,20 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       OpDesc op{};
       if (it.type == 1) {
         const uint32_t S = run_support[it.run];
-        int bidx[32];
-        int nb = 0;
-        for (int p = 0; p < C; ++p)
-          if (S >> p & 1) bidx[p] = nb++;
+        if (run_table[it.run] < 0) {
+          std::vector<int> order(T.begin(), T.end());
+          for (int q : pb.R) order.push_back(q);
+          int rc = build_table(it.run, order);
+          if (rc) return rc;
+        }
+        const std::vector<int>& bidx = run_bidx[it.run];
         op.code = OP_DIAG;
         op.table = run_table[it.run];
         for (int k = 0; k < D.tbits; ++k) op.tcontrib[k] = (S >> T[k] & 1) ? (uint16_t)(1u << bidx[T[k]]) : 0;
         for (int j = 0; j < (1 << M); ++j) {
           uint32_t v = 0;
-          for (int s = 0; s < M; ++s)
-            if ((j >> s & 1) && (S >> pb.R[s] & 1)) v |= 1u << bidx[pb.R[s]];
+          for (int s2 = 0; s2 < M; ++s2)
+            if ((j >> s2 & 1) && (S >> pb.R[s2] & 1)) v |= 1u << bidx[pb.R[s2]];
           op.pr[j] = (uint16_t)v;
         }
       } else {

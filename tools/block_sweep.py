@@ -37,6 +37,11 @@ cases = {
     "12RX": [RX(q) for q in range(12)],
     "5RX+2tables": [RZZ(a, b) for a in range(12) for b in range(a + 1, 12)][:30] + [RX(q) for q in range(5)]
     + [RZZ(a, b) for a in range(12) for b in range(a + 1, 12)][30:],
+    "5RX+1table": [RX(q) for q in range(5)] + [RZZ(a, b) for a in range(12) for b in range(a + 1, 12)],
+    "2tables(H11 between)": [RZZ(a, b) for a in range(11) for b in range(a + 1, 11)] + [H(11)]
+    + [RZZ(a, 11) for a in range(11)] + [RZZ(a, b) for a in range(5) for b in range(a + 1, 5)],
+    "2tables8bit": [RZZ(a, b) for a in range(8) for b in range(a + 1, 8)] + [H(11)]
+    + [RZZ(a, b) for a in range(4, 12) for b in range(a + 1, 12)],
     "sqs_k7_hi": "S1",
     "sqs_k7_lo": "S2",
     "sqs_k12": "S3",
