@@ -473,11 +473,23 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     }
     phs.back().items.push_back((int)i);
   }
-  if (phs.empty()) {
-    if (!dest) return QK_OK;  // no gates at all: nothing to do
-    PhaseB pb;                 // layout-only pass (restore / relabel)
-    for (int q = C - 1; q >= 0 && (int)pb.R.size() < M; --q) pb.R.push_back(q);
-    phs.push_back(pb);
+  if (phs.empty() && !dest) return QK_OK;  // no gates at all: nothing to do
+  if (dest) {
+    // fused (permuted) store: the 5 positions landing on destination bits
+    // 0..4 must be lanes of the last phase (512-B runs per warp store). If
+    // the last phase holds one of them in a register slot, append a
+    // layout-only phase whose register slots take the highest destinations.
+    std::vector<int> by_dest;
+    for (int q = 0; q < C; ++q) by_dest.push_back(q);
+    std::sort(by_dest.begin(), by_dest.end(), [&](int x, int y) { return (*dest)[Q[x]] < (*dest)[Q[y]]; });
+    bool ok = !phs.empty();
+    for (int i = 0; i < 5 && i < C && ok; ++i)
+      if (std::find(phs.back().R.begin(), phs.back().R.end(), by_dest[i]) != phs.back().R.end()) ok = false;
+    if (!ok) {
+      PhaseB pb;
+      for (int i = C - 1; i >= 0 && (int)pb.R.size() < M; --i) pb.R.push_back(by_dest[i]);
+      phs.push_back(pb);
+    }
   }
   // 4. tables for runs (built on device at load), H scale folded into the first
   //    table. A run's table index bits are ordered for the phase that applies
@@ -1199,19 +1211,6 @@ int compile_program(qk_sim* s) {
         size_t best_j = ii + 1;
         std::vector<int> P(nb);  // P[q]: reference position whose data lands on q
         for (int q = 0; q < nb; ++q) P[q] = q;
-        std::vector<int> Rlast;
-        {
-          HostPlan scratch;
-          InstrPlan sp;
-          if (compile_block(scratch, mapped, s->L, nb, sp, emsg, 10, Cg) == QK_OK && sp.npass == 1) {
-            const PassDesc& pd = scratch.passes[0];
-            const PhaseDesc& D = scratch.phases[pd.phase0 + pd.nphases - 1];
-            std::vector<char> isT(Cg, 0);
-            for (int k = 0; k < D.tbits; ++k) isT[D.tpos[k]] = 1;
-            for (int q = 0; q < Cg; ++q)
-              if (!isT[q]) Rlast.push_back(q);
-          }
-        }
         for (size_t j = ii + 1; j < s->prog.size() && s->prog[j].type == QK_INS_SQS && !s->prog[j].a.empty(); ++j) {
           std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
           bool ok = true;
@@ -1225,21 +1224,19 @@ int compile_program(qk_sim* s) {
           // source addresses of the next chunk's qubits
           std::vector<char> in_next(nb, 0);
           for (int q = 0; q < Cg; ++q) in_next[sigma[P2[q]]] = 1;
-          std::vector<int> stay_lane, stay_reg, incoming, rest;
+          std::vector<int> stay, incoming, rest;
           for (int a2 = 0; a2 < nb; ++a2) {
-            if (in_next[a2] && a2 < Cg) {
-              (std::find(Rlast.begin(), Rlast.end(), a2) == Rlast.end() ? stay_lane : stay_reg).push_back(a2);
-            } else if (in_next[a2]) {
-              incoming.push_back(a2);
-            } else {
-              rest.push_back(a2);
-            }
+            if (in_next[a2] && a2 < Cg) stay.push_back(a2);
+            else if (in_next[a2]) incoming.push_back(a2);
+            else rest.push_back(a2);
           }
-          if (stay_lane.size() < 3) break;   // lanes 0-2 on dest bits 0-2: full 128-B lines
+          // >= 5 qubits that stay in the chunk go to destination bits 0..4, so
+          // every warp writes whole 512-B runs (128-B runs scattered at 64-KiB
+          // strides measured slower than a separate SQS pass)
+          if (stay.size() < 5) break;
           std::vector<int> d(nb);
           int pos = 0;
-          for (int x : stay_lane) d[x] = pos++;
-          for (int x : stay_reg) d[x] = pos++;
+          for (int x : stay) d[x] = pos++;
           for (int x : incoming) d[x] = pos++;
           for (int x : rest) d[x] = pos++;
           P = P2;

@@ -42,6 +42,9 @@ cases = {
     + [RZZ(a, 11) for a in range(11)] + [RZZ(a, b) for a in range(5) for b in range(a + 1, 5)],
     "2tables8bit": [RZZ(a, b) for a in range(8) for b in range(a + 1, 8)] + [H(11)]
     + [RZZ(a, b) for a in range(4, 12) for b in range(a + 1, 12)],
+    "12H|fused k7 hi": "F1",
+    "12H|fused k9": "F2",
+    "12H|fused k7 lo(3 stay)": "F3",
     "sqs_k7_hi": "S1",
     "sqs_k7_lo": "S2",
     "sqs_k12": "S3",
@@ -50,7 +53,13 @@ only = os.environ.get("CASE")
 for name, gates in cases.items():
     if only and not name.startswith(only):
         continue
-    if gates == "S1":
+    if gates == "F1":
+        ins = [GateBlock(tuple(H(q) for q in range(12))), InMemSwap(tuple(range(5, 12)), tuple(range(12, 19)))]
+    elif gates == "F2":
+        ins = [GateBlock(tuple(H(q) for q in range(12))), InMemSwap(tuple(range(3, 12)), tuple(range(12, 21)))]
+    elif gates == "F3":
+        ins = [GateBlock(tuple(H(q) for q in range(12))), InMemSwap((0, 1, 2, 3, 4, 10, 11), tuple(range(12, 19)))]
+    elif gates == "S1":
         ins = [InMemSwap(tuple(range(5, 12)), tuple(range(12, 19)))]
     elif gates == "S2":
         ins = [InMemSwap((0, 1, 2, 3, 4, 10, 11), tuple(range(12, 19)))]
