@@ -38,6 +38,8 @@ WORKLOADS = {
     "qft33": ("qft33_c10_r0.txt", 33, 10, 0),
     "qft30": ("qft30_c10_r0.txt", 30, 10, 0),
     "qaoa26": ("qaoa26_c12_r0.txt", 26, 12, 0),
+    "qft26": ("qft26_c10_r0.txt", 26, 10, 0),
+    "qaoa24": ("qaoa24_c12_r0.txt", 24, 12, 0),
 }
 MULTI = {2: ("qaoa31_c12_r1.txt", 31, 12, 1), 4: ("qaoa32_c12_r2.txt", 32, 12, 2),
          8: ("qaoa33_c12_r3.txt", 33, 12, 3)}
@@ -200,7 +202,9 @@ def main():
     if world > 1 or args.gpus > 1:
         import torch.distributed as dist
         if not dist.is_initialized():
-            dist.init_process_group("gloo" if args.impl == "reference" else "nccl")
+            backend = os.environ.get("QK_BENCH_BACKEND",
+                                     "gloo" if args.impl == "reference" else "nccl")
+            dist.init_process_group(backend)
     if args.impl == "reference":
         rc = run_reference(args, world, rank)
         if world > 1:
@@ -310,15 +314,16 @@ def run_multi(args, world, rank, local):
     from paper_2406_14084_b200.distributed import ShardedSimulator
     fname, n, c, r = MULTI[world]
     text = open(os.path.join(CIRCUITS, fname)).read()
-    torch.cuda.set_device(local)
-    sim = ShardedSimulator(n, r, device=local)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    sim = ShardedSimulator(n, r, device=dev)
     perm = sim.load_text(text, c)
     for _ in range(args.warmup):
         sim.reset()
         sim.run(perm)
     sim.stats(reset=True)
     dist.barrier()
-    with ClockSampler(local) as clk:
+    with ClockSampler(dev) as clk:
         sim.sync()
         dist.barrier()
         t0 = time.perf_counter()
@@ -328,7 +333,9 @@ def run_multi(args, world, rank, local):
         sim.sync()
         dist.barrier()
         wall = time.perf_counter() - t0
-    t = torch.tensor([wall], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([wall], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = float(t.item()) / args.steps
     st = sim.stats()
@@ -348,7 +355,9 @@ def run_multi(args, world, rank, local):
         dist.barrier()
         if i >= args.warmup:
             e2e.append(time.perf_counter() - t0)
-    te = torch.tensor([float(np.mean(e2e))], dtype=torch.float64, device=f"cuda:{local}")
+    te = torch.tensor([float(np.mean(e2e))], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        te = te.cuda()
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
         emit({"metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
