@@ -881,7 +881,8 @@ struct qk_sim {
   // multi-process
   qk_barrier_fn barrier = nullptr;
   void* barrier_ctx = nullptr;
-  std::vector<double*> peers;  // by shard index
+  std::vector<double*> peers;   // by shard index: the peer's bufs[0]
+  std::vector<double*> peers1;  // the peer's bufs[1] (double-buffered shards)
   int nshards = 1, shard = 0;
 };
 
@@ -1316,7 +1317,23 @@ int compile_program(qk_sim* s) {
         }
         ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
       } else {
-        ip.sqs = -2;  // cross-process exchange (shard mode: sigma is the identity)
+        ip.sqs = -2;  // cross-process exchange: needs the reference layout
+        bool id = true;
+        for (int q = 0; q < nb; ++q) id = id && sigma[q] == q;
+        if (!id) {
+          std::vector<int> d(nb);
+          for (int q = 0; q < nb; ++q) d[sigma[q]] = q;
+          InstrPlan rp;
+          rp.type = QK_INS_BLOCK;
+          rp.dest = d;
+          InstrH empty;
+          empty.type = QK_INS_BLOCK;
+          int rc2 = compile_block(s->hp, empty, s->L, nb, rp, emsg, 10, Cg);
+          if (rc2 || rp.npass != 1) return fail(QK_ESIM, "internal: layout restore pass failed");
+          rp.synthetic = 1;
+          s->iplan.push_back(std::move(rp));
+          for (int q = 0; q < nb; ++q) sigma[q] = q;
+        }
       }
       ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
     }
@@ -1509,13 +1526,16 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   int rc = csqs_plan(s->n, s->r, s->count, s->shard, ip.a, ip.b, segs, in_a, in_b);
   if (rc) return rc;
   for (auto& sg : segs)
-    if (!s->peers[sg.peer]) return fail(QK_ESIM, "peer shard %d not mapped (qk_ipc_open)", (int)sg.peer);
+    if (!(s->cur ? s->peers1 : s->peers)[sg.peer])
+      return fail(QK_ESIM, "peer shard %d not mapped (qk_ipc_open)", (int)sg.peer);
   if (s->barrier) {
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
   }
   for (auto& sg : segs) {
-    rc = launch_swap_segments(s->state + 2 * sg.my_off, s->peers[sg.peer] + 2 * sg.peer_off, sg.len,
+    // every shard runs the same plan, so the peers' current buffer is bufs[cur] too
+    double* peer_state = (s->cur ? s->peers1 : s->peers)[sg.peer];
+    rc = launch_swap_segments(s->state + 2 * sg.my_off, peer_state + 2 * sg.peer_off, sg.len,
                               (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "peer exchange failed");
   }
@@ -1570,7 +1590,7 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   }
   s->state = s->bufs[0];
   // second buffer for out-of-place fused block+SQS passes when it fits comfortably
-  if (count == (1 << r) && !getenv("QK_INPLACE") && 2.0 * (double)need <= 0.90 * (double)free_b) {
+  if (!getenv("QK_INPLACE") && 2.0 * (double)need <= 0.90 * (double)free_b) {
     if (cudaMalloc(&s->bufs[1], need) != cudaSuccess) {
       cudaGetLastError();
       s->bufs[1] = nullptr;
@@ -1584,7 +1604,9 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   if (rc) return fail(QK_ECUDA, "state init failed");
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   s->peers.assign(s->nshards, nullptr);
-  s->peers[s->shard] = s->state;
+  s->peers1.assign(s->nshards, nullptr);
+  s->peers[s->shard] = s->bufs[0];
+  s->peers1[s->shard] = s->bufs[1];
   *out = s;
   return QK_OK;
 }
@@ -1672,6 +1694,8 @@ int qk_destroy(qk_sim* s) {
     if (e) cudaEventDestroy(e);
   for (size_t i = 0; i < s->peers.size(); ++i)
     if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
+  for (size_t i = 0; i < s->peers1.size(); ++i)
+    if ((int)i != s->shard && s->peers1[i]) cudaIpcCloseMemHandle(s->peers1[i]);
   if (s->bufs[0]) cudaFree(s->bufs[0]);
   if (s->bufs[1]) cudaFree(s->bufs[1]);
   if (s->blob) cudaFree(s->blob);
@@ -2142,25 +2166,40 @@ int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set, c
   return QK_OK;
 }
 
-int qk_ipc_handle(qk_sim* s, void* handle64) {
-  if (!s || !handle64) return fail(QK_EINVAL, "null argument");
+int qk_ipc_handle(qk_sim* s, void* handle128) {
+  if (!s || !handle128) return fail(QK_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(s->device));
-  cudaIpcMemHandle_t h;
-  CUDA_TRY(cudaIpcGetMemHandle(&h, s->state));
-  memcpy(handle64, &h, sizeof h);
+  unsigned char* out = static_cast<unsigned char*>(handle128);
+  memset(out, 0, 128);
+  for (int b = 0; b < 2; ++b) {
+    if (!s->bufs[b]) continue;
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, s->bufs[b]));
+    memcpy(out + 64 * b, &h, sizeof h);
+  }
   return QK_OK;
 }
 
-int qk_ipc_open(qk_sim* s, int peer, const void* handle64) {
-  if (!s || !handle64) return fail(QK_EINVAL, "null argument");
+int qk_ipc_open(qk_sim* s, int peer, const void* handle128) {
+  if (!s || !handle128) return fail(QK_EINVAL, "null argument");
   if (peer < 0 || peer >= s->nshards) return fail(QK_EINVAL, "bad peer shard %d", peer);
   if (peer == s->shard) return QK_OK;
   CUDA_TRY(cudaSetDevice(s->device));
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle64, sizeof h);
-  void* p = nullptr;
-  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-  s->peers[peer] = (double*)p;
+  const unsigned char* in = static_cast<const unsigned char*>(handle128);
+  for (int b = 0; b < 2; ++b) {
+    bool zero = true;
+    for (int i = 0; i < 64; ++i) zero = zero && in[64 * b + i] == 0;
+    if (zero) {
+      if (b == 1 && s->bufs[1]) return fail(QK_ESIM, "peer shard %d has no second buffer", peer);
+      continue;
+    }
+    if (b == 1 && !s->bufs[1]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, in + 64 * b, sizeof h);
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    (b ? s->peers1 : s->peers)[peer] = (double*)p;
+  }
   return QK_OK;
 }
 

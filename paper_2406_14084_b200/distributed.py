@@ -37,13 +37,13 @@ class ShardedSimulator:
         dev = self.rank if device is None else device
         self.h = _lib.Handle(n, r, self.b, dev, rank_lo=self.rank * self.count, count=self.count)
         # map every peer's state (CUDA IPC over NVLink)
-        buf = ctypes.create_string_buffer(64)
+        buf = ctypes.create_string_buffer(128)
         _lib.check(_lib.lib().qk_ipc_handle(self.h.ptr, buf))
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(buf.raw), group=group)
         for peer, hb in enumerate(handles):
             if peer != self.rank:
-                raw = ctypes.create_string_buffer(hb, 64)
+                raw = ctypes.create_string_buffer(hb, 128)
                 _lib.check(_lib.lib().qk_ipc_open(self.h.ptr, peer, raw))
         self._cb = _lib.BARRIER_FN(self._barrier)
         _lib.check(_lib.lib().qk_set_barrier(self.h.ptr, self._cb, None))
