@@ -31,7 +31,7 @@ enum OpCode : int32_t {
   OP_CX = 3,     // controlled X: target slot r0; control = slot r1 (ctrl_reg=1) or chunk-local position ctrl
   OP_SWAP = 4,   // swap register slots r0, r1
   OP_DIAG = 5,   // multiply by tables[table + (pt | pr[j])]
-  OP_SCALE = 6,  // multiply by coef[0]
+  OP_SCALE = 6,  // multiply by the complex coef[0] + i coef[1]
 };
 
 struct OpDesc {
@@ -74,7 +74,8 @@ struct TableDesc {
   int64_t out;            // offset (complex) of the table in the table pool
   int32_t bits;           // table has 2^bits entries
   int32_t g0, ng;         // gate range in the TableGate array
-  double scale;           // folded pass scale (H normalisation)
+  double scale;           // folded pass scale (H normalisation, factored 2x2 gates), real part
+  double scale_im;        // imaginary part
 };
 
 // SQS / single-device CSQS bit-permutation: new[i] = old[bitswap(i, A, B)]

@@ -17,6 +17,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -106,25 +107,6 @@ __device__ __forceinline__ u32 swz(u32 i) { return i ^ ((i >> 3) & 7u); }
 __device__ __forceinline__ void hb(double2& a, double2& b) {
   a.x += b.x; a.y += b.y; b.x = fma(-2.0, b.x, a.x); b.y = fma(-2.0, b.y, a.y); }
 __device__ __forceinline__ void xb(double2& a, double2& b) { double2 t = a; a = b; b = t; }
-__device__ __forceinline__ void mb(double2& a, double2& b, const double* m) {
-  double2 n0, n1;
-  n0.x = fma(m[0], a.x, fma(-m[1], a.y, fma(m[2], b.x, -m[3] * b.y)));
-  n0.y = fma(m[0], a.y, fma(m[1], a.x, fma(m[2], b.y, m[3] * b.x)));
-  n1.x = fma(m[4], a.x, fma(-m[5], a.y, fma(m[6], b.x, -m[7] * b.y)));
-  n1.y = fma(m[4], a.y, fma(m[5], a.x, fma(m[6], b.y, m[7] * b.x)));
-  a = n0; b = n1; }
-// real 2x2 (RY, Hadamard-like): 8 FP64 ops per pair
-__device__ __forceinline__ void mr(double2& a, double2& b, const double* m) {
-  double2 n0, n1;
-  n0.x = fma(m[0], a.x, m[2] * b.x); n0.y = fma(m[0], a.y, m[2] * b.y);
-  n1.x = fma(m[4], a.x, m[6] * b.x); n1.y = fma(m[4], a.y, m[6] * b.y);
-  a = n0; b = n1; }
-// real diagonal, imaginary off-diagonal (RX): 8 FP64 ops per pair
-__device__ __forceinline__ void mx(double2& a, double2& b, const double* m) {
-  double2 n0, n1;
-  n0.x = fma(m[0], a.x, -m[3] * b.y); n0.y = fma(m[0], a.y, m[3] * b.x);
-  n1.x = fma(m[6], b.x, -m[5] * a.y); n1.y = fma(m[6], b.y, m[5] * a.x);
-  a = n0; b = n1; }
 __device__ __forceinline__ double2 cm(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x)); }
 )CUDA";
@@ -133,6 +115,110 @@ struct Gen {
   std::ostringstream o;
   int ntab = 0, ncoef = 0;
 };
+
+// One real output of a 2x2 complex map as a minimal FMA chain: terms with
+// coefficient 0 vanish, +-1 are free adds, the rest read a parameter slot
+// (pushed to `coef`). Structure (which terms are 0 / +-1 / general) is part of
+// the kernel source; general values stay parameters.
+typedef std::map<double, int> SlotCache;  // value -> parameter slot (one gate's coefficients)
+
+std::string lin(const std::vector<std::pair<double, std::string>>& terms, std::vector<double>* coef,
+                SlotCache* cache) {
+  std::string e;
+  std::vector<std::pair<double, std::string>> gen;
+  for (auto& t : terms) {
+    if (t.first == 0.0) continue;
+    if (t.first == 1.0 || t.first == -1.0) {
+      const bool neg = t.first < 0;
+      if (e.empty()) e = neg ? "(-" + t.second + ")" : t.second;
+      else e = "(" + e + (neg ? " - " : " + ") + t.second + ")";
+    } else {
+      gen.push_back(t);
+    }
+  }
+  for (auto& t : gen) {
+    auto it = cache->find(t.first);
+    if (it == cache->end()) {
+      it = cache->emplace(t.first, (int)coef->size()).first;
+      coef->push_back(t.first);
+    }
+    const std::string c = "p.coef[" + std::to_string(it->second) + "]";
+    if (e.empty()) e = "(" + c + " * " + t.second + ")";
+    else e = "fma(" + c + ", " + t.second + ", " + e + ")";
+  }
+  return e.empty() ? "0.0" : e;
+}
+
+// n0 = m00 a + m01 b, n1 = m10 a + m11 b (m = 8 doubles: re, im row-major)
+void emit_mat(std::ostringstream& b, int j, int jj, const double* m, std::vector<double>* coef,
+              SlotCache* cache) {
+  const std::string A = "v[" + std::to_string(j) + "]", B = "v[" + std::to_string(jj) + "]";
+  auto out = [&](const double* r) {
+    // re: r0 a.x - r1 a.y + r2 b.x - r3 b.y ; im: r0 a.y + r1 a.x + r2 b.y + r3 b.x
+    std::string x = lin({{r[0], A + ".x"}, {-r[1], A + ".y"}, {r[2], B + ".x"}, {-r[3], B + ".y"}}, coef, cache);
+    std::string y = lin({{r[0], A + ".y"}, {r[1], A + ".x"}, {r[2], B + ".y"}, {r[3], B + ".x"}}, coef, cache);
+    return "make_double2(" + x + ", " + y + ")";
+  };
+  const std::string n0 = out(m), n1 = out(m + 4);
+  b << "    { const double2 n0 = " << n0 << ", n1 = " << n1 << "; " << A << " = n0; " << B << " = n1; }\n";
+}
+
+// ---- shared-memory layouts ---------------------------------------------------
+// A layout maps chunk index i to the 16-B slot i ^ sum_{p >= 3, bit p of i} m[p]
+// (m[p] < 8 only touches the bank bits 0..2, so it is a bijection). LDS.128 /
+// STS.128 are served 8 lanes at a time; lanes 0..2 of a phase sit on chunk
+// positions a0..a2, and the access is conflict-free iff their bank
+// contributions are linearly independent over GF(2). Phase 0 reads the TMA
+// SWIZZLE_128B image (m[3..5] = 1, 2, 4, nothing above); every later layout
+// is chosen per phase transition so that both the writing phase's lanes and
+// the reading phase's lanes are conflict-free.
+typedef std::vector<uint8_t> Layout;
+
+Layout sw128_layout(int C) {
+  Layout m(C, 0);
+  for (int p = 0; p < C; ++p) m[p] = p < 3 ? (uint8_t)(1u << p) : (p < 6 ? (uint8_t)(1u << (p - 3)) : 0);
+  return m;
+}
+
+bool indep3(uint8_t a, uint8_t b, uint8_t c) {
+  return a && b && c && a != b && (a ^ b) != c && a != c && b != c;
+}
+
+Layout choose_layout(int C, const uint8_t* wl, const uint8_t* rl) {
+  Layout m(C, 0);
+  for (int p = 0; p < 3 && p < C; ++p) m[p] = (uint8_t)(1u << p);
+  std::vector<int> freep;
+  for (int k = 0; k < 3; ++k) {
+    if (wl[k] >= 3 && std::find(freep.begin(), freep.end(), wl[k]) == freep.end()) freep.push_back(wl[k]);
+    if (rl[k] >= 3 && std::find(freep.begin(), freep.end(), rl[k]) == freep.end()) freep.push_back(rl[k]);
+  }
+  const int nf = (int)freep.size();
+  long long total = 1;
+  for (int k = 0; k < nf; ++k) total *= 7;
+  for (long long code = 0; code < total; ++code) {
+    long long c = code;
+    for (int k = 0; k < nf; ++k) {
+      m[freep[k]] = (uint8_t)(1 + c % 7);
+      c /= 7;
+    }
+    if (indep3(m[wl[0]], m[wl[1]], m[wl[2]]) && indep3(m[rl[0]], m[rl[1]], m[rl[2]])) return m;
+  }
+  return sw128_layout(C);  // no conflict-free choice (cannot happen for distinct lanes)
+}
+
+uint32_t lay(const Layout& m, uint32_t i) {
+  uint32_t s = i;
+  for (int p = 3; p < (int)m.size(); ++p)
+    if (i >> p & 1) s ^= m[p];
+  return s;
+}
+
+// base slot of a thread in layout m: XOR of its thread bits' slot contributions
+void emit_lay_base(std::ostringstream& o, const char* var, const Layout& m, const uint8_t* tpos, int n) {
+  o << "    const u32 " << var << " = 0u";
+  for (int k = 0; k < n; ++k) o << " ^ (((tid >> " << k << ") & 1u) * " << lay(m, 1u << tpos[k]) << "u)";
+  o << ";\n";
+}
 
 void emit_bits(std::ostringstream& o, const char* var, const char* src, const uint8_t* pos, int n) {
   o << "    const u32 " << var << " = 0u";
@@ -148,7 +234,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
                 std::vector<double>* coef) {
   const int C = tp.C, M = tp.M, T = C - M, NA = 1 << M;
   if (M != 4 && M != 3) return false;
-  std::ostringstream b;
+  std::ostringstream b, pro;  // pro: consumer prologue (loop-invariant table values)
   toff->clear();
   coef->clear();
   // tables and coefficients become parameter slots in program order
@@ -159,17 +245,29 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     }
   int ng = 0, st = 0;
   if (tma_smem_bytes(C, M, &ng, &st) < 0) return false;
+  // registers: 4 per complex entry, 2^M entries per table; one table for
+  // 16-amplitude threads, two for 8-amplitude threads
+  const char* hz = getenv("QK_JIT_HOIST");
+  const int hoist = std::min<int>((int)toff->size(), hz ? atoi(hz) : (M == 4 ? 1 : 2));
+  for (int t = 0; t < hoist; ++t) pro << "  double2 tv" << t << "[" << NA << "];\n";
   const int GT = 1 << T;
   const int consumers = GT * ng;
   const int rows_chunk = 1 << (C - 3);
   b << "    double2 v[" << NA << "];\n";
+  // layouts[k]: the smem image phase k reads (0: TMA SWIZZLE_128B)
+  std::vector<Layout> layouts(tp.nphases);
+  layouts[0] = sw128_layout(C);
+  for (int ph = 1; ph < tp.nphases; ++ph)
+    layouts[ph] = getenv("QK_JIT_SW128") ? sw128_layout(C) : choose_layout(C, tp.ph[ph - 1].tpos, tp.ph[ph].tpos);
   int tab_i = 0;
   for (int ph = 0; ph < tp.nphases; ++ph) {
     const TPhase& D = tp.ph[ph];
     const bool last = ph + 1 == tp.nphases;
     b << "    {  // phase " << ph << "\n";
     emit_bits(b, "lt", "tid", D.tpos, T);
-    for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = sm[swz(lt | " << D.rloc[j] << "u)];\n";
+    const Layout& rdl = layouts[ph];
+    emit_lay_base(b, "lr", rdl, D.tpos, T);
+    for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = sm[lr ^ " << lay(rdl, D.rloc[j]) << "u];\n";
     if (last) b << "    (void)0;\n";
     for (int o = D.op_begin; o < D.op_end; ++o) {
       const TOp& op = tp.ops[o];
@@ -178,33 +276,36 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           for (int s = 0; s < M; ++s) {
             const int k = op.st[s];
             if (!k) continue;
-            int ci = -1;
-            const char* fn = "mb";
-            if (k == 3) {
-              ci = (int)coef->size();
-              const double* m = tp.coef + op.cf[s];
-              for (int q = 0; q < 8; ++q) coef->push_back(m[q]);
-              // m = m00r m00i m01r m01i m10r m10i m11r m11i
-              if (m[1] == 0.0 && m[3] == 0.0 && m[5] == 0.0 && m[7] == 0.0) fn = "mr";
-              else if (m[1] == 0.0 && m[7] == 0.0 && m[2] == 0.0 && m[4] == 0.0) fn = "mx";
-            }
+            SlotCache cache;
             for (int j = 0; j < NA; ++j) {
               if (j & (1 << s)) continue;
               const int jj = j | (1 << s);
               if (k == 1) b << "    hb(v[" << j << "], v[" << jj << "]);\n";
               else if (k == 2) b << "    xb(v[" << j << "], v[" << jj << "]);\n";
-              else b << "    " << fn << "(v[" << j << "], v[" << jj << "], p.coef + " << ci << ");\n";
+              else emit_mat(b, j, jj, tp.coef + op.cf[s], coef, &cache);
             }
           }
           break;
         case OP_DIAG: {
-          b << "    { const double2* tb = p.tabs + p.toff[" << tab_i++ << "];\n";
-          b << "      const u32 pt = 0u";
+          // The table index is chunk-local: a thread reads the same 2^M
+          // entries for every chunk, so the first `hoist` tables are loaded
+          // once before the chunk loop and stay in registers.
+          const int ti = tab_i++;
+          std::ostringstream& dst = ti < hoist ? pro : b;
+          const std::string ind = ti < hoist ? "  " : "    ";
+          dst << ind << "{ const double2* tb = p.tabs + p.toff[" << ti << "];\n";
+          dst << ind << "  const u32 pt = 0u";
           for (int k = 0; k < T; ++k)
-            if (op.tcontrib[k]) b << " | (((tid >> " << k << ") & 1u) * " << op.tcontrib[k] << "u)";
-          b << ";\n";
-          for (int j = 0; j < NA; ++j) b << "      v[" << j << "] = cm(v[" << j << "], __ldg(tb + (pt | " << op.pr[j] << "u)));\n";
-          b << "    }\n";
+            if (op.tcontrib[k]) dst << " | (((tid >> " << k << ") & 1u) * " << op.tcontrib[k] << "u)";
+          dst << ";\n";
+          if (ti < hoist) {
+            for (int j = 0; j < NA; ++j) pro << "    tv" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
+            pro << "  }\n";
+            for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], tv" << ti << "[" << j << "]);\n";
+          } else {
+            for (int j = 0; j < NA; ++j) b << "      v[" << j << "] = cm(v[" << j << "], __ldg(tb + (pt | " << op.pr[j] << "u)));\n";
+            b << "    }\n";
+          }
           break;
         }
         case OP_CX: {
@@ -228,8 +329,14 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         case OP_SCALE: {
           const int ci = (int)coef->size();
           coef->push_back(tp.coef[op.coef]);
-          b << "    { const double sc = p.coef[" << ci << "];\n";
-          for (int j = 0; j < NA; ++j) b << "      v[" << j << "].x *= sc; v[" << j << "].y *= sc;\n";
+          coef->push_back(tp.coef[op.coef + 1]);
+          if (tp.coef[op.coef + 1] == 0.0) {
+            b << "    { const double sc = p.coef[" << ci << "];\n";
+            for (int j = 0; j < NA; ++j) b << "      v[" << j << "].x *= sc; v[" << j << "].y *= sc;\n";
+          } else {
+            b << "    { const double2 sc = make_double2(p.coef[" << ci << "], p.coef[" << ci + 1 << "]);\n";
+            for (int j = 0; j < NA; ++j) b << "      v[" << j << "] = cm(v[" << j << "], sc);\n";
+          }
           b << "    }\n";
           break;
         }
@@ -238,7 +345,9 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       }
     }
     if (!last) {
-      for (int j = 0; j < NA; ++j) b << "    sm[swz(lt | " << D.rloc[j] << "u)] = v[" << j << "];\n";
+      const Layout& wrl = layouts[ph + 1];
+      emit_lay_base(b, "lw", wrl, D.tpos, T);
+      for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(wrl, D.rloc[j]) << "u] = v[" << j << "];\n";
       b << "    gbar(bar_id, " << GT << ");\n";
     } else {
       b << "    fence_async_smem();\n    gbar(bar_id, " << GT << ");\n";
@@ -288,6 +397,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "  const int ct = threadIdx.x - 32;\n"
     << "  const int g = ct >> " << T << ";\n"
     << "  const u32 tid = ct & " << (GT - 1) << "u;\n"
+    << pro.str()
     << "  const int bar_id = 1 + g;\n"
     << "  for (u64 i = g;; i += " << ng << ") {\n"
     << "    const u64 chunk = blockIdx.x + i * G;\n"

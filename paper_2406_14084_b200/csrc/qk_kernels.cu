@@ -201,9 +201,9 @@ __global__ void __launch_bounds__(MAXT, 512 / MAXT + 1) k_block_pass(double2* __
       } else if (code == OP_SWAP) {
         swap_dispatch<M>(v, r0, op->r1);
       } else if (code == OP_SCALE) {
-        const double s = coef[op->coef];
+        const double2 s = make_double2(coef[op->coef], coef[op->coef + 1]);
 #pragma unroll
-        for (int j = 0; j < NA; ++j) v[j] = make_double2(v[j].x * s, v[j].y * s);
+        for (int j = 0; j < NA; ++j) v[j] = cmul(v[j], s);
       }
     }
     if (ph == np - 1) {
@@ -267,7 +267,7 @@ __global__ void k_build_tables(const TableDesc* __restrict__ T, const TableGate*
   const uint64_t n = 1ull << d.bits;
   for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
        x += (uint64_t)gridDim.x * blockDim.x) {
-    double2 acc = make_double2(d.scale, 0.0);
+    double2 acc = make_double2(d.scale, d.scale_im);
     for (int g = d.g0; g < d.g0 + d.ng; ++g) {
       const TableGate& tg = G[g];
       uint32_t sub = 0;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -338,6 +339,24 @@ void mat2(const GateH& g, cplx m[4]) {
   }
 }
 
+// m = lam * f with the larger of |m00|, |m01| factored out (exactly 1 in f).
+// A unitary 2x2 has |m00| = |m11| >= 1/sqrt2 or |m01| = |m10| >= 1/sqrt2, so
+// f stays well conditioned. The scalar lam is global to the pass (every
+// amplitude is touched by the gate) and joins the pass scale; the kernels then
+// apply f, whose exact ones and zeros (RX: 1 and -i tan, RY: 1 and +-tan)
+// make the butterfly 4 FMAs per pair instead of 8-16.
+void factor_mat(const cplx m[4], cplx f[4], cplx* lam) {
+  const int piv = std::abs(m[0]) >= std::abs(m[1]) ? 0 : 1;
+  const cplx l = m[piv];
+  auto div = [&](cplx x) {
+    if (l.imag() == 0.0) return cplx(x.real() / l.real(), x.imag() / l.real());
+    if (l.real() == 0.0) return cplx(x.imag() / l.imag(), -x.real() / l.imag());
+    return x / l;
+  };
+  for (int k = 0; k < 4; ++k) f[k] = k == piv ? cplx(1.0, 0.0) : div(m[k]);
+  *lam = l;
+}
+
 // ---------------------------------------------------------------------------
 // plans
 
@@ -369,18 +388,26 @@ struct InstrPlan {
 
 int popc(uint64_t x) { return __builtin_popcountll(x); }
 
-// thread-bit order: lane bits 0..2 on positions distinct mod 3 (swizzle-friendly)
+// thread-bit order: lane bits 0..2 (the 8 lanes of one 128-bit shared-memory
+// wavefront) on the lowest positions whose SWIZZLE_128B bank contributions
+// (p < 3: bit p, 3 <= p < 6: bit p-3, none above) are independent, so the TMA
+// image is read conflict-free; the remaining thread bits follow ascending, so
+// a phase without register qubits among 0..4 stores whole 512-B runs.
 std::vector<int> order_tpos(const std::vector<int>& T) {
   if (T.size() < 3) return T;
   std::vector<int> first;
+  uint32_t span = 1;  // bit x set: x is in the span of the chosen masks
   for (int p : T) {
-    bool ok = true;
-    for (int q : first)
-      if (q % 3 == p % 3) ok = false;
-    if (ok) first.push_back(p);
+    if (p >= 6) break;
+    const uint32_t m = 1u << (p % 3);
+    if (span >> m & 1) continue;
+    first.push_back(p);
+    uint32_t ns = span;
+    for (uint32_t x = 0; x < 8; ++x)
+      if (span >> x & 1) ns |= 1u << (x ^ m);
+    span = ns;
     if (first.size() == 3) break;
   }
-  if (first.size() < 3) return T;
   std::vector<int> out = first;
   for (int p : T)
     if (std::find(first.begin(), first.end(), p) == first.end()) out.push_back(p);
@@ -495,8 +522,21 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
   //    table. A run's table index bits are ordered for the phase that applies
   //    it: the lanes' positions first, then the register slots, so the 32
   //    lanes of a warp read one contiguous 512-B span of the table.
-  const double scale = (nh % 2 == 0) ? std::ldexp(1.0, -nh / 2) : std::ldexp(kSqrt1_2, -(nh - 1) / 2);
-  bool scale_folded = (nh == 0);
+  cplx scale = (nh % 2 == 0) ? std::ldexp(1.0, -nh / 2) : std::ldexp(kSqrt1_2, -(nh - 1) / 2);
+  std::vector<std::array<cplx, 4>> mat_f(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    const GateH* g = items[i].g;
+    if (items[i].type != 0 || (g->kind != QK_U && g->kind != QK_RX && g->kind != QK_RY)) continue;
+    cplx m[4], lam;
+    mat2(*g, m);
+    if (getenv("QK_NO_FACTOR")) {
+      for (int k = 0; k < 4; ++k) mat_f[i][k] = m[k];
+      continue;
+    }
+    factor_mat(m, mat_f[i].data(), &lam);
+    scale *= lam;
+  }
+  bool scale_folded = (scale == cplx(1.0, 0.0));
   std::vector<int64_t> run_table(runs.size(), -1);
   std::vector<std::vector<int>> run_bidx(runs.size());
   auto build_table = [&](int r, const std::vector<int>& order) -> int {
@@ -513,8 +553,10 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     td.g0 = (int)hp.tgates.size();
     td.ng = (int)runs[r].size();
     td.scale = 1.0;
+    td.scale_im = 0.0;
     if (!scale_folded) {
-      td.scale = scale;
+      td.scale = scale.real();
+      td.scale_im = scale.imag();
       scale_folded = true;
     }
     for (const GateH* g : runs[r]) {
@@ -623,10 +665,8 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
           case QK_RY: {
             op.code = OP_MAT;
             op.r0 = slot(loc[g->t[0]]);
-            cplx m[4];
-            mat2(*g, m);
             op.coef = (int)hp.coef.size();
-            for (auto& x : m) {
+            for (auto& x : mat_f[ii]) {
               hp.coef.push_back(x.real());
               hp.coef.push_back(x.imag());
             }
@@ -662,7 +702,8 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       OpDesc op{};
       op.code = OP_SCALE;
       op.coef = (int)hp.coef.size();
-      hp.coef.push_back(scale);
+      hp.coef.push_back(scale.real());
+      hp.coef.push_back(scale.imag());
       hp.ops.push_back(op);
       scale_folded = true;
     }
@@ -1002,9 +1043,11 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
           for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
           for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
           if (op.code == OP_SCALE) {
-            if (ncoef + 1 > kTMaxCoef) return false;
+            if (ncoef + 2 > kTMaxCoef) return false;
             tp.coef[ncoef] = hp.coef[op.coef];
-            t.coef = (int16_t)ncoef++;
+            tp.coef[ncoef + 1] = hp.coef[op.coef + 1];
+            t.coef = (int16_t)ncoef;
+            ncoef += 2;
           }
         }
       }
@@ -1094,6 +1137,13 @@ int upload_plan(qk_sim* s) {
       std::vector<long long> toff;
       std::vector<double> coef;
       if (!jit_source(s->tma[s->pass_tma[p]], &src, &toff, &coef)) continue;
+      if (const char* dd = getenv("QK_JIT_DUMP")) {
+        const std::string path = std::string(dd) + "/pass" + std::to_string(p) + ".cu";
+        if (FILE* f = fopen(path.c_str(), "w")) {
+          fwrite(src.data(), 1, src.size(), f);
+          fclose(f);
+        }
+      }
       srcs.push_back(std::move(src));
       src_pass.push_back((int)p);
       toffs.push_back(std::move(toff));
@@ -1167,7 +1217,7 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits) {
   if (pd.nouter != nbits - pd.C) return false;
   const int ob = hp.phases[pd.phase0].op_begin, oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
   int ncoef = 0;
-  for (int o = ob; o < oe; ++o) ncoef += hp.ops[o].code == OP_MAT ? 8 : (hp.ops[o].code == OP_SCALE ? 1 : 0);
+  for (int o = ob; o < oe; ++o) ncoef += hp.ops[o].code == OP_MAT ? 8 : (hp.ops[o].code == OP_SCALE ? 2 : 0);
   return oe - ob <= kTMaxOps && ncoef <= kTMaxCoef;
 }
 
@@ -1797,6 +1847,9 @@ int qk_run(qk_sim* s, double* timings) {
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
     const int c = s->iplan[i].type;
+    if (getenv("QK_DUMP_TIMES"))
+      fprintf(stderr, "instr %zu type %d pass0 %d passes %d permuted %d fused %d: %.3f ms\n", i, c, s->iplan[i].pass0, s->iplan[i].npass,
+              (int)s->iplan[i].permuted, (int)fused_away(s, s->iplan[i]), ms);
     cls[c] += ms;
     s->stat_ms[c] += ms;
     if (fused_away(s, s->iplan[i])) continue;

@@ -202,9 +202,10 @@ __device__ __forceinline__ void apply_ops(double2 (&v)[1 << M], const TmaParams&
         default: if constexpr (M > 3) swap_slots<M, 2, 3>(v); break;
       }
     } else if (code == OP_SCALE) {
-      const double s = p.coef[op.coef];
+      const double sr = p.coef[op.coef], si = p.coef[op.coef + 1];
 #pragma unroll
-      for (int j = 0; j < NA; ++j) v[j] = make_double2(v[j].x * s, v[j].y * s);
+      for (int j = 0; j < NA; ++j)
+        v[j] = make_double2(fma(v[j].x, sr, -v[j].y * si), fma(v[j].x, si, v[j].y * sr));
     }
   }
 }
