@@ -249,11 +249,12 @@ def run_single(args):
     st = h.stats()
     dev_per_step = sum(times) / args.steps           # device event time of the run
     value = dev_bracket / args.steps                 # CUDA events around K steps (incl. reset)
-    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb = st
+    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st
     peak, peak_kind = peaks()
     achieved_block = bb / (block_ms * 1e-3) / 1e9 if block_ms else 0.0
     achieved_sqs = sb / (sqs_ms * 1e-3) / 1e9 if sqs_ms else 0.0
-    achieved_all = (bb + sb + xb) / ((block_ms + sqs_ms + xrs_ms) * 1e-3) / 1e9
+    achieved_x = x_b / (x_ms * 1e-3) / 1e9 if x_ms else 0.0
+    achieved_all = (bb + sb + xb + x_b) / ((block_ms + sqs_ms + xrs_ms + x_ms) * 1e-3) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(prof):
@@ -287,14 +288,16 @@ def run_single(args):
                       "device_time_per_step_s": dev_per_step,
                       "host_wall_per_step_s": wall / args.steps,
                       "blocks_s": block_ms * 1e-3 / args.steps, "sqs_s": sqs_ms * 1e-3 / args.steps,
-                      "achieved_all_gbs": achieved_all, "achieved_sqs_gbs": achieved_sqs},
+                      "xblock_s": x_ms * 1e-3 / args.steps, "xblock_launches_per_step": x_n / args.steps,
+                      "achieved_all_gbs": achieved_all, "achieved_sqs_gbs": achieved_sqs,
+                      "achieved_xblock_gbs": achieved_x},
            "roofline": {"bound": "hbm", "achieved": achieved_block, "peak": peak,
                         "unit": "GB/s", "frac": achieved_block / peak, "traffic": traffic,
                         "kernel": "k_block_tma / qk_jit (persistent TMA gate-block pass)",
                         "peak_kind": peak_kind,
                         "algorithmic_bytes_per_launch": bb / max(1, block_n),
                         "launch_ms": block_ms / max(1, block_n)},
-           "gpu_launches": int(block_n + sqs_n + xrs_n) + args.steps,   # + 1 reset kernel per step
+           "gpu_launches": int(block_n + sqs_n + xrs_n + x_n) + args.steps,   # + 1 reset kernel per step
            "e2e": {"value": float(np.mean(e2e_vals)), "unit": "s",
                    "h2d_bytes_per_step": len(text.encode()),
                    "d2h_bytes_per_step": 8 + 16 * args.amps},
@@ -342,7 +345,7 @@ def run_multi(args, world, rank, local):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)          # max over ranks
     value = float(t.item()) / args.steps
     st = sim.stats()
-    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb = st
+    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st
     peak, peak_kind = peaks()
     achieved_block = bb / (block_ms * 1e-3) / 1e9 if block_ms else 0.0
     # e2e through the public API
@@ -376,7 +379,7 @@ def run_multi(args, world, rank, local):
                            "unit": "GB/s", "frac": achieved_block / peak, "traffic": None,
                            "kernel": "k_block_tma / qk_jit (gate-block pass)",
                            "peak_kind": peak_kind},
-              "gpu_launches": int(block_n + sqs_n + xrs_n),
+              "gpu_launches": int(block_n + sqs_n + xrs_n + x_n),
               "e2e": {"value": float(te.item()), "unit": "s",
                       "h2d_bytes_per_step": len(text.encode()),
                       "d2h_bytes_per_step": 8 + 16 * args.amps},

@@ -121,7 +121,9 @@ int qk_run(qk_sim* sim, double* timings);
 /* Per-kernel-class device time (ms) and launch count since the last reset of
  * the counters: out[0..5] = block_ms, block_launches, sqs_ms, sqs_launches,
  * xrs_ms, xrs_launches. Also algorithmic bytes: out[6] block bytes, out[7]
- * sqs bytes, out[8] xrs bytes. */
+ * sqs bytes, out[8] xrs bytes. out[9..11] = ms, launches and
+ * bytes of the cluster-exchange block passes (block + full chunk swap in one
+ * pass), which out[0..1] and out[6] exclude; out must hold 12 doubles. */
 int qk_kernel_stats(qk_sim* sim, double* out, int reset);
 
 /* Enable per-launch event timing (1) or per-instruction-class timing only (0). */

@@ -250,7 +250,7 @@ class Handle:
         return {"gate": float(t[0]), "ims": float(t[1]), "xrs": float(t[2])}, float(t[3])
 
     def stats(self, reset=False):
-        out = np.zeros(9, dtype=np.float64)
+        out = np.zeros(12, dtype=np.float64)
         check(lib().qk_kernel_stats(self.ptr, dptr(out), int(reset)))
         return out
 

@@ -127,6 +127,8 @@ struct alignas(64) TmaParams {
   int32_t direct_store;         // 1: last phase stores with STG.128, 0: TMA bulk store
   int32_t permuted;             // 1: last phase scatters to the post-SQS positions (out-of-place)
   int32_t nbits;
+  int32_t xbits;                // > 0: cluster-exchange store (qk_jit.cpp), 2^xbits CTAs per cluster
+  uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)
   uint64_t ldst_t[12];          // last phase: thread bit k -> destination offset
   uint64_t ldst_r[16];          // last phase: register amplitude j -> destination offset
@@ -150,6 +152,8 @@ bool jit_available();
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef);
 void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles);
 int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream);
+// cluster-exchange pass: 2^xbits CTAs per cluster, nsuper supertiles
+int jit_launch_x(void* kern, const void* params, int C, int M, int xbits, uint64_t nsuper, CUstream_st* stream);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);

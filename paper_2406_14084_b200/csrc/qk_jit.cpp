@@ -99,6 +99,22 @@ __device__ __forceinline__ void mbar_wait(u64* b, u32 parity) {
 __device__ __forceinline__ void tma_load(void* dst, const QkMap* map, int c0, int c1, u64* bar) {
   asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
                ::"r"(su32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(su32(bar)) : "memory"); }
+__device__ __forceinline__ void tma_prefetch(const QkMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1) : "memory"); }
+__device__ __forceinline__ u32 mapa(u32 a, u32 r) {
+  u32 d; asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(r)); return d; }
+__device__ __forceinline__ void mbar_arrive_remote(u32 rbar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory"); }
+__device__ __forceinline__ void mbar_wait_cl(u64* b, u32 parity) {
+  asm volatile("{\n\t.reg .pred P;\nQKC_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t@!P bra QKC_%=;\n}"
+               ::"r"(su32(b)), "r"(parity) : "memory"); }
+__device__ __forceinline__ double2 ld_cl(u32 a) {
+  double2 v; asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory"); return v; }
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+__device__ __forceinline__ u32 cl_rank() { u32 r; asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r)); return r; }
+__device__ __forceinline__ u32 cl_id() { u32 r; asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r)); return r; }
+__device__ __forceinline__ u32 cl_num() { u32 r; asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r)); return r; }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void gbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void st_cs(double2* p, double2 v) {
@@ -259,6 +275,27 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   layouts[0] = sw128_layout(C);
   for (int ph = 1; ph < tp.nphases; ++ph)
     layouts[ph] = getenv("QK_JIT_SW128") ? sw128_layout(C) : choose_layout(C, tp.ph[ph - 1].tpos, tp.ph[ph].tpos);
+  // Cluster-exchange store (xbits = X > 0): 2^X CTAs of a cluster hold the
+  // 2^X chunks of one supertile (cluster rank = the X spectator qubits). The
+  // last phase writes its chunk back to shared memory; after a cluster-wide
+  // `ready`, CTA b gathers the amplitudes whose X highest-destination chunk
+  // bits equal b from all 2^X CTAs (ld.shared::cluster) and stores them with
+  // the spectators on destination bits 0..X-1, i.e. whole 2^X-amplitude runs.
+  const int X = tp.xbits, NR = 1 << X;
+  std::vector<int> gb, jl, tj, rj;  // gather / lane / thread / register chunk positions
+  Layout lf;
+  if (X) {
+    if (T < 2 + X || X > 4) return false;
+    std::vector<int> ord;
+    for (int q = 0; q < C; ++q) ord.push_back(q);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int c) { return tp.dpos[a] < tp.dpos[c]; });
+    gb.assign(ord.end() - X, ord.end());
+    jl.assign(ord.begin(), ord.begin() + 2);
+    tj.assign(ord.begin() + 2, ord.begin() + 2 + (T - 2 - X));
+    rj.assign(ord.begin() + 2 + (T - 2 - X), ord.end() - X);
+    const uint8_t rl[3] = {(uint8_t)jl[0], (uint8_t)jl[1], (uint8_t)(tj.empty() ? rj[0] : tj[0])};
+    lf = choose_layout(C, tp.ph[tp.nphases - 1].tpos, rl);
+  }
   int tab_i = 0;
   for (int ph = 0; ph < tp.nphases; ++ph) {
     const TPhase& D = tp.ph[ph];
@@ -344,7 +381,40 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           return false;
       }
     }
-    if (!last) {
+    if (last && X) {
+      emit_lay_base(b, "lw", lf, D.tpos, T);
+      for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(lf, D.rloc[j]) << "u] = v[" << j << "];\n";
+      b << "    gbar(bar_id, " << GT << ");\n";
+      b << "    if (tid == 0)\n      for (u32 q = 0; q < " << NR << "u; ++q) mbar_arrive_remote(mapa(su32(ready + s), q));\n";
+      b << "    mbar_wait_cl(ready + s, round & 1u);\n";
+      b << "    {\n      const u32 rr = (tid >> 2) & " << NR - 1 << "u;\n";
+      b << "      const u32 rb = mapa(su32(sm), rr);\n";
+      // slot and destination of the thread's base amplitude
+      b << "      const u32 gs = 0u";
+      for (int k = 0; k < 2; ++k) b << " ^ (((tid >> " << k << ") & 1u) * " << lay(lf, 1u << jl[k]) << "u)";
+      for (size_t k = 0; k < tj.size(); ++k) b << " ^ (((tid >> " << 2 + X + k << ") & 1u) * " << lay(lf, 1u << tj[k]) << "u)";
+      for (int k = 0; k < X; ++k) b << " ^ (((rank >> " << k << ") & 1u) * " << lay(lf, 1u << gb[k]) << "u)";
+      b << ";\n      const u64 dst = dsup";
+      for (int k = 0; k < 2; ++k) b << " | ((u64)((tid >> " << k << ") & 1u) << " << (int)tp.dpos[jl[k]] << ")";
+      for (size_t k = 0; k < tj.size(); ++k) b << " | ((u64)((tid >> " << 2 + X + k << ") & 1u) << " << (int)tp.dpos[tj[k]] << ")";
+      for (int k = 0; k < X; ++k) b << " | ((u64)((rr >> " << k << ") & 1u) << " << (int)tp.dpos[tp.xpos[k]] << ")";
+      for (int k = 0; k < X; ++k) b << " | ((u64)((rank >> " << k << ") & 1u) << " << (int)tp.dpos[gb[k]] << ")";
+      b << ";\n";
+      for (int jj = 0; jj < NA; ++jj) {
+        uint32_t ci = 0;
+        for (int m = 0; m < M; ++m)
+          if (jj >> m & 1) ci |= 1u << rj[m];
+        b << "      v[" << jj << "] = ld_cl(rb + ((gs ^ " << lay(lf, ci) << "u) << 4));\n";
+      }
+      for (int jj = 0; jj < NA; ++jj) {
+        uint64_t d = 0;
+        for (int m = 0; m < M; ++m)
+          if (jj >> m & 1) d |= 1ull << tp.dpos[rj[m]];
+        b << "      st_cs(p.out + (dst | " << d << "ull), v[" << jj << "]);\n";
+      }
+      b << "    }\n    gbar(bar_id, " << GT << ");\n";
+      b << "    if (tid == 0)\n      for (u32 q = 0; q < " << NR << "u; ++q) mbar_arrive_remote(mapa(su32(done + s), q));\n";
+    } else if (!last) {
       const Layout& wrl = layouts[ph + 1];
       emit_lay_base(b, "lw", wrl, D.tpos, T);
       for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(wrl, D.rloc[j]) << "u] = v[" << j << "];\n";
@@ -369,6 +439,64 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   std::ostringstream o;
   o << "#define QK_NTAB " << toff->size() << "\n#define QK_NCOEF " << coef->size() << "\n";
   o << kPreamble;
+  if (X) {
+    // supertile u: outer source bits O (ascending) <- bits of u, spectators <- rank
+    std::vector<int> O;
+    for (int q = C; q < tp.nbits; ++q) {
+      bool sp = false;
+      for (int k = 0; k < X; ++k) sp = sp || tp.xpos[k] == q;
+      if (!sp) O.push_back(q);
+    }
+    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n"
+      << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
+      << "  unsigned char* base = smem_raw;\n"
+      << "  const u32 stage_bytes = " << (16u << C) << "u;\n"
+      << "  u64* full = (u64*)(base + " << (size_t)st * (16u << C) << "ull);\n"
+      << "  u64* done = full + " << st << ";\n"
+      << "  u64* ready = done + " << st << ";\n"
+      << "  if (threadIdx.x == 0) {\n"
+      << "    for (int s = 0; s < " << st << "; ++s) { mbar_init(full + s, 1); mbar_init(done + s, " << NR << "); mbar_init(ready + s, " << NR << "); }\n"
+      << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n"
+      << "  __syncthreads();\n"
+      << "  cluster_sync();\n"
+      << "  const u32 rank = cl_rank();\n"
+      << "  const u64 CID = cl_id(), NCL = cl_num();\n"
+      << "  if (threadIdx.x < 32) {\n"
+      << "    if (threadIdx.x == 0) {\n"
+      << "      asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&p.map) : \"memory\");\n"
+      << "      for (u64 i = 0;; ++i) {\n"
+      << "        const u64 u = CID + i * NCL;\n"
+      << "        if (u >= p.nchunks) break;\n"
+      << "        const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
+      << "        if (round > 0) { mbar_wait_cl(done + s, (round - 1) & 1u); fence_async_smem(); }\n"
+      << "        mbar_expect_tx(full + s, stage_bytes);\n"
+      << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n"
+      << "        const u64 caddr = 0ull";
+    for (size_t k = 0; k < O.size(); ++k) o << " | (((u >> " << k << ") & 1ull) << " << O[k] << ")";
+    for (int k = 0; k < X; ++k) o << " | ((u64)((rank >> " << k << ") & 1u) << " << (int)tp.xpos[k] << ")";
+    o << ";\n        const int row0 = (int)(caddr >> 3);\n";
+    for (int t = 0; t < tp.ntma; ++t)
+      o << "        tma_load(dst + " << t * tp.box_rows * 128 << ", &p.map, 0, row0 + " << t * tp.box_rows << ", full + s);\n";
+    o << "      }\n    }\n    __syncwarp();\n  } else {\n"
+      << "  const int ct = threadIdx.x - 32;\n"
+      << "  const int g = ct >> " << T << ";\n"
+      << "  const u32 tid = ct & " << (GT - 1) << "u;\n"
+      << pro.str()
+      << "  const int bar_id = 1 + g;\n"
+      << "  for (u64 i = g;; i += " << ng << ") {\n"
+      << "    const u64 u = CID + i * NCL;\n"
+      << "    if (u >= p.nchunks) break;\n"
+      << "    const u64 dsup = 0ull";
+    for (size_t k = 0; k < O.size(); ++k) o << " | (((u >> " << k << ") & 1ull) << " << (int)tp.dpos[O[k]] << ")";
+    o << ";\n"
+      << "    const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
+      << "    double2* sm = (double2*)(base + (size_t)s * stage_bytes);\n"
+      << "    mbar_wait(full + s, round & 1u);\n"
+      << b.str()
+      << "  }\n  }\n  cluster_sync();\n}\n";
+    *src = o.str();
+    return true;
+  }
   o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n"
     << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
     << "  unsigned char* base = smem_raw;\n"
@@ -393,6 +521,16 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "        const int row0 = (int)(chunk * " << rows_chunk << "ull);\n";
   for (int t = 0; t < tp.ntma; ++t)
     o << "        tma_load(dst + " << t * tp.box_rows * 128 << ", &p.map, 0, row0 + " << t * tp.box_rows << ", full + s);\n";
+  // with a shallow ring, pull the chunk that will refill this stage into L2
+  // now, so its load hits L2 when the stage is released
+  const char* pfe = getenv("QK_JIT_PREFETCH");
+  if (pfe ? atoi(pfe) != 0 : st <= 2) {
+    o << "        if (chunk + " << st << "ull * G < p.nchunks) {\n"
+      << "          const int prow = (int)((chunk + " << st << "ull * G) * " << rows_chunk << "ull);\n";
+    for (int t = 0; t < tp.ntma; ++t)
+      o << "          tma_prefetch(&p.map, 0, prow + " << t * tp.box_rows << ");\n";
+    o << "        }\n";
+  }
   o << "      }\n    }\n    return;\n  }\n"
     << "  const int ct = threadIdx.x - 32;\n"
     << "  const int g = ct >> " << T << ";\n"
@@ -562,6 +700,63 @@ int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, i
   cudaError_t e = cudaLaunchKernel((const void*)kern, dim3((unsigned)grid), dim3(threads), args, smem,
                                    reinterpret_cast<cudaStream_t>(stream));
   return (int)e;
+}
+
+// Launch a cluster-exchange pass: 2^xbits CTAs per cluster, as many
+// resident clusters as fit (persistent over the nsuper supertiles).
+int jit_launch_x(void* kern, const void* params, int C, int M, int xbits, uint64_t nsuper, CUstream_st* stream) {
+  int ng = 0, st = 0;
+  const int smem0 = tma_smem_bytes(C, M, &ng, &st);
+  if (smem0 < 0) return -1;
+  const int smem = smem0 + 8 * st;  // + the `ready` barriers
+  const int threads = 32 + (1 << (C - M)) * ng;
+  const int csize = 1 << xbits;
+  static std::mutex mu;
+  static std::map<std::pair<void*, int>, int> max_clusters;
+  int ncl = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(kern, smem);
+    auto it = max_clusters.find(key);
+    if (it == max_clusters.end()) {
+      if (csize > 8) cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = csize;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(csize * 64);
+      cfg.blockDim = dim3(threads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      if (getenv("QK_JIT_VERBOSE")) fprintf(stderr, "qk_jit: cluster %d: %d resident clusters\n", csize, n);
+      it = max_clusters.emplace(key, n).first;
+    }
+    ncl = it->second;
+  }
+  if (ncl <= 0) return (int)cudaErrorLaunchOutOfResources;
+  const uint64_t grid_cl = nsuper < (uint64_t)ncl ? nsuper : (uint64_t)ncl;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)(grid_cl * csize));
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<void*>(params)};
+  return (int)cudaLaunchKernelExC(&cfg, (const void*)kern, args);
 }
 
 }  // namespace qk

@@ -380,6 +380,7 @@ struct InstrPlan {
   int permuted = 0;          // block: last pass scatters out-of-place (set at upload)
   int fused_by = -1;         // SQS/CSQS: index of the block whose last pass absorbs it
   int synthetic = 0;         // block: layout-restore pass appended by the planner
+  std::vector<int> xspec;    // block: spectator source bits of a cluster-exchange store (qk_jit.cpp)
   int sqs = -1;              // SQS / single-device CSQS
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
@@ -732,7 +733,8 @@ int block_chunk_width(const InstrH& ins, int L, int cmin = 10) {
 
 int compile_block(HostPlan& hp, const InstrH& ins, int L, int nbits, InstrPlan& ip,
                   std::string& emsg, int cmin = 10, int cfix = 0) {
-  const std::vector<int>* dest = ip.dest.empty() ? nullptr : &ip.dest;
+  // a cluster-exchange store permutes through shared memory: no lane constraints
+  const std::vector<int>* dest = (ip.dest.empty() || !ip.xspec.empty()) ? nullptr : &ip.dest;
   int maxt = -1;
   for (auto& g : ins.gates)
     for (int t : g.t) maxt = std::max(maxt, t);
@@ -907,9 +909,10 @@ struct qk_sim {
   std::vector<cudaEvent_t> events;
   cudaEvent_t marks[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   int per_launch = 0;
-  double stat_ms[3] = {0, 0, 0};
-  double stat_launch[3] = {0, 0, 0};
-  double stat_bytes[3] = {0, 0, 0};
+  // per kernel class: block passes, SQS, CSQS, cluster-exchange block passes
+  double stat_ms[4] = {0, 0, 0, 0};
+  double stat_launch[4] = {0, 0, 0, 0};
+  double stat_bytes[4] = {0, 0, 0, 0};
   // persistent TMA passes
   int num_sms = 148;
   bool allow_tma = true;
@@ -979,9 +982,10 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
   return &s->maps[buf][slot];
 }
 
-bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<int>* dest) {
+bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<int>* dest,
+              const std::vector<int>* xspec = nullptr) {
   if (getenv("QK_NO_TMA")) return false;
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || s->nbits > 34) return false;
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > (getenv("QK_TMA13") ? 13 : 12) || pd.nphases > kTMaxPh || s->nbits > 34) return false;
   if (pd.nouter != s->nbits - pd.C) return false;
   for (int k = 0; k < pd.nouter; ++k)
     if (pd.opos[k] != pd.C + k) return false;
@@ -1005,6 +1009,10 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
     }
   }
   tp.nchunks = 1ull << (s->nbits - pd.C);
+  if (xspec && !xspec->empty()) {
+    tp.xbits = (int)xspec->size();
+    for (int k = 0; k < tp.xbits; ++k) tp.xpos[k] = (uint8_t)(*xspec)[k];
+  }
   tp.C = pd.C;
   tp.M = pd.M;
   tp.nphases = pd.nphases;
@@ -1103,14 +1111,17 @@ int upload_plan(qk_sim* s) {
   }
   s->tma.clear();
   s->pass_tma.assign(hp.passes.size(), -1);
-  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr);
+  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr), pass_x(hp.passes.size(), nullptr);
   for (auto& ip : s->iplan) {
     ip.permuted = 0;
-    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) pass_dest[ip.pass0 + ip.npass - 1] = &ip.dest;
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) {
+      pass_dest[ip.pass0 + ip.npass - 1] = &ip.dest;
+      pass_x[ip.pass0 + ip.npass - 1] = &ip.xspec;
+    }
   }
   for (size_t p = 0; p < hp.passes.size(); ++p) {
     TmaParams tp;
-    if (make_tma(s, hp.passes[p], tp, pass_dest[p])) {
+    if (make_tma(s, hp.passes[p], tp, pass_dest[p], pass_x[p])) {
       s->pass_tma[p] = (int)s->tma.size();
       s->tma.push_back(tp);
     }
@@ -1157,7 +1168,8 @@ int upload_plan(qk_sim* s) {
       // QkJitParams: map[16 words] | tabs | state | out | nchunks | toff[ntab+1] | coef[ncoef+1]
       std::vector<uint64_t> blob(16 + 4 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
       blob[16] = (uint64_t)(uintptr_t)s->d_pool;
-      blob[19] = s->tma[s->pass_tma[p]].nchunks;
+      const TmaParams& tq = s->tma[s->pass_tma[p]];
+      blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
       for (size_t k = 0; k < toffs[i].size(); ++k) blob[20 + k] = (uint64_t)toffs[i][k];
       const size_t co = 20 + toffs[i].size() + 1;
       for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
@@ -1213,7 +1225,7 @@ int check_csqs(const qk_sim* s, const std::vector<int>& local_set, const std::ve
 bool tma_plan_ok(const HostPlan& hp, int pass, int nbits) {
   if (getenv("QK_NO_TMA")) return false;
   const PassDesc& pd = hp.passes[pass];
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > 12 || pd.nphases > kTMaxPh || nbits > 34) return false;
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > (getenv("QK_TMA13") ? 13 : 12) || pd.nphases > kTMaxPh || nbits > 34) return false;
   if (pd.nouter != nbits - pd.C) return false;
   const int ob = hp.phases[pd.phase0].op_begin, oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
   int ncoef = 0;
@@ -1241,6 +1253,9 @@ int compile_program(qk_sim* s) {
     Cg = std::max(Cg, w);
   }
   if (Cg < 9 || Cg > 12 || Cg > nb) relabel = false;
+  // cluster-exchange fusion needs the load-time specialised kernels
+  const char* jenv = getenv("QK_JIT");
+  const bool xfuse = relabel && !getenv("QK_NO_XFUSE") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   std::vector<int> sigma(nb);
   for (int q = 0; q < nb; ++q) sigma[q] = q;
   std::vector<char> fused(s->prog.size(), 0);
@@ -1294,12 +1309,66 @@ int compile_program(qk_sim* s) {
           best_d = d;
           best_j = j + 1;
         }
+        // No run keeps 5 chunk qubits on the lanes (e.g. QAOA's full 12-qubit
+        // chunk swaps): fuse the first swap run through a cluster exchange.
+        // X = 3 incoming qubits become the cluster rank (spectators) and land
+        // on destination bits 0..2, so the gathered stores are 128-B runs and
+        // the next chunk is contiguous again.
+        std::vector<int> xspec;
+        if (best_d.empty() && xfuse) {
+          std::vector<int> P2(nb);
+          for (int q = 0; q < nb; ++q) P2[q] = q;
+          size_t j = ii + 1;
+          for (; j < s->prog.size() && s->prog[j].type == QK_INS_SQS && !s->prog[j].a.empty(); ++j) {
+            std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
+            bool ok = true;
+            for (int q : a) ok = ok && q >= 0 && q < s->L;
+            for (int q : b) ok = ok && q >= 0 && q < s->L;
+            if (!ok) break;
+            std::sort(a.begin(), a.end());
+            std::sort(b.begin(), b.end());
+            for (size_t k = 0; k < a.size(); ++k) std::swap(P2[a[k]], P2[b[k]]);
+          }
+          if (j > ii + 1) {
+            std::vector<char> in_next(nb, 0);
+            for (int q = 0; q < Cg; ++q) in_next[sigma[P2[q]]] = 1;
+            std::vector<int> incoming, stay, other_in, leaving, rest;
+            for (int a2 = 0; a2 < nb; ++a2) {
+              if (in_next[a2] && a2 >= Cg) incoming.push_back(a2);
+              else if (in_next[a2]) stay.push_back(a2);
+              else if (a2 < Cg) leaving.push_back(a2);
+              else rest.push_back(a2);
+            }
+            const int X = 3;
+            if ((int)incoming.size() >= X) {
+              std::vector<int> d(nb);
+              int pos = 0;
+              for (int k = 0; k < X; ++k) {
+                xspec.push_back(incoming[k]);
+                d[incoming[k]] = pos++;
+              }
+              for (int x : stay) d[x] = pos++;
+              for (size_t k = X; k < incoming.size(); ++k) d[incoming[k]] = pos++;
+              for (int x : leaving) d[x] = pos++;
+              for (int x : rest) d[x] = pos++;
+              P = P2;
+              best_d = d;
+              best_j = j;
+            }
+          }
+        }
         if (!best_d.empty()) {
           ip.dest = best_d;
+          ip.xspec = xspec;
           const size_t hp_passes = s->hp.passes.size();
           int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, Cg);
           if (rc) return fail(rc, "%s", emsg.c_str());
-          if (ip.npass == 1 && tma_plan_ok(s->hp, (int)hp_passes, nb)) {
+          // The cluster exchange moves 7/8 of every chunk over DSMEM (~20 B/clk
+          // per SM), so an exchange pass costs ~1.6x a plain pass whatever its
+          // gates: it beats block + separate SQS only for single-phase blocks.
+          const bool x_ok = xspec.empty() || getenv("QK_XFUSE_ALL") ||
+                            (ip.npass == 1 && s->hp.passes[hp_passes].nphases == 1);
+          if (ip.npass == 1 && x_ok && tma_plan_ok(s->hp, (int)hp_passes, nb)) {
             std::vector<int> ns(nb);
             for (int q = 0; q < nb; ++q) ns[q] = best_d[sigma[P[q]]];
             sigma = ns;
@@ -1319,6 +1388,7 @@ int compile_program(qk_sim* s) {
           // not fusable after all: recompile in place (drop the permuted pass)
           s->hp.passes.resize(hp_passes);
           ip.dest.clear();
+          ip.xspec.clear();
         }
       }
       int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, relabel ? Cg : 0);
@@ -1460,7 +1530,9 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       memcpy(blob.data(), map, 128);
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
-      rc = jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream);
+      rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
+                                   (CUstream_st*)s->stream)
+                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream);
     } else {
       rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
     }
@@ -1851,10 +1923,14 @@ int qk_run(qk_sim* s, double* timings) {
       fprintf(stderr, "instr %zu type %d pass0 %d passes %d permuted %d fused %d: %.3f ms\n", i, c, s->iplan[i].pass0, s->iplan[i].npass,
               (int)s->iplan[i].permuted, (int)fused_away(s, s->iplan[i]), ms);
     cls[c] += ms;
-    s->stat_ms[c] += ms;
-    if (fused_away(s, s->iplan[i])) continue;
-    s->stat_bytes[c] += s->iplan[i].bytes;
-    s->stat_launch[c] += c == QK_INS_BLOCK ? s->iplan[i].npass : (s->iplan[i].sqs != -1 ? 1 : 0);
+    const InstrPlan& ip = s->iplan[i];
+    const bool xp = c == QK_INS_BLOCK && ip.npass > 0 && s->pass_tma[ip.pass0 + ip.npass - 1] >= 0 &&
+                    s->tma[s->pass_tma[ip.pass0 + ip.npass - 1]].xbits > 0;
+    const int sc = xp ? 3 : c;
+    s->stat_ms[sc] += ms;
+    if (fused_away(s, ip)) continue;
+    s->stat_bytes[sc] += ip.bytes;
+    s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
   }
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (timings) {
@@ -1874,8 +1950,13 @@ int qk_kernel_stats(qk_sim* s, double* out, int reset) {
       out[2 * c + 1] = s->stat_launch[c];
       out[6 + c] = s->stat_bytes[c];
     }
+  if (out) {
+    out[9] = s->stat_ms[3];
+    out[10] = s->stat_launch[3];
+    out[11] = s->stat_bytes[3];
+    }
   if (reset)
-    for (int c = 0; c < 3; ++c) s->stat_ms[c] = s->stat_launch[c] = s->stat_bytes[c] = 0;
+    for (int c = 0; c < 4; ++c) s->stat_ms[c] = s->stat_launch[c] = s->stat_bytes[c] = 0;
   return QK_OK;
 }
 

@@ -327,7 +327,8 @@ def test_bv_basis_state_30_qubits(gpu):
 
 # ---------------------------------------------------------------------------
 # at scale: every execution strategy must agree (persistent-ring stage reuse,
-# fused out-of-place SQS, interpreter fallback) on reference-optimized circuits
+# fused out-of-place SQS, cluster-exchange SQS, interpreter fallback) on
+# reference-optimized circuits
 
 
 @pytest.mark.parametrize("name,n,c", [("qaoa24_c12_r0", 24, 12), ("qft26_c10_r0", 26, 10)])
@@ -336,7 +337,7 @@ def test_execution_strategies_agree_at_scale(gpu, name, n, c):
     from conftest import ROOT
     text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
     outs = {}
-    for mode in ("default", "QK_NO_FUSE", "QK_NO_TMA", "QK_NO_JIT"):
+    for mode in ("default", "QK_XFUSE_ALL", "QK_NO_XFUSE", "QK_NO_FUSE", "QK_NO_TMA", "QK_NO_JIT"):
         if mode != "default":
             os.environ[mode] = "1"
         try:

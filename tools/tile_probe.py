@@ -26,7 +26,13 @@ cases = {
     "mem diag20..29": [RZZ(a, a + 1) for a in range(20, 29)],
     "mem H23..32": [H(q) for q in range(n - 10, n)],
     "mem H 10..19": [H(q) for q in range(10, 20)],
+    "chunk H0..11": [H(q) for q in range(12)],
+    "chunk H0..12": [H(q) for q in range(13)],
+    "chunk diag0..12": [RZZ(a, a + 1) for a in range(12)],
 }
+only = os.environ.get("CASES")
+if only:
+    cases = {k: v for k, v in cases.items() if k.startswith(tuple(only.split(",")))}
 for name, gates in cases.items():
     sim.load([GateBlock(tuple(gates))])
     for _ in range(2):
