@@ -273,8 +273,15 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // layouts[k]: the smem image phase k reads (0: TMA SWIZZLE_128B)
   std::vector<Layout> layouts(tp.nphases);
   layouts[0] = sw128_layout(C);
-  for (int ph = 1; ph < tp.nphases; ++ph)
-    layouts[ph] = getenv("QK_JIT_SW128") ? sw128_layout(C) : choose_layout(C, tp.ph[ph - 1].tpos, tp.ph[ph].tpos);
+  // keep the previous layout when the next phase's lanes are conflict-free
+  // under it too: an unchanged layout needs no barrier between a phase's
+  // reads and its writes
+  for (int ph = 1; ph < tp.nphases; ++ph) {
+    const Layout& prev = layouts[ph - 1];
+    const uint8_t* rl = tp.ph[ph].tpos;
+    if (getenv("QK_JIT_SW128") || indep3(prev[rl[0]], prev[rl[1]], prev[rl[2]])) layouts[ph] = prev;
+    else layouts[ph] = choose_layout(C, tp.ph[ph - 1].tpos, rl);
+  }
   // Cluster-exchange store (xbits = X > 0): 2^X CTAs of a cluster hold the
   // 2^X chunks of one supertile (cluster rank = the X spectator qubits). The
   // last phase writes its chunk back to shared memory; after a cluster-wide
@@ -294,7 +301,8 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     tj.assign(ord.begin() + 2, ord.begin() + 2 + (T - 2 - X));
     rj.assign(ord.begin() + 2 + (T - 2 - X), ord.end() - X);
     const uint8_t rl[3] = {(uint8_t)jl[0], (uint8_t)jl[1], (uint8_t)(tj.empty() ? rj[0] : tj[0])};
-    lf = choose_layout(C, tp.ph[tp.nphases - 1].tpos, rl);
+    const Layout& ll = layouts[tp.nphases - 1];
+    lf = indep3(ll[rl[0]], ll[rl[1]], ll[rl[2]]) ? ll : choose_layout(C, tp.ph[tp.nphases - 1].tpos, rl);
   }
   int tab_i = 0;
   for (int ph = 0; ph < tp.nphases; ++ph) {
@@ -382,10 +390,18 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       }
     }
     if (last && X) {
+      // a thread rewrites its own amplitudes, but at other slots when the
+      // layout changes: every read of the phase must land first
+      if (lf != rdl) b << "    gbar(bar_id, " << GT << ");\n";
       emit_lay_base(b, "lw", lf, D.tpos, T);
       for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(lf, D.rloc[j]) << "u] = v[" << j << "];\n";
+      // generic writes of the stage must be ordered before the TMA (async
+      // proxy) refill that follows the `done` exchange
+      b << "    fence_async_smem();\n";
       b << "    gbar(bar_id, " << GT << ");\n";
-      b << "    if (tid == 0)\n      for (u32 q = 0; q < " << NR << "u; ++q) mbar_arrive_remote(mapa(su32(ready + s), q));\n";
+      b << "    if (tid == 0) {\n";
+      if (getenv("QK_X_FENCE")) b << "      asm volatile(\"fence.acq_rel.cluster;\" ::: \"memory\");\n";
+      b << "      for (u32 q = 0; q < " << NR << "u; ++q) mbar_arrive_remote(mapa(su32(ready + s), q));\n    }\n";
       b << "    mbar_wait_cl(ready + s, round & 1u);\n";
       b << "    {\n      const u32 rr = (tid >> 2) & " << NR - 1 << "u;\n";
       b << "      const u32 rb = mapa(su32(sm), rr);\n";
@@ -416,6 +432,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       b << "    if (tid == 0)\n      for (u32 q = 0; q < " << NR << "u; ++q) mbar_arrive_remote(mapa(su32(done + s), q));\n";
     } else if (!last) {
       const Layout& wrl = layouts[ph + 1];
+      if (wrl != rdl) b << "    gbar(bar_id, " << GT << ");\n";
       emit_lay_base(b, "lw", wrl, D.tpos, T);
       for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(wrl, D.rloc[j]) << "u] = v[" << j << "];\n";
       b << "    gbar(bar_id, " << GT << ");\n";
@@ -447,7 +464,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       for (int k = 0; k < X; ++k) sp = sp || tp.xpos[k] == q;
       if (!sp) O.push_back(q);
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jitx(const __grid_constant__ QkJitParams p) {\n"
       << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
       << "  unsigned char* base = smem_raw;\n"
       << "  const u32 stage_bytes = " << (16u << C) << "u;\n"
@@ -676,7 +693,8 @@ void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles
       Entry* e = ents[k];
       if (e->failed) continue;
       if (cudaLibraryLoadData(&e->lib, e->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-          cudaLibraryGetKernel(&e->kern, e->lib, "qk_jit") != cudaSuccess) {
+          (cudaLibraryGetKernel(&e->kern, e->lib, "qk_jit") != cudaSuccess &&
+           cudaLibraryGetKernel(&e->kern, e->lib, "qk_jitx") != cudaSuccess)) {
         cudaGetLastError();
         e->failed = true;
         continue;

@@ -331,7 +331,8 @@ def test_bv_basis_state_30_qubits(gpu):
 # reference-optimized circuits
 
 
-@pytest.mark.parametrize("name,n,c", [("qaoa24_c12_r0", 24, 12), ("qft26_c10_r0", 26, 10)])
+@pytest.mark.parametrize("name,n,c", [("qaoa24_c12_r0", 24, 12), ("qaoa26_c12_r0", 26, 12),
+                                      ("qft26_c10_r0", 26, 10)])
 def test_execution_strategies_agree_at_scale(gpu, name, n, c):
     import os
     from conftest import ROOT
