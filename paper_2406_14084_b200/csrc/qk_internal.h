@@ -128,6 +128,8 @@ struct alignas(64) TmaParams {
   int32_t permuted;             // 1: last phase scatters to the post-SQS positions (out-of-place)
   int32_t nbits;
   int32_t xbits;                // > 0: cluster-exchange store (qk_jit.cpp), 2^xbits CTAs per cluster
+  int32_t lazy;                 // 1: strided tile (tbit) loaded through `map` (N-D), stored in place
+  uint8_t tbit[16];             // lazy: physical address bit of every chunk-local bit (ascending)
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)
   uint64_t ldst_t[12];          // last phase: thread bit k -> destination offset
@@ -136,6 +138,58 @@ struct alignas(64) TmaParams {
   TOp ops[kTMaxOps];
   double coef[kTMaxCoef];
 };
+
+// ---- strided tiles of the lazy in-place layout ------------------------------------
+// A tile is 2^C amplitudes at physical address bits T (ascending, always
+// containing bits 0..2). The TMA view: dim 0 = bits 0..2 as 16 doubles (128-B
+// rows, SWIZZLE_128B), then one dim per maximal run of tile / non-tile bits
+// (tile runs split into <= 8-bit dims, box = full extent; non-tile dims box 1).
+// When that needs more than 5 dims, everything from the 5th dim up is one
+// merged dim with box 1, and the tile bits inside it are iterated by separate
+// loads (they are the top chunk-local bits, so each load fills one contiguous
+// slice of the stage).
+struct TileDims {
+  int rank;
+  int lo[5], len[5], box[5];
+  int inbox;         // chunk-local bits covered by one box
+  int nit;           // iterated chunk-local bits (the top ones)
+};
+
+inline bool tile_dims(const uint8_t* T, int C, int nbits, TileDims* d) {
+  if (C < 3 || C > 16 || nbits > 48 || T[0] != 0 || T[1] != 1 || T[2] != 2) return false;
+  bool in[64] = {false};
+  for (int k = 0; k < C; ++k) in[T[k]] = true;
+  int lo[64], len[64], box[64];
+  bool tile[64];
+  int nd = 0;
+  lo[0] = 0; len[0] = 3; box[0] = 16; tile[0] = true; nd = 1;
+  for (int p = 3; p < nbits;) {
+    int q = p;
+    while (q < nbits && in[q] == in[p]) ++q;
+    if (in[p]) {
+      for (int a = p; a < q; a += 8) {
+        const int l = (q - a) < 8 ? (q - a) : 8;
+        lo[nd] = a; len[nd] = l; box[nd] = 1 << l; tile[nd] = true; ++nd;
+      }
+    } else {
+      lo[nd] = p; len[nd] = q - p; box[nd] = 1; tile[nd] = false; ++nd;
+    }
+    p = q;
+  }
+  d->inbox = 0;
+  if (nd <= 5) {
+    d->rank = nd;
+  } else {
+    d->rank = 5;
+    lo[4] = lo[4]; len[4] = nbits - lo[4]; box[4] = 1; tile[4] = false;
+  }
+  for (int j = 0; j < d->rank; ++j) {
+    d->lo[j] = lo[j]; d->len[j] = len[j]; d->box[j] = box[j];
+    if (tile[j]) d->inbox += j == 0 ? 3 : len[j];
+  }
+  d->nit = C - d->inbox;
+  return d->nit >= 0 && d->nit <= 6;
+}
 
 }  // namespace qk
 

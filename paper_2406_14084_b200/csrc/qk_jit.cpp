@@ -242,6 +242,58 @@ void emit_bits(std::ostringstream& o, const char* var, const char* src, const ui
   o << ";\n";
 }
 
+// TMA loads (or L2 prefetches) of one strided tile, coordinates computed from
+// the chunk index `cv` (its bit k = the k-th non-tile physical bit).
+std::string lazy_loads(const TmaParams& tp, const char* cv, const char* dst, bool prefetch, const char* ind) {
+  TileDims td;
+  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td)) return "";
+  std::vector<int> oidx(tp.nbits, -1), tidx(tp.nbits, -1);
+  for (int k = 0; k < tp.C; ++k) tidx[tp.tbit[k]] = k;
+  int no = 0;
+  for (int p = 0; p < tp.nbits; ++p)
+    if (tidx[p] < 0) oidx[p] = no++;
+  std::ostringstream o;
+  for (int it = 0; it < (1 << td.nit); ++it) {
+    std::vector<std::string> cs;
+    for (int jd = 0; jd < td.rank; ++jd) {
+      if (jd == 0) {
+        cs.push_back("0");
+        continue;
+      }
+      std::ostringstream c;
+      c << "(int)(0ull";
+      uint64_t konst = 0;
+      for (int p = td.lo[jd]; p < td.lo[jd] + td.len[jd]; ++p) {
+        if (oidx[p] >= 0)
+          c << " | (((" << cv << " >> " << oidx[p] << ") & 1ull) << " << p - td.lo[jd] << ")";
+        else if (td.box[jd] == 1 && tidx[p] >= td.inbox && ((it >> (tidx[p] - td.inbox)) & 1))
+          konst |= 1ull << (p - td.lo[jd]);
+      }
+      c << " | " << konst << "ull)";
+      cs.push_back(c.str());
+    }
+    o << ind;
+    if (prefetch) {
+      o << "asm volatile(\"cp.async.bulk.prefetch.tensor." << td.rank << "d.L2.global.tile [%0, {";
+    } else {
+      o << "asm volatile(\"cp.async.bulk.tensor." << td.rank
+        << "d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {";
+    }
+    const int base = prefetch ? 1 : 2;
+    for (int jd = 0; jd < td.rank; ++jd) o << (jd ? ", " : "") << "%" << base + jd;
+    if (prefetch) {
+      o << "}];\" :: \"l\"(&p.map)";
+    } else {
+      o << "}], [%" << base + td.rank << "];\" :: \"r\"(su32(" << dst << " + " << ((size_t)it << td.inbox) * 16
+        << ")), \"l\"(&p.map)";
+    }
+    for (auto& c : cs) o << ", \"r\"(" << c << ")";
+    if (!prefetch) o << ", \"r\"(su32(full + s))";
+    o << " : \"memory\");\n";
+  }
+  return o.str();
+}
+
 }  // namespace
 
 // Emit the source of one pass. Returns false when the structure is outside
@@ -264,7 +316,9 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // registers: 4 per complex entry, 2^M entries per table; one table for
   // 16-amplitude threads, two for 8-amplitude threads
   const char* hz = getenv("QK_JIT_HOIST");
-  const int hoist = std::min<int>((int)toff->size(), hz ? atoi(hz) : (M == 4 ? 1 : 2));
+  // (none for 512-thread groups: 120 registers per thread leave no room)
+  const int hoist = std::min<int>((int)toff->size(),
+                                  hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
   for (int t = 0; t < hoist; ++t) pro << "  double2 tv" << t << "[" << NA << "];\n";
   const int GT = 1 << T;
   const int consumers = GT * ng;
@@ -534,14 +588,25 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "        const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
     << "        if (round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
     << "        mbar_expect_tx(full + s, stage_bytes);\n"
-    << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n"
-    << "        const int row0 = (int)(chunk * " << rows_chunk << "ull);\n";
+    << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n";
+  const char* pfe = getenv("QK_JIT_PREFETCH");
+  if (tp.lazy) {
+    // strided tile (qk_internal.h tile_dims): one N-D box per value of the
+    // iterated top tile bits; coordinates from the chunk's outer bits
+    o << lazy_loads(tp, "chunk", "dst", false, "        ");
+    if (pfe ? atoi(pfe) != 0 : st <= 2) {
+      o << "        if (chunk + " << st << "ull * G < p.nchunks) {\n"
+        << "          const u64 nchunk = chunk + " << st << "ull * G;\n"
+        << lazy_loads(tp, "nchunk", nullptr, true, "          ") << "        }\n";
+    }
+  } else {
+  o << "        const int row0 = (int)(chunk * " << rows_chunk << "ull);\n";
   for (int t = 0; t < tp.ntma; ++t)
     o << "        tma_load(dst + " << t * tp.box_rows * 128 << ", &p.map, 0, row0 + " << t * tp.box_rows << ", full + s);\n";
+  }
   // with a shallow ring, pull the chunk that will refill this stage into L2
   // now, so its load hits L2 when the stage is released
-  const char* pfe = getenv("QK_JIT_PREFETCH");
-  if (pfe ? atoi(pfe) != 0 : st <= 2) {
+  if (!tp.lazy && (pfe ? atoi(pfe) != 0 : st <= 2)) {
     o << "        if (chunk + " << st << "ull * G < p.nchunks) {\n"
       << "          const int prow = (int)((chunk + " << st << "ull * G) * " << rows_chunk << "ull);\n";
     for (int t = 0; t < tp.ntma; ++t)

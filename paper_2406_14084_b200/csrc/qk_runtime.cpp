@@ -381,6 +381,8 @@ struct InstrPlan {
   int fused_by = -1;         // SQS/CSQS: index of the block whose last pass absorbs it
   int synthetic = 0;         // block: layout-restore pass appended by the planner
   std::vector<int> xspec;    // block: spectator source bits of a cluster-exchange store (qk_jit.cpp)
+  int lazy = 0;              // SQS / local CSQS absorbed into the lazy layout: no kernel
+  std::vector<int> tile;     // block: strided tile (physical bits) of a lazy in-place pass
   int sqs = -1;              // SQS / single-device CSQS
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
@@ -890,6 +892,9 @@ struct qk_sim {
   std::vector<InstrPlan> iplan;
   HostPlan hp;
   std::vector<int> final_perm;
+  // lazy in-place layout: reference address bit q of the handle's state lives
+  // at physical bit lay[q]; qk_run leaves lay_final (the plan's end layout)
+  std::vector<int> lay, lay_final;
   // device plan
   void* blob = nullptr;
   size_t blob_bytes = 0;
@@ -983,16 +988,55 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
 }
 
 bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<int>* dest,
-              const std::vector<int>* xspec = nullptr) {
+              const std::vector<int>* xspec = nullptr, const std::vector<int>* tile = nullptr) {
   if (getenv("QK_NO_TMA")) return false;
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > (getenv("QK_TMA13") ? 13 : 12) || pd.nphases > kTMaxPh || s->nbits > 34) return false;
+  const bool lz = tile && !tile->empty();
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > ((lz || getenv("QK_TMA13")) ? 13 : 12) || pd.nphases > kTMaxPh ||
+      s->nbits > 34)
+    return false;
   if (pd.nouter != s->nbits - pd.C) return false;
-  for (int k = 0; k < pd.nouter; ++k)
-    if (pd.opos[k] != pd.C + k) return false;
+  std::vector<int> vdest;
+  TileDims td{};
+  if (lz) {
+    // strided tile: chunk-local bit x <-> physical tile[x]; outer (chunk index)
+    // bit k <-> the k-th non-tile bit; stored in place through the permuted path
+    uint8_t tb[16];
+    for (int x = 0; x < pd.C; ++x) tb[x] = (uint8_t)(*tile)[x];
+    if ((int)tile->size() != pd.C || !tile_dims(tb, pd.C, s->nbits, &td)) return false;
+    std::vector<char> in(s->nbits, 0);
+    for (int p : *tile) in[p] = 1;
+    for (int p : *tile) vdest.push_back(dest ? (*dest)[p] : p);  // in-tile store permutation
+    for (int p = 0; p < s->nbits; ++p)
+      if (!in[p]) vdest.push_back(p);
+    dest = &vdest;
+  } else {
+    for (int k = 0; k < pd.nouter; ++k)
+      if (pd.opos[k] != pd.C + k) return false;
+  }
   const HostPlan& hp = s->hp;
   const int box_rows = std::min(256, 1 << (pd.C - 3));
-  if (!state_map(s, 0, box_rows)) return false;
   memset(&tp, 0, sizeof tp);
+  if (lz) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[5];
+    cuuint64_t strides[4];
+    cuuint32_t box[5], es[5];
+    for (int j = 0; j < td.rank; ++j) {
+      dims[j] = j == 0 ? 16 : (cuuint64_t)1 << td.len[j];
+      if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
+      box[j] = (cuuint32_t)td.box[j];
+      es[j] = 1;
+    }
+    if (fn(&tp.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, td.rank, s->bufs[0], dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    tp.lazy = 1;
+    for (int x = 0; x < pd.C; ++x) tp.tbit[x] = (uint8_t)(*tile)[x];
+  } else if (!state_map(s, 0, std::min(256, 1 << (pd.C - 3)))) {
+    return false;
+  }
   tp.tabs = s->d_pool;
   tp.direct_store = (getenv("QK_TMA_STORE") && !dest) ? 0 : 1;
   tp.nbits = s->nbits;
@@ -1111,17 +1155,19 @@ int upload_plan(qk_sim* s) {
   }
   s->tma.clear();
   s->pass_tma.assign(hp.passes.size(), -1);
-  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr), pass_x(hp.passes.size(), nullptr);
+  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr), pass_x(hp.passes.size(), nullptr),
+      pass_tile(hp.passes.size(), nullptr);
   for (auto& ip : s->iplan) {
     ip.permuted = 0;
     if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) {
       pass_dest[ip.pass0 + ip.npass - 1] = &ip.dest;
       pass_x[ip.pass0 + ip.npass - 1] = &ip.xspec;
     }
+    if (ip.type == QK_INS_BLOCK && ip.npass == 1 && !ip.tile.empty()) pass_tile[ip.pass0] = &ip.tile;
   }
   for (size_t p = 0; p < hp.passes.size(); ++p) {
     TmaParams tp;
-    if (make_tma(s, hp.passes[p], tp, pass_dest[p], pass_x[p])) {
+    if (make_tma(s, hp.passes[p], tp, pass_dest[p], pass_x[p], pass_tile[p])) {
       s->pass_tma[p] = (int)s->tma.size();
       s->tma.push_back(tp);
     }
@@ -1177,6 +1223,27 @@ int upload_plan(qk_sim* s) {
       s->jit_blob[p] = std::move(blob);
     }
   }
+  // strided-tile passes exist only as specialised kernels: without one the
+  // generic register-tiled pass runs them (arbitrary chunk bits, in place)
+  for (size_t p = 0; p < hp.passes.size(); ++p)
+    if (s->pass_tma[p] >= 0 && s->tma[s->pass_tma[p]].lazy && !(p < s->pass_jit.size() && s->pass_jit[p])) {
+      const TmaParams& tq = s->tma[s->pass_tma[p]];
+      for (int x = 0; x < tq.C; ++x)  // the generic pass cannot permute the tile on store
+        if (tq.dpos[x] != tq.tbit[x]) return fail(QK_ESIM, "lazy pass needs the specialised kernel (NVRTC)");
+      s->pass_tma[p] = -1;
+    }
+  if (getenv("QK_DUMP_PLAN"))
+    for (size_t i = 0; i < s->iplan.size(); ++i) {
+      const InstrPlan& ip = s->iplan[i];
+      if (ip.type != QK_INS_BLOCK) continue;
+      for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
+        fprintf(stderr, "instr %zu pass %d C=%d phases=%d tma=%d jit=%d x=%d tile=", i, p, hp.passes[p].C,
+                hp.passes[p].nphases, s->pass_tma[p] >= 0, p < (int)s->pass_jit.size() && s->pass_jit[p] != nullptr,
+                s->pass_tma[p] >= 0 ? s->tma[s->pass_tma[p]].xbits : 0);
+        for (int t : ip.tile) fprintf(stderr, "%d,", t);
+        fprintf(stderr, "\n");
+      }
+    }
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
                                  (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
@@ -1222,6 +1289,38 @@ int check_csqs(const qk_sim* s, const std::vector<int>& local_set, const std::ve
 
 // Conservative plan-time check that a single-pass block runs on the TMA path
 // (a fused pass must: the swaps it absorbs have no other executor).
+bool lay_identity(const std::vector<int>& l) {
+  for (size_t q = 0; q < l.size(); ++q)
+    if (l[q] != (int)q) return false;
+  return true;
+}
+
+// Two rounds of disjoint bit swaps (SQS, applied in order) that bring the data
+// of layout `lay` (reference bit q at physical bit lay[q]) back to the
+// reference layout. An SQS on physical bits (x, y) turns lay into tau o lay, so
+// we need tau2 o tau1 = pi = lay^-1; on every cycle (a_0 .. a_{m-1}) of pi the
+// reflections a_i <-> a_{-i} and a_i <-> a_{1-i} compose to pi.
+void restore_rounds(const std::vector<int>& lay, std::vector<std::pair<int, int>> rounds[2]) {
+  const int n = (int)lay.size();
+  std::vector<int> pi(n);
+  for (int q = 0; q < n; ++q) pi[lay[q]] = q;
+  std::vector<char> seen(n, 0);
+  for (int a = 0; a < n; ++a) {
+    if (seen[a] || pi[a] == a) continue;
+    std::vector<int> cyc;
+    for (int x = a; !seen[x]; x = pi[x]) {
+      seen[x] = 1;
+      cyc.push_back(x);
+    }
+    const int m = (int)cyc.size();
+    for (int i = 0; i < m; ++i) {
+      const int j1 = (m - i) % m, j2 = ((1 - i) % m + m) % m;
+      if (i < j1) rounds[0].push_back({cyc[i], cyc[j1]});
+      if (i < j2) rounds[1].push_back({cyc[i], cyc[j2]});
+    }
+  }
+}
+
 bool tma_plan_ok(const HostPlan& hp, int pass, int nbits) {
   if (getenv("QK_NO_TMA")) return false;
   const PassDesc& pd = hp.passes[pass];
@@ -1258,6 +1357,39 @@ int compile_program(qk_sim* s) {
   const bool xfuse = relabel && !getenv("QK_NO_XFUSE") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   std::vector<int> sigma(nb);
   for (int q = 0; q < nb; ++q) sigma[q] = q;
+  // Lazy in-place mode (no second buffer, e.g. 33 qubits on one B200): SQS and
+  // in-handle CSQS only relabel (sigma); a block runs as one strided-tile pass
+  // over its targets' current physical bits plus bits 0..2 (128-B rows), stored
+  // back in place. The handle keeps the end layout (lay_final), maps every
+  // readback through it and restores the reference layout before writers.
+  const bool lazy = !s->bufs[1] && !relabel && !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") &&
+                    jit_available() && nb >= (jenv ? atoi(jenv) : 20) && nb >= 16;
+  auto emit_restore = [&]() {
+    std::vector<std::pair<int, int>> rounds[2];
+    restore_rounds(sigma, rounds);
+    for (auto& rd : rounds) {
+      if (rd.empty()) continue;
+      std::vector<int> A, B;
+      for (auto& pr : rd) {
+        A.push_back(pr.first);
+        B.push_back(pr.second);
+      }
+      InstrPlan rp;
+      rp.type = QK_INS_SQS;
+      rp.synthetic = 1;
+      rp.sqs = compile_sqs(s->hp, A, B, nb, true);
+      rp.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)A.size()));
+      s->iplan.push_back(std::move(rp));
+      for (int& v : sigma)
+        for (auto& pr : rd) {
+          if (v == pr.first) { v = pr.second; break; }
+          if (v == pr.second) { v = pr.first; break; }
+        }
+    }
+    return lay_identity(sigma);
+  };
+  std::vector<int> ident(nb);
+  for (int q = 0; q < nb; ++q) ident[q] = q;
   std::vector<char> fused(s->prog.size(), 0);
   auto remap = [&](const InstrH& ins) {
     InstrH m = ins;
@@ -1269,6 +1401,85 @@ int compile_program(qk_sim* s) {
     auto& ins = s->prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
+    if (ins.type == QK_INS_BLOCK && lazy && !ins.gates.empty()) {
+      InstrH mapped = remap(ins);
+      std::vector<char> inT(nb, 0);
+      int maxt = -1;
+      for (auto& g : mapped.gates)
+        for (int t : g.t) {
+          if (t < 0 || t >= nb) return fail(QK_ESIM, "gate target %d beyond local range", t);
+          inT[t] = 1;
+          maxt = std::max(maxt, t);
+        }
+      for (int p = 0; p < 3; ++p) inT[p] = 1;
+      int cnt = 0;
+      for (char c2 : inT) cnt += c2;
+      for (int p = 0; p < nb && cnt < 10; ++p)
+        if (!inT[p]) inT[p] = 1, ++cnt;
+      std::vector<int> T;
+      for (int p = 0; p < nb; ++p)
+        if (inT[p]) T.push_back(p);
+      const bool contiguous = T.back() == (int)T.size() - 1 && T.size() <= 12;
+      TileDims tdchk{};
+      uint8_t tb8[16] = {0};
+      for (size_t x = 0; x < T.size() && x < 16; ++x) tb8[x] = (uint8_t)T[x];
+      if (cnt <= 13 && !contiguous && tile_dims(tb8, cnt, nb, &tdchk)) {
+        // Store permutation inside the tile (in place, same address set):
+        // qubits the next block needs move onto bits 0..2, so its tile only
+        // has to add what is missing (10 bits instead of 13 when all fit).
+        std::vector<int> dphys = ident;
+        std::vector<int> sig2 = sigma;
+        size_t jj = ii + 1;
+        bool ok = true;
+        for (; jj < s->prog.size(); ++jj) {
+          const InstrH& nx = s->prog[jj];
+          if (nx.type == QK_INS_BLOCK) {
+            if (!nx.gates.empty()) break;
+            continue;
+          }
+          bool in_local = true;
+          for (int q : nx.a) in_local = in_local && q >= 0 && q < nb;
+          for (int q : nx.b) in_local = in_local && q >= 0 && q < nb;
+          if (!in_local) {
+            ok = false;
+            break;
+          }
+          std::vector<int> sa = nx.a, sb = nx.b;
+          std::sort(sa.begin(), sa.end());
+          std::sort(sb.begin(), sb.end());
+          for (size_t k = 0; k < sa.size(); ++k) std::swap(sig2[sa[k]], sig2[sb[k]]);
+        }
+        if (ok && jj < s->prog.size() && !getenv("QK_NO_LAZY_PERM")) {
+          std::vector<char> need(nb, 0);
+          for (auto& g : s->prog[jj].gates)
+            for (int t : g.t)
+              if (t >= 0 && t < nb) need[sig2[t]] = 1;
+          std::vector<int> want, low;
+          for (int p : T)
+            if (p >= 3 && need[p]) want.push_back(p);
+          for (int p = 0; p < 3; ++p)
+            if (!need[p]) low.push_back(p);
+          for (size_t k = 0; k < want.size() && k < low.size(); ++k) {
+            dphys[low[k]] = want[k];
+            dphys[want[k]] = low[k];
+          }
+        }
+        std::vector<const GateH*> gs;
+        for (auto& g : mapped.gates) gs.push_back(&g);
+        ip.pass0 = (int)s->hp.passes.size();
+        int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+        if (rc) return fail(rc, "%s", emsg.c_str());
+        ip.npass = (int)s->hp.passes.size() - ip.pass0;
+        ip.bytes = 32.0 * std::ldexp(1.0, nb) * ip.npass;
+        ip.tile = T;
+        ip.dest = dphys;
+        for (int& v : sigma) v = dphys[v];
+        s->iplan.push_back(std::move(ip));
+        continue;
+      }
+      // contiguous chunk: the standard pass; a tile the TMA view cannot take: restore first
+      if (!contiguous && !emit_restore()) return fail(QK_ESIM, "internal: layout restore failed");
+    }
     if (ins.type == QK_INS_BLOCK) {
       InstrH mapped = remap(ins);
       if (relabel && !ins.gates.empty()) {
@@ -1413,6 +1624,14 @@ int compile_program(qk_sim* s) {
         a.push_back(sigma[sa[k]]);
         b.push_back(sigma[sb[k]]);
       }
+      if (lazy) {
+        // relabel only: sigma'[sa_k] = sigma[sb_k] and vice versa
+        for (size_t k = 0; k < sa.size(); ++k) std::swap(sigma[sa[k]], sigma[sb[k]]);
+        ip.lazy = 1;
+        ip.bytes = 0;
+        s->iplan.push_back(std::move(ip));
+        continue;
+      }
       ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
       ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
     } else {
@@ -1426,6 +1645,18 @@ int compile_program(qk_sim* s) {
       ip.a = ins.a;
       ip.b = ins.b;
       ip.csqs_s = (int)ins.a.size();
+      if (local_only && lazy) {
+        std::vector<int> sa = ins.a, sb = ins.b;
+        std::sort(sa.begin(), sa.end());
+        std::sort(sb.begin(), sb.end());
+        for (size_t k = 0; k < sa.size(); ++k) std::swap(sigma[sa[k]], sigma[sb[k]]);
+        ip.lazy = 1;
+        ip.bytes = 0;
+        s->iplan.push_back(std::move(ip));
+        continue;
+      }
+      if (!local_only && lazy && !lay_identity(sigma) && !emit_restore())
+        return fail(QK_ESIM, "internal: layout restore failed");
       if (local_only) {
         std::vector<int> sa = ins.a, sb = ins.b;
         std::sort(sa.begin(), sa.end());
@@ -1459,10 +1690,14 @@ int compile_program(qk_sim* s) {
     }
     s->iplan.push_back(std::move(ip));
   }
-  // restore the reference layout at the end of the program
-  bool ident = true;
-  for (int q = 0; q < nb; ++q) ident = ident && sigma[q] == q;
-  if (!ident) {
+  // lazy mode: the handle keeps the end layout; relabel mode restores it
+  s->lay_final = ident;
+  if (lazy) {
+    s->lay_final = sigma;
+    for (int q = 0; q < nb; ++q) sigma[q] = q;
+  }
+  bool is_ident = lay_identity(sigma);
+  if (!is_ident) {
     std::vector<int> d(nb);
     for (int q = 0; q < nb; ++q) d[sigma[q]] = q;
     InstrPlan ip;
@@ -1519,15 +1754,18 @@ int ensure_events(qk_sim* s, size_t n) {
 int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
   if (s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0) {
     TmaParams& tp = s->tma[s->pass_tma[p]];
-    const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
-    if (!map) return fail(QK_ECUDA, "tensor map unavailable");
-    tp.map = *map;
+    if (!tp.lazy) {  // lazy passes carry their own strided view of bufs[0]
+      const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
+      if (!map) return fail(QK_ECUDA, "tensor map unavailable");
+      tp.map = *map;
+    }
+    const bool flip = tp.permuted && !tp.lazy;
     tp.state = s->bufs[s->cur];
-    tp.out = tp.permuted ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
+    tp.out = flip ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
     int rc;
     if (p < (int)s->pass_jit.size() && s->pass_jit[p]) {
       std::vector<uint64_t>& blob = s->jit_blob[p];
-      memcpy(blob.data(), map, 128);
+      memcpy(blob.data(), &tp.map, 128);
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
@@ -1537,7 +1775,7 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
     }
     if (rc) return fail(QK_ECUDA, "tma block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
-    if (tp.permuted) {
+    if (flip) {
       s->cur ^= 1;
       s->state = s->bufs[s->cur];
     }
@@ -1554,7 +1792,7 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
 int exchange_cross(qk_sim* s, const InstrPlan& ip);
 
 bool fused_away(const qk_sim* s, const InstrPlan& ip) {
-  return ip.fused_by >= 0 && s->iplan[ip.fused_by].permuted;
+  return ip.lazy || (ip.fused_by >= 0 && s->iplan[ip.fused_by].permuted);
 }
 
 int run_instr(qk_sim* s, const InstrPlan& ip) {
@@ -1675,6 +1913,41 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   return QK_OK;
 }
 
+// Bring the state back to the reference layout (two SQS rounds at most).
+int materialize(qk_sim* s) {
+  if (s->lay.empty() || lay_identity(s->lay)) return QK_OK;
+  std::vector<std::pair<int, int>> rounds[2];
+  restore_rounds(s->lay, rounds);
+  for (auto& rd : rounds) {
+    if (rd.empty()) continue;
+    std::vector<int> A, B;
+    for (auto& pr : rd) {
+      A.push_back(pr.first);
+      B.push_back(pr.second);
+    }
+    HostPlan tmp;
+    compile_sqs(tmp, A, B, s->nbits, true);
+    int rc = launch_sqs(s->state, &tmp.sqs[0], nullptr, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "layout restore failed: %s", cudaGetErrorString((cudaError_t)rc));
+    for (int& v : s->lay)
+      for (auto& pr : rd) {
+        if (v == pr.first) { v = pr.second; break; }
+        if (v == pr.second) { v = pr.first; break; }
+      }
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (!lay_identity(s->lay)) return fail(QK_ESIM, "internal: layout restore did not reach the reference layout");
+  return QK_OK;
+}
+
+// physical address (handle-local) of reference address i under the layout
+uint64_t lay_addr(const qk_sim* s, uint64_t i) {
+  if (s->lay.empty()) return i;
+  uint64_t j = 0;
+  for (int q = 0; q < s->nbits; ++q) j |= ((i >> q) & 1ull) << s->lay[q];
+  return j;
+}
+
 int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out) {
   if (!out) return fail(QK_EINVAL, "null output handle");
   *out = nullptr;
@@ -1711,6 +1984,9 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
     return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", required);
   }
   s->state = s->bufs[0];
+  s->lay.resize(nbits);
+  for (int q = 0; q < nbits; ++q) s->lay[q] = q;
+  s->lay_final = s->lay;
   // second buffer for out-of-place fused block+SQS passes when it fits comfortably
   if (!getenv("QK_INPLACE") && 2.0 * (double)need <= 0.90 * (double)free_b) {
     if (cudaMalloc(&s->bufs[1], need) != cudaSuccess) {
@@ -1834,6 +2110,7 @@ int qk_reset(qk_sim* s) {
   CUDA_TRY(cudaSetDevice(s->device));
   s->cur = 0;
   s->state = s->bufs[0];
+  for (int q = 0; q < s->nbits; ++q) s->lay[q] = q;  // |0...0> is the same in every layout
   int rc = launch_fill_zero_one(s->state, s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
   CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -1903,9 +2180,11 @@ int qk_set_profiling(qk_sim* s, int per_launch) {
 int qk_run(qk_sim* s, double* timings) {
   if (!s) return fail(QK_EINVAL, "null handle");
   CUDA_TRY(cudaSetDevice(s->device));
+  int rc = materialize(s);  // the plan starts from the reference layout
+  if (rc) return rc;
   const auto t0 = std::chrono::steady_clock::now();
   const size_t ni = s->iplan.size();
-  int rc = ensure_events(s, 2 * ni + 2);
+  rc = ensure_events(s, 2 * ni + 2);
   if (rc) return rc;
   for (size_t i = 0; i < ni; ++i) {
     CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
@@ -1914,6 +2193,7 @@ int qk_run(qk_sim* s, double* timings) {
     CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
   double cls[3] = {0, 0, 0};
   for (size_t i = 0; i < ni; ++i) {
     float ms = 0;
@@ -1976,6 +2256,23 @@ int qk_read_physical(qk_sim* s, int part, uint64_t off, uint64_t count, double* 
   if (part < 0 || part >= s->count || off + count > psize || off > psize)
     return fail(QK_EINVAL, "read outside partition");
   CUDA_TRY(cudaSetDevice(s->device));
+  if (count && !lay_identity(s->lay)) {
+    // lazy layout: gather through the bit permutation (reference index i -> lay_addr(i))
+    std::vector<int> pm(s->nbits);
+    for (int q = 0; q < s->nbits; ++q) pm[s->lay[q]] = q;
+    const uint64_t chunk = 1u << 22;
+    int rc = ensure_scratch(s, chunk * 16);
+    if (rc) return rc;
+    for (uint64_t b = 0; b < count; b += chunk) {
+      const uint64_t m = std::min(chunk, count - b);
+      rc = launch_gather_logical(s->state, pm.data(), s->nbits, part * psize + off + b, m, (double*)s->d_scratch,
+                                 (CUstream_st*)s->stream);
+      if (rc) return fail(QK_ECUDA, "layout gather failed");
+      CUDA_TRY(cudaMemcpyAsync(reim + 2 * b, s->d_scratch, m * 16, cudaMemcpyDeviceToHost, s->stream));
+      CUDA_TRY(cudaStreamSynchronize(s->stream));
+    }
+    return QK_OK;
+  }
   if (count)
     CUDA_TRY(cudaMemcpyAsync(reim, s->state + 2 * (part * psize + off), count * 16, cudaMemcpyDeviceToHost,
                              s->stream));
@@ -1988,6 +2285,7 @@ int qk_write_physical(qk_sim* s, int part, uint64_t off, uint64_t count, const d
   const uint64_t psize = 1ull << s->L;
   if (part < 0 || part >= s->count || off + count > psize || off > psize)
     return fail(QK_EINVAL, "write outside partition");
+  { int mrc = materialize(s); if (mrc) return mrc; }  // writes address the reference layout
   CUDA_TRY(cudaSetDevice(s->device));
   if (count)
     CUDA_TRY(cudaMemcpyAsync(s->state + 2 * (part * psize + off), reim, count * 16, cudaMemcpyHostToDevice,
@@ -2012,7 +2310,7 @@ int qk_gather(qk_sim* s, const uint64_t* idx, uint64_t count, double* reim) {
   std::vector<uint64_t> rel(std::min(count, chunk));
   for (uint64_t b = 0; b < count; b += chunk) {
     const uint64_t m = std::min(chunk, count - b);
-    for (uint64_t i = 0; i < m; ++i) rel[i] = idx[b + i] - lo;
+    for (uint64_t i = 0; i < m; ++i) rel[i] = lay_addr(s, idx[b + i] - lo);
     CUDA_TRY(cudaMemcpyAsync(d_idx, rel.data(), m * 8, cudaMemcpyHostToDevice, s->stream));
     rc = launch_gather(s->state, d_idx, m, d_out, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "gather failed");
@@ -2044,7 +2342,8 @@ int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64
   const uint64_t chunk = 1u << 22;
   int rc = ensure_scratch(s, chunk * 16);
   if (rc) return rc;
-  std::vector<int> pm(perm, perm + s->n);
+  std::vector<int> pm(s->n);
+  for (int pos = 0; pos < s->n; ++pos) pm[pos < s->nbits ? s->lay[pos] : pos] = perm[pos];
   for (uint64_t b = 0; b < count; b += chunk) {
     const uint64_t m = std::min(chunk, count - b);
     rc = launch_gather_logical(s->state, pm.data(), s->n, start + b, m, (double*)s->d_scratch,
@@ -2110,6 +2409,7 @@ int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t
 int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, const double* params,
                    size_t nparams, int c, uint64_t row_start, uint64_t row_stop) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  { int mrc = materialize(s); if (mrc) return mrc; }
   if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
   if (c < 1 || c > s->L) return fail(QK_EINVAL, "bad chunk width %d", c);
   CUDA_TRY(cudaSetDevice(s->device));
@@ -2163,6 +2463,7 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
 
 int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  { int mrc = materialize(s); if (mrc) return mrc; }
   CUDA_TRY(cudaSetDevice(s->device));
   int rc;
   std::string emsg;
@@ -2199,6 +2500,7 @@ int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const dou
 int qk_sqs(qk_sim* s, int part, const int32_t* out_set, const int32_t* in_set, int k, int cl,
            uint64_t start, uint64_t stop) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  { int mrc = materialize(s); if (mrc) return mrc; }
   if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
   std::vector<int> a(out_set, out_set + k), b(in_set, in_set + k);
   for (int q : a)
@@ -2240,6 +2542,7 @@ int qk_sqs(qk_sim* s, int part, const int32_t* out_set, const int32_t* in_set, i
 
 int qk_csqs(qk_sim* s, const int32_t* local_set, const int32_t* rank_set, int S) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  { int mrc = materialize(s); if (mrc) return mrc; }
   std::vector<int> a(local_set, local_set + S), b(rank_set, rank_set + S);
   int rc = check_csqs(s, a, b);
   if (rc) return rc;

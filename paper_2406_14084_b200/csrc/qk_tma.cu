@@ -337,7 +337,7 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages) {
   if (S > 4 * NG) S = 4 * NG;
   if (ng) *ng = NG;
   if (stages) *stages = S;
-  if (S < 1 || (S < 2 && !(C == 13 && getenv("QK_TMA13"))) || S < NG) return -1;
+  if (S < 1 || (S < 2 && C != 13) || S < NG) return -1;  // C = 13: one 128-KiB stage
   return (int)(S * stage + 2 * S * 8);
 }
 

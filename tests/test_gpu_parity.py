@@ -338,9 +338,12 @@ def test_execution_strategies_agree_at_scale(gpu, name, n, c):
     from conftest import ROOT
     text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
     outs = {}
-    for mode in ("default", "QK_XFUSE_ALL", "QK_NO_XFUSE", "QK_NO_FUSE", "QK_NO_TMA", "QK_NO_JIT"):
-        if mode != "default":
-            os.environ[mode] = "1"
+    modes = ("default", "QK_XFUSE_ALL", "QK_NO_XFUSE", "QK_NO_FUSE", "QK_NO_TMA", "QK_NO_JIT",
+             "QK_INPLACE+QK_JIT=0", "QK_INPLACE+QK_JIT=0+QK_NO_LAZY_PERM", "QK_INPLACE+QK_NO_LAZY")
+    for mode in modes:
+        envs = [] if mode == "default" else [e.partition("=") for e in mode.split("+")]
+        for k, _, v in envs:
+            os.environ[k] = v or "1"
         try:
             sim = Simulator(LayoutParams(n=n, c=n))
             perm = sim.load_text(text, c)
@@ -350,7 +353,51 @@ def test_execution_strategies_agree_at_scale(gpu, name, n, c):
             outs[mode] = res.physical_vector()
             assert abs(res.norm() - 1.0) <= 1e-12, (mode, res.norm())
         finally:
-            os.environ.pop(mode, None)
+            for k, _, _ in envs:
+                os.environ.pop(k, None)
     base = outs["QK_NO_TMA"]
     for mode, vec in outs.items():
         assert np.max(np.abs(vec - base)) <= TOL, mode
+
+
+@pytest.mark.gpu
+def test_lazy_layout_readbacks_and_writers(gpu):
+    """In-place states keep SQS as a layout relabeling (no second buffer; forced
+    here at 24 qubits): every readback maps through the layout, a second run
+    and kernel-level writers first restore the reference layout. All of it
+    must match a handle that executes every swap."""
+    import os
+    from conftest import ROOT
+    text = open(os.path.join(ROOT, "bench_circuits", "qaoa24_c12_r0.txt")).read()
+    n = 24
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, 1 << n, size=64)
+
+    def session(env):
+        for k, v in env.items():
+            os.environ[k] = v
+        try:
+            sim = Simulator(LayoutParams(n=n, c=n))
+            perm = sim.load_text(text, 12)
+            sim.handle.reset()
+            res = sim.run_loaded(perm)
+            out = {"phys": res.physical_vector(), "norm": res.norm(),
+                   "amp": [res.amplitude(int(i)) for i in idx[:8]],
+                   "logical": res.logical_amplitudes(4096, start=12345),
+                   "slice": np.array(res.partitions[0].amps[1000:1064])}
+            res2 = sim.run_loaded(perm)          # no reset: continues from the end layout
+            out["twice"] = res2.physical_vector()
+            in_memory_swap(sim.partitions[0].amps, (0, 5), (7, 20), 2)   # kernel-level writer
+            out["after_sqs"] = sim.partitions[0].amps[:]
+            sim.close()
+            return out
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+
+    lazy = session({"QK_INPLACE": "1", "QK_JIT": "0"})
+    eager = session({"QK_NO_TMA": "1"})
+    for key in ("phys", "logical", "slice", "twice", "after_sqs"):
+        assert np.max(np.abs(np.asarray(lazy[key]) - np.asarray(eager[key]))) <= TOL, key
+    assert abs(lazy["norm"] - eager["norm"]) <= 1e-12
+    assert np.max(np.abs(np.array(lazy["amp"]) - np.array(eager["amp"]))) <= TOL
