@@ -40,6 +40,8 @@ WORKLOADS = {
     "qaoa26": ("qaoa26_c12_r0.txt", 26, 12, 0),
     "qft26": ("qft26_c10_r0.txt", 26, 10, 0),
     "qaoa24": ("qaoa24_c12_r0.txt", 24, 12, 0),
+    "bv30": ("bv30_c10_r0.txt", 30, 10, 0),
+    "h30": ("h30_c10_r0.txt", 30, 10, 0),
 }
 MULTI = {2: ("qaoa31_c12_r1.txt", 31, 12, 1), 4: ("qaoa32_c12_r2.txt", 32, 12, 2),
          8: ("qaoa33_c12_r3.txt", 33, 12, 3)}

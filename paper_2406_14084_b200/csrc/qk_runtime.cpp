@@ -895,6 +895,7 @@ struct qk_sim {
   // lazy in-place layout: reference address bit q of the handle's state lives
   // at physical bit lay[q]; qk_run leaves lay_final (the plan's end layout)
   std::vector<int> lay, lay_final;
+  std::vector<CUtensorMap> lazy_map1;  // per TMA pass: the strided view of bufs[1] (lazy passes)
   // device plan
   void* blob = nullptr;
   size_t blob_bytes = 0;
@@ -987,6 +988,26 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
   return &s->maps[buf][slot];
 }
 
+// N-D strided view of `buf` for the tile of a lazy pass (qk_internal.h tile_dims)
+bool encode_lazy_map(const TmaParams& tp, double* buf, CUtensorMap* out) {
+  TileDims td{};
+  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td)) return false;
+  auto fn = encode_fn();
+  if (!fn || !buf) return false;
+  cuuint64_t dims[5];
+  cuuint64_t strides[4];
+  cuuint32_t box[5], es[5];
+  for (int j = 0; j < td.rank; ++j) {
+    dims[j] = j == 0 ? 16 : (cuuint64_t)1 << td.len[j];
+    if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
+    box[j] = (cuuint32_t)td.box[j];
+    es[j] = 1;
+  }
+  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, td.rank, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<int>* dest,
               const std::vector<int>* xspec = nullptr, const std::vector<int>* tile = nullptr) {
   if (getenv("QK_NO_TMA")) return false;
@@ -1017,23 +1038,11 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
   const int box_rows = std::min(256, 1 << (pd.C - 3));
   memset(&tp, 0, sizeof tp);
   if (lz) {
-    auto fn = encode_fn();
-    if (!fn) return false;
-    cuuint64_t dims[5];
-    cuuint64_t strides[4];
-    cuuint32_t box[5], es[5];
-    for (int j = 0; j < td.rank; ++j) {
-      dims[j] = j == 0 ? 16 : (cuuint64_t)1 << td.len[j];
-      if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
-      box[j] = (cuuint32_t)td.box[j];
-      es[j] = 1;
-    }
-    if (fn(&tp.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, td.rank, s->bufs[0], dims, strides, box, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return false;
     tp.lazy = 1;
+    tp.C = pd.C;
+    tp.nbits = s->nbits;
     for (int x = 0; x < pd.C; ++x) tp.tbit[x] = (uint8_t)(*tile)[x];
+    if (!encode_lazy_map(tp, s->bufs[0], &tp.map)) return false;
   } else if (!state_map(s, 0, std::min(256, 1 << (pd.C - 3)))) {
     return false;
   }
@@ -1154,6 +1163,7 @@ int upload_plan(qk_sim* s) {
     s->pool_bytes = pool_bytes;
   }
   s->tma.clear();
+  s->lazy_map1.clear();
   s->pass_tma.assign(hp.passes.size(), -1);
   std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr), pass_x(hp.passes.size(), nullptr),
       pass_tile(hp.passes.size(), nullptr);
@@ -1170,6 +1180,9 @@ int upload_plan(qk_sim* s) {
     if (make_tma(s, hp.passes[p], tp, pass_dest[p], pass_x[p], pass_tile[p])) {
       s->pass_tma[p] = (int)s->tma.size();
       s->tma.push_back(tp);
+      s->lazy_map1.emplace_back();
+      if (tp.lazy && s->bufs[1] && !encode_lazy_map(tp, s->bufs[1], &s->lazy_map1.back()))
+        return fail(QK_ECUDA, "tensor map unavailable");
     }
   }
   for (auto& ip : s->iplan)
@@ -1362,8 +1375,12 @@ int compile_program(qk_sim* s) {
   // over its targets' current physical bits plus bits 0..2 (128-B rows), stored
   // back in place. The handle keeps the end layout (lay_final), maps every
   // readback through it and restores the reference layout before writers.
-  const bool lazy = !s->bufs[1] && !relabel && !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") &&
-                    jit_available() && nb >= (jenv ? atoi(jenv) : 20) && nb >= 16;
+  // It also replaces relabeling when every chunk is <= 10 qubits (the tiles
+  // then stay <= 13 bits; QFT30: 0.112 s lazy vs 0.132 s relabeled).
+  const bool lazy_ok = !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") && jit_available() &&
+                       nb >= (jenv ? atoi(jenv) : 20) && nb >= 16;
+  const bool lazy = lazy_ok && (!s->bufs[1] || (relabel && Cg <= 10));
+  if (lazy) relabel = false;
   auto emit_restore = [&]() {
     std::vector<std::pair<int, int>> rounds[2];
     restore_rounds(sigma, rounds);
@@ -1754,18 +1771,20 @@ int ensure_events(qk_sim* s, size_t n) {
 int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
   if (s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0) {
     TmaParams& tp = s->tma[s->pass_tma[p]];
-    if (!tp.lazy) {  // lazy passes carry their own strided view of bufs[0]
+    if (!tp.lazy) {
       const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
       if (!map) return fail(QK_ECUDA, "tensor map unavailable");
       tp.map = *map;
     }
+    // lazy passes carry their own strided views of bufs[0] / bufs[1]
+    const CUtensorMap* lazy_map = tp.lazy ? (s->cur ? &s->lazy_map1[s->pass_tma[p]] : &tp.map) : &tp.map;
     const bool flip = tp.permuted && !tp.lazy;
     tp.state = s->bufs[s->cur];
     tp.out = flip ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
     int rc;
     if (p < (int)s->pass_jit.size() && s->pass_jit[p]) {
       std::vector<uint64_t>& blob = s->jit_blob[p];
-      memcpy(blob.data(), &tp.map, 128);
+      memcpy(blob.data(), lazy_map, 128);
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
