@@ -21,7 +21,8 @@ def _port():
         return s.getsockname()[1]
 
 
-CIRCUITS = [("example", 10, 4, 2, 8), ("random", 12, 5, 2, 6), ("random3", 13, 6, 3, 7)]
+CIRCUITS = [("example", 10, 4, 2, 8), ("random", 12, 5, 2, 6), ("random3", 13, 6, 3, 7),
+            ("random18", 18, 8, 1, 10)]
 
 
 def _circuit(name, n, c, r, seed=0):
@@ -60,12 +61,21 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_two_processes_share_the_state(gpu):
+@pytest.mark.parametrize("mode", ["default", "lazy"])
+def test_two_processes_share_the_state(gpu, mode):
+    """`lazy`: the shards run in place with the lazy layout (QK_INPLACE, JIT at
+    every size), so cross-shard CSQS follow layout restores."""
     import torch.multiprocessing as mp
     from paper_2406_14084_b200 import LayoutParams, Simulator
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_worker, args=(2, _port(), results), nprocs=2, join=True)
+    env = {"QK_INPLACE": "1", "QK_JIT": "0"} if mode == "lazy" else {}
+    os.environ.update(env)
+    try:
+        mp.spawn(_worker, args=(2, _port(), results), nprocs=2, join=True)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
     for name, n, c, r, b in CIRCUITS:
         text = _circuit(name, n, c, r)
         sim = Simulator(LayoutParams(n=n, c=n - r, r=r, b=b))
