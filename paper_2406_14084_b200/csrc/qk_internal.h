@@ -43,6 +43,9 @@ struct OpDesc {
   int64_t table;      // offset (complex entries) into the diagonal table pool
   uint16_t tcontrib[16];  // thread bit k -> table index contribution
   uint16_t pr[16];        // register amplitude j -> table index contribution
+  int32_t nco;            // OP_DIAG over address bits outside the chunk (folded diagonal blocks):
+  uint8_t co_k[8];        //   chunk-index bit co_k[i] -> table index contribution co_v[i]
+  uint16_t co_v[8];
 };
 
 struct PhaseDesc {
@@ -109,6 +112,9 @@ struct TOp {
   int16_t cf[4];
   uint16_t tcontrib[12];
   uint16_t pr[16];
+  int8_t nco;             // OpDesc::nco / co_k / co_v (specialised kernels only)
+  uint8_t co_k[8];
+  uint16_t co_v[8];
 };
 
 struct TPhase {
@@ -129,6 +135,7 @@ struct alignas(64) TmaParams {
   int32_t nbits;
   int32_t xbits;                // > 0: cluster-exchange store (qk_jit.cpp), 2^xbits CTAs per cluster
   int32_t lazy;                 // 1: strided tile (tbit) loaded through `map` (N-D), stored in place
+  int32_t needs_jit;            // 1: ops the interpreter cannot run (outer-bit table terms)
   uint8_t tbit[16];             // lazy: physical address bit of every chunk-local bit (ascending)
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)

@@ -319,7 +319,20 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // (none for 512-thread groups: 120 registers per thread leave no room)
   const int hoist = std::min<int>((int)toff->size(),
                                   hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
-  for (int t = 0; t < hoist; ++t) pro << "  double2 tv" << t << "[" << NA << "];\n";
+  // hoist the first `hoist` tables that have no per-chunk (outer-bit) term
+  std::vector<char> hoisted;
+  {
+    int left = hoist;
+    for (int ph = 0; ph < tp.nphases; ++ph)
+      for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o)
+        if (tp.ops[o].code == OP_DIAG) {
+          const bool h = left > 0 && tp.ops[o].nco == 0;
+          hoisted.push_back(h);
+          if (h) --left;
+        }
+  }
+  for (size_t t = 0; t < hoisted.size(); ++t)
+    if (hoisted[t]) pro << "  double2 tv" << t << "[" << NA << "];\n";
   const int GT = 1 << T;
   const int consumers = GT * ng;
   const int rows_chunk = 1 << (C - 3);
@@ -390,14 +403,17 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           // entries for every chunk, so the first `hoist` tables are loaded
           // once before the chunk loop and stay in registers.
           const int ti = tab_i++;
-          std::ostringstream& dst = ti < hoist ? pro : b;
-          const std::string ind = ti < hoist ? "  " : "    ";
+          const bool hz = hoisted[ti];
+          std::ostringstream& dst = hz ? pro : b;
+          const std::string ind = hz ? "  " : "    ";
           dst << ind << "{ const double2* tb = p.tabs + p.toff[" << ti << "];\n";
           dst << ind << "  const u32 pt = 0u";
           for (int k = 0; k < T; ++k)
             if (op.tcontrib[k]) dst << " | (((tid >> " << k << ") & 1u) * " << op.tcontrib[k] << "u)";
+          for (int k = 0; k < op.nco; ++k)  // folded diagonal gates on bits outside the chunk
+            dst << " | ((u32)((chunk >> " << (int)op.co_k[k] << ") & 1ull) * " << op.co_v[k] << "u)";
           dst << ";\n";
-          if (ti < hoist) {
+          if (hz) {
             for (int j = 0; j < NA; ++j) pro << "    tv" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
             pro << "  }\n";
             for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], tv" << ti << "[" << j << "]);\n";

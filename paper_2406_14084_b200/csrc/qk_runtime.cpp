@@ -443,9 +443,18 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
   int last_run = -1;
   uint32_t blocked = 0;
   int nh = 0;
+  // diagonal gates may also act on address bits outside the chunk (diagonal
+  // blocks folded into this pass): their value is fixed per chunk, so they
+  // only add a per-chunk term to the table index (specialised kernels only)
+  std::vector<uint64_t> run_outer;
   for (const GateH* g : gates) {
     uint32_t tm = 0;
+    uint64_t om = 0;
     for (int t : g->t) {
+      if (t >= 0 && t < 64 && loc[t] < 0 && is_diag(g->kind) && t < nbits) {
+        om |= 1ull << t;
+        continue;
+      }
       if (t >= 64 || loc[t] < 0) {
         emsg = "gate target outside pass chunk";
         return QK_ESIM;
@@ -453,12 +462,19 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       tm |= 1u << loc[t];
     }
     if (is_diag(g->kind)) {
-      if (last_run >= 0 && !(tm & blocked)) {
+      const int width = last_run >= 0 ? popc(run_support[last_run] | tm) + popc(run_outer[last_run] | om) : 99;
+      if (last_run >= 0 && !(tm & blocked) && width <= 14 && popc(run_outer[last_run] | om) <= 8) {
         runs[last_run].push_back(g);
         run_support[last_run] |= tm;
+        run_outer[last_run] |= om;
       } else {
+        if (popc(om) > 8) {
+          emsg = "diagonal gate over too many bits outside the chunk";
+          return QK_ESIM;
+        }
         runs.push_back({g});
         run_support.push_back(tm);
+        run_outer.push_back(om);
         last_run = (int)runs.size() - 1;
         blocked = 0;
         items.push_back({1, nullptr, last_run});
@@ -542,6 +558,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
   bool scale_folded = (scale == cplx(1.0, 0.0));
   std::vector<int64_t> run_table(runs.size(), -1);
   std::vector<std::vector<int>> run_bidx(runs.size());
+  std::vector<std::vector<int>> run_obidx(runs.size());  // physical outer bit -> table bit
   auto build_table = [&](int r, const std::vector<int>& order) -> int {
     const uint32_t S = run_support[r];
     std::vector<int> bidx(C, -1);
@@ -550,6 +567,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       if (p >= 0 && p < C && (S >> p & 1) && bidx[p] < 0) bidx[p] = nb++;
     for (int p = 0; p < C; ++p)
       if ((S >> p & 1) && bidx[p] < 0) bidx[p] = nb++;
+    run_obidx[r].assign(64, -1);
+    for (int p = 0; p < 64; ++p)
+      if (run_outer[r] >> p & 1) run_obidx[r][p] = nb++;
     TableDesc td{};
     td.out = hp.pool;
     td.bits = nb;
@@ -565,7 +585,10 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     for (const GateH* g : runs[r]) {
       TableGate tg{};
       tg.nt = (int)g->t.size();
-      for (int j = 0; j < tg.nt; ++j) tg.slot[j] = bidx[loc[g->t[j]]];
+      for (int j = 0; j < tg.nt; ++j) {
+        const int t = g->t[j];
+        tg.slot[j] = loc[t] >= 0 ? bidx[loc[t]] : run_obidx[r][t];
+      }
       tg.entries = (int64_t)hp.entries.size() / 2;
       std::vector<cplx> e = diag_entries(*g);
       if (g->kind == QK_D) {
@@ -658,6 +681,12 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
             if ((j >> s2 & 1) && (S >> pb.R[s2] & 1)) v |= 1u << bidx[pb.R[s2]];
           op.pr[j] = (uint16_t)v;
         }
+        for (size_t k = 0; k < O.size(); ++k)
+          if (run_outer[it.run] >> O[k] & 1) {
+            op.co_k[op.nco] = (uint8_t)k;
+            op.co_v[op.nco] = (uint16_t)(1u << run_obidx[it.run][O[k]]);
+            ++op.nco;
+          }
       } else {
         const GateH* g = it.g;
         switch (g->kind) {
@@ -1103,6 +1132,12 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
           t.table = (int32_t)op.table;
           for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
           for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
+          t.nco = (int8_t)op.nco;
+          for (int k = 0; k < op.nco; ++k) {
+            t.co_k[k] = op.co_k[k];
+            t.co_v[k] = op.co_v[k];
+          }
+          if (op.nco) tp.needs_jit = 1;
           if (op.code == OP_SCALE) {
             if (ncoef + 2 > kTMaxCoef) return false;
             tp.coef[ncoef] = hp.coef[op.coef];
@@ -1239,6 +1274,9 @@ int upload_plan(qk_sim* s) {
   // strided-tile passes exist only as specialised kernels: without one the
   // generic register-tiled pass runs them (arbitrary chunk bits, in place)
   for (size_t p = 0; p < hp.passes.size(); ++p)
+    if (s->pass_tma[p] >= 0 && s->tma[s->pass_tma[p]].needs_jit && !(p < s->pass_jit.size() && s->pass_jit[p]))
+      return fail(QK_ESIM, "folded diagonal block needs the specialised kernel (NVRTC)");
+  for (size_t p = 0; p < hp.passes.size(); ++p)
     if (s->pass_tma[p] >= 0 && s->tma[s->pass_tma[p]].lazy && !(p < s->pass_jit.size() && s->pass_jit[p])) {
       const TmaParams& tq = s->tma[s->pass_tma[p]];
       for (int x = 0; x < tq.C; ++x)  // the generic pass cannot permute the tile on store
@@ -1368,6 +1406,7 @@ int compile_program(qk_sim* s) {
   // cluster-exchange fusion needs the load-time specialised kernels
   const char* jenv = getenv("QK_JIT");
   const bool xfuse = relabel && !getenv("QK_NO_XFUSE") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
+  const bool fold = relabel && !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   std::vector<int> sigma(nb);
   for (int q = 0; q < nb; ++q) sigma[q] = q;
   // Lazy in-place mode (no second buffer, e.g. 33 qubits on one B200): SQS and
@@ -1505,7 +1544,29 @@ int compile_program(qk_sim* s) {
         size_t best_j = ii + 1;
         std::vector<int> P(nb);  // P[q]: reference position whose data lands on q
         for (int q = 0; q < nb; ++q) P[q] = q;
-        for (size_t j = ii + 1; j < s->prog.size() && s->prog[j].type == QK_INS_SQS && !s->prog[j].a.empty(); ++j) {
+        // Diagonal-only blocks inside the run are folded into this pass: a
+        // diagonal gate is one multiply per amplitude whichever bits it reads,
+        // so it needs no chunk of its own (targets mapped back through the
+        // swaps before it; bits outside this chunk add a per-chunk table term).
+        std::vector<GateH> folded;
+        for (size_t j = ii + 1; j < s->prog.size(); ++j) {
+          const InstrH& nx = s->prog[j];
+          if (nx.type == QK_INS_BLOCK && fold && !nx.gates.empty()) {
+            bool diag = true;
+            for (auto& g : nx.gates) {
+              diag = diag && is_diag(g.kind);
+              for (int t : g.t) diag = diag && t >= 0 && t < nb;
+            }
+            if (!diag) break;
+            for (auto& g : nx.gates) {
+              GateH m = g;
+              for (int& t : m.t) t = P[t];
+              folded.push_back(m);
+            }
+            best_j = j + 1;
+            continue;
+          }
+          if (!(nx.type == QK_INS_SQS && !nx.a.empty())) break;
           std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
           bool ok = true;
           for (int q : a) ok = ok && q >= 0 && q < s->L;
@@ -1543,7 +1604,7 @@ int compile_program(qk_sim* s) {
         // on destination bits 0..2, so the gathered stores are 128-B runs and
         // the next chunk is contiguous again.
         std::vector<int> xspec;
-        if (best_d.empty() && xfuse) {
+        if (best_d.empty() && folded.empty() && xfuse) {
           std::vector<int> P2(nb);
           for (int q = 0; q < nb; ++q) P2[q] = q;
           size_t j = ii + 1;
@@ -1585,11 +1646,28 @@ int compile_program(qk_sim* s) {
             }
           }
         }
-        if (!best_d.empty()) {
+        if (!best_d.empty() || !folded.empty()) {
           ip.dest = best_d;
           ip.xspec = xspec;
           const size_t hp_passes = s->hp.passes.size();
-          int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, Cg);
+          int rc;
+          if (folded.empty()) {
+            rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, Cg);
+          } else {
+            // one pass over [0, Cg): the block's gates, then the folded diagonal ones
+            std::vector<GateH> fm = folded;
+            for (auto& g : fm)
+              for (int& t : g.t) t = sigma[t];
+            std::vector<const GateH*> gs;
+            for (auto& g : mapped.gates) gs.push_back(&g);
+            for (auto& g : fm) gs.push_back(&g);
+            std::vector<int> Q;
+            for (int p = 0; p < Cg; ++p) Q.push_back(p);
+            ip.pass0 = (int)hp_passes;
+            rc = compile_pass(s->hp, gs, Q, nb, 0, emsg, best_d.empty() ? nullptr : &best_d);
+            ip.npass = (int)s->hp.passes.size() - ip.pass0;
+            ip.bytes = 32.0 * std::ldexp(1.0, nb) * ip.npass;
+          }
           if (rc) return fail(rc, "%s", emsg.c_str());
           // The cluster exchange moves 7/8 of every chunk over DSMEM (~20 B/clk
           // per SM), so an exchange pass costs ~1.6x a plain pass whatever its
@@ -1597,16 +1675,18 @@ int compile_program(qk_sim* s) {
           const bool x_ok = xspec.empty() || getenv("QK_XFUSE_ALL") ||
                             (ip.npass == 1 && s->hp.passes[hp_passes].nphases == 1);
           if (ip.npass == 1 && x_ok && tma_plan_ok(s->hp, (int)hp_passes, nb)) {
-            std::vector<int> ns(nb);
-            for (int q = 0; q < nb; ++q) ns[q] = best_d[sigma[P[q]]];
-            sigma = ns;
+            if (!best_d.empty()) {  // only folded diagonal blocks: the layout stays
+              std::vector<int> ns(nb);
+              for (int q = 0; q < nb; ++q) ns[q] = best_d[sigma[P[q]]];
+              sigma = ns;
+            }
             for (size_t j = ii + 1; j < best_j; ++j) fused[j] = 1;
             ip.fused_by = -1;
             s->iplan.push_back(std::move(ip));
             const int block_idx = (int)s->iplan.size() - 1;
             for (size_t j = ii + 1; j < best_j; ++j) {
               InstrPlan fp;
-              fp.type = QK_INS_SQS;
+              fp.type = s->prog[j].type;  // SQS, or a folded diagonal block (no pass)
               fp.fused_by = block_idx;
               s->iplan.push_back(std::move(fp));
             }
