@@ -1221,7 +1221,7 @@ int upload_plan(qk_sim* s) {
     }
   }
   for (auto& ip : s->iplan)
-    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) {
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty() && ip.tile.empty()) {
       ip.permuted = s->pass_tma[ip.pass0 + ip.npass - 1] >= 0;
       // the planner already relabeled the qubits for this pass: it must run
       if (!ip.permuted) return fail(QK_ESIM, "internal: fused pass is not executable on the TMA path");
@@ -1372,10 +1372,11 @@ void restore_rounds(const std::vector<int>& lay, std::vector<std::pair<int, int>
   }
 }
 
-bool tma_plan_ok(const HostPlan& hp, int pass, int nbits) {
+bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
   if (getenv("QK_NO_TMA")) return false;
   const PassDesc& pd = hp.passes[pass];
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > (getenv("QK_TMA13") ? 13 : 12) || pd.nphases > kTMaxPh || nbits > 34) return false;
+  if (getenv("QK_TMA13")) cmax = 13;
+  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > cmax || pd.nphases > kTMaxPh || nbits > 34) return false;
   if (pd.nouter != nbits - pd.C) return false;
   const int ob = hp.phases[pd.phase0].op_begin, oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
   int ncoef = 0;
@@ -1447,6 +1448,17 @@ int compile_program(qk_sim* s) {
   std::vector<int> ident(nb);
   for (int q = 0; q < nb; ++q) ident[q] = q;
   std::vector<char> fused(s->prog.size(), 0);
+  auto diag_block = [&](const InstrH& b) {
+    if (b.type != QK_INS_BLOCK || b.gates.empty()) return false;
+    for (auto& g : b.gates) {
+      if (!is_diag(g.kind)) return false;
+      for (int t : g.t)
+        if (t < 0 || t >= nb) return false;
+    }
+    return true;
+  };
+  const bool lazy_fold = lazy && !getenv("QK_NO_FOLD");
+  std::vector<int> folded_into(s->prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
   auto remap = [&](const InstrH& ins) {
     InstrH m = ins;
     for (auto& g : m.gates)
@@ -1457,6 +1469,11 @@ int compile_program(qk_sim* s) {
     auto& ins = s->prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
+    if (ins.type == QK_INS_BLOCK && folded_into[ii] >= 0) {
+      ip.fused_by = folded_into[ii];  // applied by an earlier pass (no kernel)
+      s->iplan.push_back(std::move(ip));
+      continue;
+    }
     if (ins.type == QK_INS_BLOCK && lazy && !ins.gates.empty()) {
       InstrH mapped = remap(ins);
       std::vector<char> inT(nb, 0);
@@ -1475,7 +1492,7 @@ int compile_program(qk_sim* s) {
       std::vector<int> T;
       for (int p = 0; p < nb; ++p)
         if (inT[p]) T.push_back(p);
-      const bool contiguous = T.back() == (int)T.size() - 1 && T.size() <= 12;
+      const bool contiguous = T.back() == (int)T.size() - 1 && T.size() <= 12 && !lazy_fold;
       TileDims tdchk{};
       uint8_t tb8[16] = {0};
       for (size_t x = 0; x < T.size() && x < 16; ++x) tb8[x] = (uint8_t)T[x];
@@ -1490,7 +1507,7 @@ int compile_program(qk_sim* s) {
         for (; jj < s->prog.size(); ++jj) {
           const InstrH& nx = s->prog[jj];
           if (nx.type == QK_INS_BLOCK) {
-            if (!nx.gates.empty()) break;
+            if (!nx.gates.empty() && !(lazy_fold && diag_block(nx))) break;
             continue;
           }
           bool in_local = true;
@@ -1520,16 +1537,63 @@ int compile_program(qk_sim* s) {
             dphys[want[k]] = low[k];
           }
         }
+        // fold the diagonal-only blocks up to the next other block: their
+        // qubits sit (after the lazy swaps in between) at sig3[t], i.e. at
+        // dphys[sig3[t]] before this pass's store permutation
+        std::vector<GateH> folded;
+        std::vector<size_t> folded_at;
+        if (lazy_fold) {
+          std::vector<int> sig3(nb);
+          for (int q = 0; q < nb; ++q) sig3[q] = dphys[sigma[q]];
+          for (size_t j = ii + 1; j < s->prog.size(); ++j) {
+            const InstrH& nx = s->prog[j];
+            if (nx.type == QK_INS_BLOCK) {
+              if (nx.gates.empty()) continue;
+              if (!diag_block(nx)) break;
+              for (auto& g : nx.gates) {
+                GateH m = g;
+                for (int& t : m.t) t = dphys[sig3[t]];
+                folded.push_back(m);
+              }
+              folded_at.push_back(j);
+              continue;
+            }
+            bool in_local = true;
+            for (int q : nx.a) in_local = in_local && q >= 0 && q < nb;
+            for (int q : nx.b) in_local = in_local && q >= 0 && q < nb;
+            if (!in_local) break;
+            std::vector<int> sa = nx.a, sb = nx.b;
+            std::sort(sa.begin(), sa.end());
+            std::sort(sb.begin(), sb.end());
+            for (size_t k = 0; k < sa.size(); ++k) std::swap(sig3[sa[k]], sig3[sb[k]]);
+          }
+        }
         std::vector<const GateH*> gs;
         for (auto& g : mapped.gates) gs.push_back(&g);
+        for (auto& g : folded) gs.push_back(&g);
         ip.pass0 = (int)s->hp.passes.size();
         int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+        if (!rc && !folded.empty() && !tma_plan_ok(s->hp, ip.pass0, nb, 13)) {
+          // too many ops for one specialised pass: the folded blocks run on their own
+          s->hp.passes.resize(ip.pass0);
+          folded.clear();
+          folded_at.clear();
+          gs.resize(mapped.gates.size());
+          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+        }
+        if (!rc && !tma_plan_ok(s->hp, ip.pass0, nb, 13) && dphys != ident) {
+          // the generic pass will run it: no in-tile store permutation
+          s->hp.passes.resize(ip.pass0);
+          dphys = ident;
+          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+        }
         if (rc) return fail(rc, "%s", emsg.c_str());
         ip.npass = (int)s->hp.passes.size() - ip.pass0;
         ip.bytes = 32.0 * std::ldexp(1.0, nb) * ip.npass;
         ip.tile = T;
         ip.dest = dphys;
         for (int& v : sigma) v = dphys[v];
+        for (size_t j : folded_at) folded_into[j] = (int)s->iplan.size();
         s->iplan.push_back(std::move(ip));
         continue;
       }
