@@ -135,6 +135,7 @@ struct alignas(64) TmaParams {
   int32_t nbits;
   int32_t xbits;                // > 0: cluster-exchange store (qk_jit.cpp), 2^xbits CTAs per cluster
   int32_t lazy;                 // 1: strided tile (tbit) loaded through `map` (N-D), stored in place
+  int32_t rowbits;              // lazy: contiguous row bits of the tile view (3: 128-B, 2: 64-B rows)
   int32_t needs_jit;            // 1: ops the interpreter cannot run (outer-bit table terms)
   uint8_t tbit[16];             // lazy: physical address bit of every chunk-local bit (ascending)
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
@@ -162,15 +163,18 @@ struct TileDims {
   int nit;           // iterated chunk-local bits (the top ones)
 };
 
-inline bool tile_dims(const uint8_t* T, int C, int nbits, TileDims* d) {
-  if (C < 3 || C > 16 || nbits > 48 || T[0] != 0 || T[1] != 1 || T[2] != 2) return false;
+// w = row bits: 3 (128-B rows, SWIZZLE_128B) or 2 (64-B rows, SWIZZLE_64B)
+inline bool tile_dims(const uint8_t* T, int C, int nbits, TileDims* d, int w = 3) {
+  if (C < 3 || C > 16 || nbits > 48 || (w != 2 && w != 3)) return false;
+  for (int k = 0; k < w; ++k)
+    if (T[k] != k) return false;
   bool in[64] = {false};
   for (int k = 0; k < C; ++k) in[T[k]] = true;
   int lo[64], len[64], box[64];
   bool tile[64];
   int nd = 0;
-  lo[0] = 0; len[0] = 3; box[0] = 16; tile[0] = true; nd = 1;
-  for (int p = 3; p < nbits;) {
+  lo[0] = 0; len[0] = w; box[0] = 2 << w; tile[0] = true; nd = 1;
+  for (int p = w; p < nbits;) {
     int q = p;
     while (q < nbits && in[q] == in[p]) ++q;
     if (in[p]) {
@@ -192,7 +196,7 @@ inline bool tile_dims(const uint8_t* T, int C, int nbits, TileDims* d) {
   }
   for (int j = 0; j < d->rank; ++j) {
     d->lo[j] = lo[j]; d->len[j] = len[j]; d->box[j] = box[j];
-    if (tile[j]) d->inbox += j == 0 ? 3 : len[j];
+    if (tile[j]) d->inbox += len[j];
   }
   d->nit = C - d->inbox;
   return d->nit >= 0 && d->nit <= 6;

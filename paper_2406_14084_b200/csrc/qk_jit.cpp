@@ -196,6 +196,13 @@ Layout sw128_layout(int C) {
   return m;
 }
 
+// TMA SWIZZLE_64B image (64-B rows): byte bits [4:5] ^= [7:8], i.e. i[0:1] ^= i[3:4]
+Layout sw64_layout(int C) {
+  Layout m(C, 0);
+  for (int p = 0; p < C; ++p) m[p] = p < 3 ? (uint8_t)(1u << p) : (p < 5 ? (uint8_t)(1u << (p - 3)) : 0);
+  return m;
+}
+
 bool indep3(uint8_t a, uint8_t b, uint8_t c) {
   return a && b && c && a != b && (a ^ b) != c && a != c && b != c;
 }
@@ -246,7 +253,7 @@ void emit_bits(std::ostringstream& o, const char* var, const char* src, const ui
 // the chunk index `cv` (its bit k = the k-th non-tile physical bit).
 std::string lazy_loads(const TmaParams& tp, const char* cv, const char* dst, bool prefetch, const char* ind) {
   TileDims td;
-  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td)) return "";
+  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return "";
   std::vector<int> oidx(tp.nbits, -1), tidx(tp.nbits, -1);
   for (int k = 0; k < tp.C; ++k) tidx[tp.tbit[k]] = k;
   int no = 0;
@@ -320,17 +327,24 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   const int hoist = std::min<int>((int)toff->size(),
                                   hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
   // hoist the first `hoist` tables that have no per-chunk (outer-bit) term
-  std::vector<char> hoisted;
+  // and load the first `early` per-chunk tables at the top of the chunk
+  // iteration, so their L2 latency overlaps the stage wait and earlier phases
+  std::vector<char> hoisted, early;
   {
-    int left = hoist;
+    const char* ez = getenv("QK_JIT_EARLY");
+    int left = hoist, eleft = ez ? atoi(ez) : 0;
     for (int ph = 0; ph < tp.nphases; ++ph)
       for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o)
         if (tp.ops[o].code == OP_DIAG) {
           const bool h = left > 0 && tp.ops[o].nco == 0;
+          const bool e = !h && eleft > 0 && tp.ops[o].nco > 0;
           hoisted.push_back(h);
+          early.push_back(e);
           if (h) --left;
+          if (e) --eleft;
         }
   }
+  std::ostringstream ear;  // per-iteration early table loads
   for (size_t t = 0; t < hoisted.size(); ++t)
     if (hoisted[t]) pro << "  double2 tv" << t << "[" << NA << "];\n";
   const int GT = 1 << T;
@@ -339,7 +353,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   b << "    double2 v[" << NA << "];\n";
   // layouts[k]: the smem image phase k reads (0: TMA SWIZZLE_128B)
   std::vector<Layout> layouts(tp.nphases);
-  layouts[0] = sw128_layout(C);
+  layouts[0] = (tp.lazy && tp.rowbits == 2) ? sw64_layout(C) : sw128_layout(C);
   // keep the previous layout when the next phase's lanes are conflict-free
   // under it too: an unchanged layout needs no barrier between a phase's
   // reads and its writes
@@ -403,9 +417,10 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           // entries for every chunk, so the first `hoist` tables are loaded
           // once before the chunk loop and stay in registers.
           const int ti = tab_i++;
-          const bool hz = hoisted[ti];
-          std::ostringstream& dst = hz ? pro : b;
+          const bool hz = hoisted[ti], ez = early[ti];
+          std::ostringstream& dst = hz ? pro : (ez ? ear : b);
           const std::string ind = hz ? "  " : "    ";
+          if (ez) ear << "    double2 te" << ti << "[" << NA << "];\n";
           dst << ind << "{ const double2* tb = p.tabs + p.toff[" << ti << "];\n";
           dst << ind << "  const u32 pt = 0u";
           for (int k = 0; k < T; ++k)
@@ -417,6 +432,10 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
             for (int j = 0; j < NA; ++j) pro << "    tv" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
             pro << "  }\n";
             for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], tv" << ti << "[" << j << "]);\n";
+          } else if (ez) {
+            for (int j = 0; j < NA; ++j) ear << "      te" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
+            ear << "    }\n";
+            for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], te" << ti << "[" << j << "]);\n";
           } else {
             for (int j = 0; j < NA; ++j) b << "      v[" << j << "] = cm(v[" << j << "], __ldg(tb + (pt | " << op.pr[j] << "u)));\n";
             b << "    }\n";
@@ -640,6 +659,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "    if (chunk >= p.nchunks) break;\n"
     << "    const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
     << "    double2* sm = (double2*)(base + (size_t)s * stage_bytes);\n"
+    << ear.str()
     << "    mbar_wait(full + s, round & 1u);\n"
     << b.str()
     << "  }\n}\n";

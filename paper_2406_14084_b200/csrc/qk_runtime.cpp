@@ -485,6 +485,47 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
       if (g->kind == QK_H) ++nh;
     }
   }
+  // 1b. One-qubit gates on distinct qubits with nothing between them commute.
+  //     Order each such segment so the first phase takes high positions and
+  //     the low positions 0..4 go to the second: the first phase then reads
+  //     the TMA image (bank bits from positions < 6) conflict-free and the
+  //     last phase keeps lanes on the low positions (whole-run stores).
+  if (!getenv("QK_NO_REORDER")) {
+    auto one_q = [&](const Item& it) {
+      return it.type == 0 && it.g->t.size() == 1 &&
+             (it.g->kind == QK_H || it.g->kind == QK_X || it.g->kind == QK_U || it.g->kind == QK_RX ||
+              it.g->kind == QK_RY);
+    };
+    for (size_t a = 0; a < items.size();) {
+      if (!one_q(items[a])) {
+        ++a;
+        continue;
+      }
+      size_t b = a;
+      uint32_t seen = 0;
+      while (b < items.size() && one_q(items[b]) && !(seen >> loc[items[b].g->t[0]] & 1))
+        seen |= 1u << loc[items[b++].g->t[0]];
+      if (b - a > (size_t)M) {
+        std::vector<Item> hi, lo;
+        for (size_t k = a; k < b; ++k) (loc[items[k].g->t[0]] < 5 ? lo : hi).push_back(items[k]);
+        auto pos = [&](const Item& it) { return loc[it.g->t[0]]; };
+        std::stable_sort(hi.begin(), hi.end(), [&](const Item& x, const Item& y) { return pos(x) > pos(y); });
+        std::stable_sort(lo.begin(), lo.end(), [&](const Item& x, const Item& y) { return pos(x) < pos(y); });
+        // second group: the M lowest positions; low positions beyond M join
+        // the first group (the last phase keeps lanes 0..4 on positions 0..4)
+        const size_t nmid = std::min(lo.size(), (size_t)M);
+        const size_t nextra = lo.size() - nmid;
+        const size_t nhi0 = nextra < (size_t)M ? std::min(hi.size(), (size_t)M - nextra) : 0;
+        std::vector<Item> ord;
+        for (size_t k = 0; k < nhi0; ++k) ord.push_back(hi[k]);
+        for (size_t k = nmid; k < lo.size(); ++k) ord.push_back(lo[k]);
+        for (size_t k = 0; k < nmid; ++k) ord.push_back(lo[k]);
+        for (size_t k = nhi0; k < hi.size(); ++k) ord.push_back(hi[k]);
+        for (size_t k = 0; k < ord.size(); ++k) items[a + k] = ord[k];
+      }
+      a = b;
+    }
+  }
   // 2. register needs per item
   auto needs = [&](const Item& it) -> std::vector<int> {
     if (it.type == 1) return {};
@@ -1020,20 +1061,20 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
 // N-D strided view of `buf` for the tile of a lazy pass (qk_internal.h tile_dims)
 bool encode_lazy_map(const TmaParams& tp, double* buf, CUtensorMap* out) {
   TileDims td{};
-  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td)) return false;
+  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return false;
   auto fn = encode_fn();
   if (!fn || !buf) return false;
   cuuint64_t dims[5];
   cuuint64_t strides[4];
   cuuint32_t box[5], es[5];
   for (int j = 0; j < td.rank; ++j) {
-    dims[j] = j == 0 ? 16 : (cuuint64_t)1 << td.len[j];
+    dims[j] = j == 0 ? (cuuint64_t)(2 << td.len[0]) : (cuuint64_t)1 << td.len[j];
     if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
     box[j] = (cuuint32_t)td.box[j];
     es[j] = 1;
   }
   return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, td.rank, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            tp.rowbits == 2 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1052,7 +1093,8 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
     // bit k <-> the k-th non-tile bit; stored in place through the permuted path
     uint8_t tb[16];
     for (int x = 0; x < pd.C; ++x) tb[x] = (uint8_t)(*tile)[x];
-    if ((int)tile->size() != pd.C || !tile_dims(tb, pd.C, s->nbits, &td)) return false;
+    const int w = (pd.C > 2 && (*tile)[2] == 2) ? 3 : 2;
+    if ((int)tile->size() != pd.C || !tile_dims(tb, pd.C, s->nbits, &td, w)) return false;
     std::vector<char> in(s->nbits, 0);
     for (int p : *tile) in[p] = 1;
     for (int p : *tile) vdest.push_back(dest ? (*dest)[p] : p);  // in-tile store permutation
@@ -1068,6 +1110,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
   memset(&tp, 0, sizeof tp);
   if (lz) {
     tp.lazy = 1;
+    tp.rowbits = ((*tile)[2] == 2) ? 3 : 2;
     tp.C = pd.C;
     tp.nbits = s->nbits;
     for (int x = 0; x < pd.C; ++x) tp.tbit[x] = (uint8_t)(*tile)[x];
@@ -1484,7 +1527,22 @@ int compile_program(qk_sim* s) {
           inT[t] = 1;
           maxt = std::max(maxt, t);
         }
-      for (int p = 0; p < 3; ++p) inT[p] = 1;
+      // row bits: 0..2 (128-B rows); when that makes a 13-bit tile (one
+      // 128-KiB stage) and 0..1 keeps it at 12, take 64-B rows and 3 stages,
+      // unless the tile spans many 2-MiB pages (address bits >= 17): its 1024
+      // rows then miss the TLB and half-size rows double that cost per byte
+      // (H33: 50 ms with 8 pages, 118 ms with 1024 pages, 88 ms at 128-B rows)
+      int rows = 3;
+      {
+        int c3 = 0, c2b = 0, pagebits = 0;
+        for (int p = 0; p < nb; ++p) {
+          c3 += inT[p] || p < 3;
+          c2b += inT[p] || p < 2;
+          pagebits += inT[p] && p >= 17;
+        }
+        if (c3 > 12 && c2b <= 12 && pagebits <= 4 && !getenv("QK_NO_ROW64")) rows = 2;
+      }
+      for (int p = 0; p < rows; ++p) inT[p] = 1;
       int cnt = 0;
       for (char c2 : inT) cnt += c2;
       for (int p = 0; p < nb && cnt < 10; ++p)
@@ -1496,7 +1554,7 @@ int compile_program(qk_sim* s) {
       TileDims tdchk{};
       uint8_t tb8[16] = {0};
       for (size_t x = 0; x < T.size() && x < 16; ++x) tb8[x] = (uint8_t)T[x];
-      if (cnt <= 13 && !contiguous && tile_dims(tb8, cnt, nb, &tdchk)) {
+      if (cnt <= 13 && !contiguous && tile_dims(tb8, cnt, nb, &tdchk, inT[2] ? 3 : 2)) {
         // Store permutation inside the tile (in place, same address set):
         // qubits the next block needs move onto bits 0..2, so its tile only
         // has to add what is missing (10 bits instead of 13 when all fit).
@@ -1531,7 +1589,7 @@ int compile_program(qk_sim* s) {
           for (int p : T)
             if (p >= 3 && need[p]) want.push_back(p);
           for (int p = 0; p < 3; ++p)
-            if (!need[p]) low.push_back(p);
+            if (!need[p] && inT[p]) low.push_back(p);  // in place: only inside the tile
           for (size_t k = 0; k < want.size() && k < low.size(); ++k) {
             dphys[low[k]] = want[k];
             dphys[want[k]] = low[k];

@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_block_tma(const __grid_constant
 
 static int consumers_for(int C, int M) {
   if (M == 4 && C == 12 && getenv("QK_NG2")) return 512;
+  if (M == 4 && C <= 11 && getenv("QK_CONS")) return atoi(getenv("QK_CONS"));
   return M == 4 ? kConsumers4 : kConsumers3;
 }
 
