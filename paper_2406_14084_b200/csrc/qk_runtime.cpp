@@ -426,7 +426,8 @@ struct Item {
 // Compile the gates of one pass over chunk address bits Q (ascending) of a
 // vector of `nbits` address bits.
 int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std::vector<int>& Q,
-                 int nbits, uint64_t ncta_override, std::string& emsg, const std::vector<int>* dest = nullptr) {
+                 int nbits, uint64_t ncta_override, std::string& emsg, const std::vector<int>* dest = nullptr,
+                 int lanes_req = 5) {
   const int C = (int)Q.size();
   int M = std::min(kMaxM, C);
   if (C >= 9 && C <= 12 && Q.back() == C - 1 && getenv("QK_M")) M = std::max(3, std::min(4, atoi(getenv("QK_M"))));
@@ -570,7 +571,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     for (int q = 0; q < C; ++q) by_dest.push_back(q);
     std::sort(by_dest.begin(), by_dest.end(), [&](int x, int y) { return (*dest)[Q[x]] < (*dest)[Q[y]]; });
     bool ok = !phs.empty();
-    for (int i = 0; i < 5 && i < C && ok; ++i)
+    for (int i = 0; i < lanes_req && i < C && ok; ++i)
       if (std::find(phs.back().R.begin(), phs.back().R.end(), by_dest[i]) != phs.back().R.end()) ok = false;
     if (!ok) {
       PhaseB pb;
@@ -1590,9 +1591,42 @@ int compile_program(qk_sim* s) {
             if (p >= 3 && need[p]) want.push_back(p);
           for (int p = 0; p < 3; ++p)
             if (!need[p] && inT[p]) low.push_back(p);  // in place: only inside the tile
-          for (size_t k = 0; k < want.size() && k < low.size(); ++k) {
-            dphys[low[k]] = want[k];
-            dphys[want[k]] = low[k];
+          // The qubits moved onto the row bits must be lanes of the last phase;
+          // when that costs a layout-only phase, try other picks among the
+          // wanted qubits (phase count of the block's own gates decides).
+          std::vector<const GateH*> own;
+          for (auto& g : mapped.gates) own.push_back(&g);
+          auto nph = [&](const std::vector<int>& dp) {
+            HostPlan tmp;
+            std::string em;
+            if (compile_pass(tmp, own, T, nb, 0, em, &dp, inT[2] ? 3 : 2) || tmp.passes.empty()) return 99;
+            return tmp.passes.back().nphases;
+          };
+          auto make = [&](const std::vector<int>& pick) {
+            std::vector<int> dp = ident;
+            for (size_t k = 0; k < pick.size() && k < low.size(); ++k) {
+              dp[low[k]] = pick[k];
+              dp[pick[k]] = low[k];
+            }
+            return dp;
+          };
+          std::vector<std::vector<int>> cands;
+          cands.push_back(want);
+          cands.push_back(std::vector<int>(want.rbegin(), want.rend()));
+          for (size_t k = 0; k + low.size() <= want.size() && k < 8; ++k)
+            cands.push_back(std::vector<int>(want.begin() + k, want.end()));
+          int best_ph = 99;
+          size_t best_moves = 0;
+          for (auto& c : cands) {
+            const std::vector<int> dp = make(c);
+            const int ph = nph(dp);
+            const size_t mv = std::min(c.size(), low.size());
+            // more moves first (the next tile shrinks), then fewer phases
+            if (mv > best_moves || (mv == best_moves && ph < best_ph)) {
+              best_ph = ph;
+              best_moves = mv;
+              dphys = dp;
+            }
           }
         }
         // fold the diagonal-only blocks up to the next other block: their
@@ -1630,20 +1664,20 @@ int compile_program(qk_sim* s) {
         for (auto& g : mapped.gates) gs.push_back(&g);
         for (auto& g : folded) gs.push_back(&g);
         ip.pass0 = (int)s->hp.passes.size();
-        int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+        int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys, inT[2] ? 3 : 2);
         if (!rc && !folded.empty() && !tma_plan_ok(s->hp, ip.pass0, nb, 13)) {
           // too many ops for one specialised pass: the folded blocks run on their own
           s->hp.passes.resize(ip.pass0);
           folded.clear();
           folded_at.clear();
           gs.resize(mapped.gates.size());
-          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys, inT[2] ? 3 : 2);
         }
         if (!rc && !tma_plan_ok(s->hp, ip.pass0, nb, 13) && dphys != ident) {
           // the generic pass will run it: no in-tile store permutation
           s->hp.passes.resize(ip.pass0);
           dphys = ident;
-          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys);
+          rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys, inT[2] ? 3 : 2);
         }
         if (rc) return fail(rc, "%s", emsg.c_str());
         ip.npass = (int)s->hp.passes.size() - ip.pass0;
