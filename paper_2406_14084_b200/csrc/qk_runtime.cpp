@@ -1541,7 +1541,11 @@ int compile_program(qk_sim* s) {
           c2b += inT[p] || p < 2;
           pagebits += inT[p] && p >= 17;
         }
-        if (c3 > 12 && c2b <= 12 && pagebits <= 4 && !getenv("QK_NO_ROW64")) rows = 2;
+        // dense 2x2 gates keep the 13-bit tile: its 512 consumer threads hide
+        // the FP64 chains the 256-thread 12-bit pass exposes (U33: 124 vs 90 ms)
+        bool dense = false;
+        for (auto& g : mapped.gates) dense = dense || g.kind == QK_U || g.kind == QK_RX || g.kind == QK_RY;
+        if (c3 > 12 && c2b <= 12 && pagebits <= 4 && !dense && !getenv("QK_NO_ROW64")) rows = 2;
       }
       for (int p = 0; p < rows; ++p) inT[p] = 1;
       int cnt = 0;
