@@ -542,6 +542,125 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     std::vector<int> items;
   };
   std::vector<PhaseB> phs;
+  // Dependency-aware list scheduling: gates that commute (disjoint qubits,
+  // diagonal runs, a diagonal on a CX control, CX sharing only a target or
+  // only a control) may run in any order. Each phase picks the register set
+  // that lets the most ready items run (program-order lookahead vs the most
+  // frequent qubits among upcoming items), simulated greedily.
+  if (!getenv("QK_OLD_PHASES")) {
+    const size_t n = items.size();
+    auto support = [&](const Item& it) -> uint32_t {
+      if (it.type == 1) return run_support[it.run];
+      uint32_t m = 0;
+      for (int t : it.g->t) m |= 1u << loc[t];
+      return m;
+    };
+    auto commute = [&](const Item& a, const Item& b) {
+      const uint32_t sa = support(a), sb = support(b), both = sa & sb;
+      if (!both) return true;
+      if (a.type == 1 && b.type == 1) return true;
+      const Item* d = a.type == 1 ? &a : (b.type == 1 ? &b : nullptr);
+      const Item* o = d == &a ? &b : &a;
+      if (d && o->type == 0 && o->g->kind == QK_CX) return both == (1u << loc[o->g->t[0]]);  // diag on control
+      if (!d && a.g->kind == QK_CX && b.g->kind == QK_CX) {
+        const int ac = loc[a.g->t[0]], at = loc[a.g->t[1]], bc = loc[b.g->t[0]], bt = loc[b.g->t[1]];
+        if (at == bt && ac != bc && ac != bt && bc != at) return true;   // same target
+        if (ac == bc && at != bt && at != bc && bt != ac) return true;   // same control
+      }
+      return false;
+    };
+    std::vector<std::vector<int>> preds(n);
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = 0; j < i; ++j)
+        if (!commute(items[j], items[i])) preds[i].push_back((int)j);
+    std::vector<char> done(n, 0);
+    size_t left = n;
+    auto in_r = [](const std::vector<int>& R, int q) { return std::find(R.begin(), R.end(), q) != R.end(); };
+    auto runs_with = [&](const std::vector<int>& R, std::vector<char>& dn, std::vector<int>* order) {
+      int cnt = 0;
+      for (bool progress = true; progress;) {
+        progress = false;
+        for (size_t i = 0; i < n; ++i) {
+          if (dn[i]) continue;
+          bool ok = true;
+          for (int p : preds[i]) ok = ok && dn[p];
+          if (!ok) continue;
+          for (int q : needs(items[i])) ok = ok && in_r(R, q);
+          if (!ok) continue;
+          dn[i] = 1;
+          ++cnt;
+          progress = true;
+          if (order) order->push_back((int)i);
+        }
+      }
+      return cnt;
+    };
+    while (left) {
+      // first ready item that needs registers (diagonal-only readiness runs anywhere)
+      int first = -1;
+      for (size_t i = 0; i < n && first < 0; ++i) {
+        if (done[i]) continue;
+        bool ok = true;
+        for (int p : preds[i]) ok = ok && done[p];
+        if (ok && !needs(items[i]).empty()) first = (int)i;
+      }
+      std::vector<std::vector<int>> cands;
+      if (first >= 0) {
+        std::vector<int> base = needs(items[first]);
+        // (a) program-order lookahead over the items not yet done
+        std::vector<int> a = base;
+        for (size_t j = first + 1; j < n && (int)a.size() < M; ++j)
+          if (!done[j])
+            for (int q : needs(items[j]))
+              if ((int)a.size() < M && !in_r(a, q)) a.push_back(q);
+        cands.push_back(a);
+        // (b) most frequent qubits among the next 48 items' needs
+        std::vector<int> freq(C, 0);
+        int seen = 0;
+        for (size_t j = first; j < n && seen < 48; ++j)
+          if (!done[j]) {
+            ++seen;
+            for (int q : needs(items[j])) freq[q]++;
+          }
+        std::vector<int> b = base;
+        while ((int)b.size() < M) {
+          int best = -1;
+          for (int q = 0; q < C; ++q)
+            if (!in_r(b, q) && freq[q] > 0 && (best < 0 || freq[q] > freq[best])) best = q;
+          if (best < 0) break;
+          b.push_back(best);
+        }
+        cands.push_back(b);
+      } else {
+        cands.push_back({});
+      }
+      int best_c = -1, best_n = -1;
+      for (size_t c = 0; c < cands.size(); ++c) {
+        auto& R = cands[c];
+        for (int q = C - 1; q >= 0 && (int)R.size() < M; --q)  // fill with high positions
+          if (!in_r(R, q)) R.push_back(q);
+        std::vector<char> dn = done;
+        const int k = runs_with(R, dn, nullptr);
+        if (k > best_n) {
+          best_n = k;
+          best_c = (int)c;
+        }
+      }
+      PhaseB pb;
+      pb.R = cands[best_c];
+      runs_with(pb.R, done, &pb.items);
+      if (pb.items.empty()) {
+        emsg = "internal: phase scheduling made no progress";
+        return QK_ESIM;
+      }
+      left -= pb.items.size();
+      phs.push_back(pb);
+    }
+  }
+  // the program-order builder; the scheduled phases replace it only when
+  // they need fewer phases (QAOA's layers keep the program-order phases)
+  std::vector<PhaseB> sched;
+  sched.swap(phs);
   for (size_t i = 0; i < items.size(); ++i) {
     std::vector<int> need = needs(items[i]);
     bool fits = !phs.empty();
@@ -561,6 +680,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std
     }
     phs.back().items.push_back((int)i);
   }
+  if (!sched.empty() && sched.size() < phs.size()) phs.swap(sched);
   if (phs.empty() && !dest) return QK_OK;  // no gates at all: nothing to do
   if (dest) {
     // fused (permuted) store: the 5 positions landing on destination bits
