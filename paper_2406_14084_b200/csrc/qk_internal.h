@@ -226,6 +226,7 @@ int launch_sqs_bulk(double* state, const SqsDesc* h, int num_sms, CUstream_st* s
 int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p, const int* q,
                      int np, const int* a, const int* b, int k, CUstream_st* stream);
 int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* stream);
+int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int npos, CUstream_st* stream);
 int launch_sumsq(const double* state, uint64_t n_amps, double* d_partial, double* d_out,
                  CUstream_st* stream);
 int launch_gather(const double* state, const uint64_t* d_idx, uint64_t count, double* d_out,

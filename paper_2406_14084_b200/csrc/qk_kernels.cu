@@ -561,6 +561,47 @@ __global__ void k_swap_seg(double2* __restrict__ a, double2* __restrict__ b, uin
   }
 }
 
+// Strided segment exchange: element t of the segment sits at
+// deposit(t) = sum over runs of ((t >> src) & (2^len - 1)) << dst, the same
+// offsets in both shards (every shard holds the same layout).
+struct SwapRuns {
+  int32_t n;
+  uint8_t src[24], dst[24], len[24];
+};
+
+__global__ void k_swap_strided(double2* __restrict__ a, double2* __restrict__ b, uint64_t n,
+                               const __grid_constant__ SwapRuns R) {
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t off = 0;
+    for (int k = 0; k < R.n; ++k) off |= ((t >> R.src[k]) & ((1ull << R.len[k]) - 1)) << R.dst[k];
+    const double2 x = ld_g(a + off);
+    const double2 y = ld_g(b + off);
+    st_g(a + off, y);
+    st_g(b + off, x);
+  }
+}
+
+int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int npos, CUstream_st* stream) {
+  // pos: physical positions of the free bits (ascending = thread-order bits)
+  if (!n) return 0;
+  SwapRuns R{};
+  for (int k = 0; k < npos;) {
+    int e = k + 1;
+    while (e < npos && pos[e] == pos[e - 1] + 1) ++e;
+    if (R.n >= 24) return -1;
+    R.src[R.n] = (uint8_t)k;
+    R.dst[R.n] = (uint8_t)pos[k];
+    R.len[R.n] = (uint8_t)(e - k);
+    ++R.n;
+    k = e;
+  }
+  const uint64_t blocks = (n + 255) / 256;
+  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  k_swap_strided<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), n, R);
+  return (int)cudaGetLastError();
+}
+
 int launch_swap_segments(double* a, double* b, uint64_t n, CUstream_st* stream) {
   if (!n) return 0;
   const uint64_t blocks = (n + 255) / 256;

@@ -383,6 +383,7 @@ struct InstrPlan {
   std::vector<int> xspec;    // block: spectator source bits of a cluster-exchange store (qk_jit.cpp)
   int lazy = 0;              // SQS / local CSQS absorbed into the lazy layout: no kernel
   std::vector<int> tile;     // block: strided tile (physical bits) of a lazy in-place pass
+  std::vector<int> xlay;     // cross-process CSQS: layout (reference bit -> physical) at the exchange
   int sqs = -1;              // SQS / single-device CSQS
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
@@ -2032,7 +2033,8 @@ int compile_program(qk_sim* s) {
         s->iplan.push_back(std::move(ip));
         continue;
       }
-      if (!local_only && lazy && !lay_identity(sigma) && !emit_restore())
+      const bool strided_x = !getenv("QK_NO_STRIDED_XRS");
+      if (!local_only && lazy && !strided_x && !lay_identity(sigma) && !emit_restore())
         return fail(QK_ESIM, "internal: layout restore failed");
       if (local_only) {
         std::vector<int> sa = ins.a, sb = ins.b;
@@ -2045,10 +2047,11 @@ int compile_program(qk_sim* s) {
         }
         ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
       } else {
-        ip.sqs = -2;  // cross-process exchange: needs the reference layout
+        ip.sqs = -2;  // cross-process exchange over the current layout (strided segments)
+        ip.xlay = sigma;
         bool id = true;
         for (int q = 0; q < nb; ++q) id = id && sigma[q] == q;
-        if (!id) {
+        if (!id && !strided_x) {
           std::vector<int> d(nb);
           for (int q = 0; q < nb; ++q) d[sigma[q]] = q;
           InstrPlan rp;
@@ -2061,6 +2064,7 @@ int compile_program(qk_sim* s) {
           rp.synthetic = 1;
           s->iplan.push_back(std::move(rp));
           for (int q = 0; q < nb; ++q) sigma[q] = q;
+          ip.xlay = sigma;
         }
       }
       ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
@@ -2271,11 +2275,29 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
   }
+  const bool ident_lay = ip.xlay.empty() || lay_identity(ip.xlay);
+  auto lay_of = [&](uint64_t i) {
+    if (ident_lay) return i;
+    uint64_t j = 0;
+    for (int q = 0; q < s->nbits; ++q) j |= ((i >> q) & 1ull) << ip.xlay[q];
+    return j;
+  };
   for (auto& sg : segs) {
     // every shard runs the same plan, so the peers' current buffer is bufs[cur] too
     double* peer_state = (s->cur ? s->peers1 : s->peers)[sg.peer];
-    rc = launch_swap_segments(s->state + 2 * sg.my_off, peer_state + 2 * sg.peer_off, sg.len,
-                              (CUstream_st*)s->stream);
+    if (ident_lay) {
+      rc = launch_swap_segments(s->state + 2 * sg.my_off, peer_state + 2 * sg.peer_off, sg.len,
+                                (CUstream_st*)s->stream);
+    } else {
+      // lazy / relabeled layout: the segment's free reference bits 0..k-1 sit at
+      // xlay[0..k-1]; enumerate them in physical order (coalesced runs)
+      const int k = __builtin_ctzll(sg.len);
+      std::vector<int> pos;
+      for (int q = 0; q < k; ++q) pos.push_back(ip.xlay[q]);
+      std::sort(pos.begin(), pos.end());
+      rc = launch_swap_strided(s->state + 2 * lay_of(sg.my_off), peer_state + 2 * lay_of(sg.peer_off), sg.len,
+                               pos.data(), (int)pos.size(), (CUstream_st*)s->stream);
+    }
     if (rc) return fail(QK_ECUDA, "peer exchange failed");
   }
   if (s->barrier) {
@@ -2284,7 +2306,20 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   }
   if (!in_a.empty()) {
     HostPlan tmp;
-    compile_sqs(tmp, in_a, in_b, s->nbits);
+    if (!ident_lay) {  // in-shard pairs act on the bits' current positions
+      std::vector<int> sa = in_a, sb = in_b;
+      std::sort(sa.begin(), sa.end());
+      std::sort(sb.begin(), sb.end());
+      in_a.clear();
+      in_b.clear();
+      for (size_t k = 0; k < sa.size(); ++k) {
+        in_a.push_back(ip.xlay[sa[k]]);
+        in_b.push_back(ip.xlay[sb[k]]);
+      }
+      compile_sqs(tmp, in_a, in_b, s->nbits, true);
+    } else {
+      compile_sqs(tmp, in_a, in_b, s->nbits);
+    }
     rc = launch_sqs(s->state, &tmp.sqs[0], nullptr, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "in-shard swap failed");
     CUDA_TRY(cudaStreamSynchronize(s->stream));

@@ -22,7 +22,7 @@ def _port():
 
 
 CIRCUITS = [("example", 10, 4, 2, 8), ("random", 12, 5, 2, 6), ("random3", 13, 6, 3, 7),
-            ("random18", 18, 8, 1, 10)]
+            ("random18", 18, 8, 1, 10), ("random19r2", 19, 8, 2, 10), ("random19c12", 19, 12, 1, 12)]
 
 
 def _circuit(name, n, c, r, seed=0):
@@ -61,15 +61,16 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["default", "lazy"])
+@pytest.mark.parametrize("mode", ["default", "lazy", "relabel"])
 def test_two_processes_share_the_state(gpu, mode):
     """`lazy`: the shards run in place with the lazy layout (QK_INPLACE, JIT at
-    every size), so cross-shard CSQS follow layout restores."""
+    every size); `relabel`: double-buffered shards with relabeled stores. In
+    both, cross-shard CSQS exchange strided segments of the current layout."""
     import torch.multiprocessing as mp
     from paper_2406_14084_b200 import LayoutParams, Simulator
     mgr = mp.Manager()
     results = mgr.dict()
-    env = {"QK_INPLACE": "1", "QK_JIT": "0"} if mode == "lazy" else {}
+    env = {"lazy": {"QK_INPLACE": "1", "QK_JIT": "0"}, "relabel": {"QK_JIT": "0"}}.get(mode, {})
     os.environ.update(env)
     try:
         mp.spawn(_worker, args=(2, _port(), results), nprocs=2, join=True)
