@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <deque>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -426,9 +427,47 @@ struct Item {
 
 // Compile the gates of one pass over chunk address bits Q (ascending) of a
 // vector of `nbits` address bits.
-int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates, const std::vector<int>& Q,
+int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const std::vector<int>& Q,
                  int nbits, uint64_t ncta_override, std::string& emsg, const std::vector<int>* dest = nullptr,
                  int lanes_req = 5) {
+  // 0. U(th, ph, la) = P(ph) RY(th) P(la) with P(a) = diag(1, e^{ia}) exactly
+  //    (circuit.py:420-423 Qiskit form). A run of U gates on distinct qubits
+  //    becomes [all P(la)] [all RY] [all P(ph)]: the phase gates join two
+  //    diagonal tables and each RY costs 4 FMAs per pair instead of 12.
+  std::deque<GateH> expanded;
+  std::vector<const GateH*> gates;
+  for (size_t i = 0; i < gates_in.size();) {
+    const GateH* g = gates_in[i];
+    if (g->kind != QK_U || getenv("QK_NO_UDECOMP") || g->p.size() < 3) {
+      gates.push_back(g);
+      ++i;
+      continue;
+    }
+    size_t e = i;
+    uint64_t seen = 0;
+    while (e < gates_in.size() && gates_in[e]->kind == QK_U && gates_in[e]->p.size() >= 3 &&
+           !(seen >> gates_in[e]->t[0] & 1))
+      seen |= 1ull << gates_in[e++]->t[0];
+    auto phase = [&](int q, double a) {
+      GateH d;
+      d.kind = QK_D;
+      d.t = {q};
+      d.p = {1.0, 0.0, std::cos(a), std::sin(a)};
+      expanded.push_back(d);
+      gates.push_back(&expanded.back());
+    };
+    for (size_t k = i; k < e; ++k) phase(gates_in[k]->t[0], gates_in[k]->p[2]);
+    for (size_t k = i; k < e; ++k) {
+      GateH ry;
+      ry.kind = QK_RY;
+      ry.t = gates_in[k]->t;
+      ry.p = {gates_in[k]->p[0]};
+      expanded.push_back(ry);
+      gates.push_back(&expanded.back());
+    }
+    for (size_t k = i; k < e; ++k) phase(gates_in[k]->t[0], gates_in[k]->p[1]);
+    i = e;
+  }
   const int C = (int)Q.size();
   int M = std::min(kMaxM, C);
   if (C >= 9 && C <= 12 && Q.back() == C - 1 && getenv("QK_M")) M = std::max(3, std::min(4, atoi(getenv("QK_M"))));
@@ -1869,7 +1908,10 @@ int compile_program(qk_sim* s) {
           // >= 5 qubits that stay in the chunk go to destination bits 0..4, so
           // every warp writes whole 512-B runs (128-B runs scattered at 64-KiB
           // strides measured slower than a separate SQS pass)
-          if (stay.size() < 5) break;
+          if (stay.size() < 5) {
+            if (getenv("QK_DUMP_PLAN")) fprintf(stderr, "relabel: swap run stops at instr %zu with %zu staying\n", j, stay.size());
+            break;
+          }
           std::vector<int> d(nb);
           int pos = 0;
           for (int x : stay) d[x] = pos++;
