@@ -42,6 +42,8 @@ WORKLOADS = {
     "qaoa24": ("qaoa24_c12_r0.txt", 24, 12, 0),
     "bv30": ("bv30_c10_r0.txt", 30, 10, 0),
     "h30": ("h30_c10_r0.txt", 30, 10, 0),
+    # 8 rank partitions of 30 qubits held by one handle: 128 GiB in place
+    "qaoa33r3": ("qaoa33_c12_r3.txt", 33, 12, 3),
 }
 MULTI = {2: ("qaoa31_c12_r1.txt", 31, 12, 1), 4: ("qaoa32_c12_r2.txt", 32, 12, 2),
          8: ("qaoa33_c12_r3.txt", 33, 12, 3)}

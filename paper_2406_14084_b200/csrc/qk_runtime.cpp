@@ -1601,10 +1601,11 @@ int compile_program(qk_sim* s) {
   // address bits, so every warp still writes whole 512-B runs.
   int Cg = 0;
   bool relabel = s->bufs[1] && !getenv("QK_NO_FUSE") && !getenv("QK_NO_TMA");
+  bool all_chunked = true;
   for (auto& ins : s->prog) {
     if (ins.type != QK_INS_BLOCK || ins.gates.empty()) continue;
     const int w = block_chunk_width(ins, s->L);
-    if (!w) relabel = false;
+    if (!w) relabel = all_chunked = false;
     Cg = std::max(Cg, w);
   }
   if (Cg < 9 || Cg > 12 || Cg > nb) relabel = false;
@@ -1623,7 +1624,9 @@ int compile_program(qk_sim* s) {
   // then stay <= 13 bits; QFT30: 0.112 s lazy vs 0.132 s relabeled).
   const bool lazy_ok = !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") && jit_available() &&
                        nb >= (jenv ? atoi(jenv) : 20) && nb >= 16;
-  const bool lazy = lazy_ok && (!s->bufs[1] || (relabel && Cg <= 10));
+  // (chunks wider than 10 qubits would need tiles over 13 bits: those
+  // programs execute their swaps, e.g. QAOA c12 at 33 qubits in place)
+  const bool lazy = lazy_ok && all_chunked && Cg <= 10 && (!s->bufs[1] || relabel);
   if (lazy) relabel = false;
   auto emit_restore = [&]() {
     std::vector<std::pair<int, int>> rounds[2];
@@ -1662,6 +1665,7 @@ int compile_program(qk_sim* s) {
     return true;
   };
   const bool lazy_fold = lazy && !getenv("QK_NO_FOLD");
+  const bool fold_eager = !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   std::vector<int> folded_into(s->prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
   auto remap = [&](const InstrH& ins) {
     InstrH m = ins;
@@ -2020,6 +2024,55 @@ int compile_program(qk_sim* s) {
           s->hp.passes.resize(hp_passes);
           ip.dest.clear();
           ip.xspec.clear();
+        }
+      }
+      // Eager mode (swaps executed as passes, e.g. QAOA c12 in place): the
+      // diagonal-only blocks up to the next other block still fold into this
+      // pass, their targets mapped back through the swaps in between.
+      const int w_own = block_chunk_width(ins, s->L);
+      if (!relabel && !lazy && fold_eager && !ins.gates.empty() && w_own >= 9 && w_own <= 12) {
+        std::vector<int> P(nb);
+        for (int q = 0; q < nb; ++q) P[q] = q;
+        std::vector<GateH> folded;
+        std::vector<size_t> folded_at;
+        for (size_t j = ii + 1; j < s->prog.size(); ++j) {
+          const InstrH& nx = s->prog[j];
+          if (nx.type == QK_INS_BLOCK) {
+            if (nx.gates.empty()) continue;
+            if (!diag_block(nx)) break;
+            for (auto& g : nx.gates) {
+              GateH m = g;
+              for (int& t : m.t) t = P[t];
+              folded.push_back(m);
+            }
+            folded_at.push_back(j);
+            continue;
+          }
+          bool in_local = true;
+          for (int q : nx.a) in_local = in_local && q >= 0 && q < s->L;
+          for (int q : nx.b) in_local = in_local && q >= 0 && q < s->L;
+          if (nx.type != QK_INS_SQS || !in_local) break;  // CSQS: stop folding there
+          std::vector<int> sa = nx.a, sb = nx.b;
+          std::sort(sa.begin(), sa.end());
+          std::sort(sb.begin(), sb.end());
+          for (size_t k = 0; k < sa.size(); ++k) std::swap(P[sa[k]], P[sb[k]]);
+        }
+        if (!folded.empty()) {
+          std::vector<const GateH*> gs;
+          for (auto& g : mapped.gates) gs.push_back(&g);
+          for (auto& g : folded) gs.push_back(&g);
+          std::vector<int> Q;
+          for (int p = 0; p < w_own; ++p) Q.push_back(p);
+          ip.pass0 = (int)s->hp.passes.size();
+          int rc = compile_pass(s->hp, gs, Q, nb, 0, emsg);
+          if (!rc && tma_plan_ok(s->hp, ip.pass0, nb)) {
+            ip.npass = (int)s->hp.passes.size() - ip.pass0;
+            ip.bytes = 32.0 * std::ldexp(1.0, nb) * ip.npass;
+            for (size_t j : folded_at) folded_into[j] = (int)s->iplan.size();
+            s->iplan.push_back(std::move(ip));
+            continue;
+          }
+          s->hp.passes.resize(ip.pass0);  // too many ops: no fold
         }
       }
       int rc = compile_block(s->hp, mapped, s->L, nb, ip, emsg, 10, relabel ? Cg : 0);
