@@ -1666,6 +1666,7 @@ int compile_program(qk_sim* s) {
   };
   const bool lazy_fold = lazy && !getenv("QK_NO_FOLD");
   const bool fold_eager = !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
+  const bool merge_sqs = !relabel && !lazy && !getenv("QK_NO_SQS_MERGE");
   std::vector<int> folded_into(s->prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
   auto remap = [&](const InstrH& ins) {
     InstrH m = ins;
@@ -1677,6 +1678,12 @@ int compile_program(qk_sim* s) {
     auto& ins = s->prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
+    // eager mode: a run of swaps (diagonal blocks folded away in between) is
+    // composed on the host and executed as at most two SQS passes, since any
+    // bit permutation is a product of two involutions (restore_rounds)
+    if (merge_sqs && !lay_identity(sigma) && ins.type != QK_INS_SQS &&
+        !(ins.type == QK_INS_BLOCK && (folded_into[ii] >= 0 || ins.gates.empty())) && !emit_restore())
+      return fail(QK_ESIM, "internal: swap run merge failed");
     if (ins.type == QK_INS_BLOCK && folded_into[ii] >= 0) {
       ip.fused_by = folded_into[ii];  // applied by an earlier pass (no kernel)
       s->iplan.push_back(std::move(ip));
@@ -2097,7 +2104,7 @@ int compile_program(qk_sim* s) {
         a.push_back(sigma[sa[k]]);
         b.push_back(sigma[sb[k]]);
       }
-      if (lazy) {
+      if (lazy || merge_sqs) {
         // relabel only: sigma'[sa_k] = sigma[sb_k] and vice versa
         for (size_t k = 0; k < sa.size(); ++k) std::swap(sigma[sa[k]], sigma[sb[k]]);
         ip.lazy = 1;
@@ -2166,6 +2173,7 @@ int compile_program(qk_sim* s) {
     }
     s->iplan.push_back(std::move(ip));
   }
+  if (merge_sqs && !lay_identity(sigma) && !emit_restore()) return fail(QK_ESIM, "internal: swap run merge failed");
   // lazy mode: the handle keeps the end layout; relabel mode restores it
   s->lay_final = ident;
   if (lazy) {
