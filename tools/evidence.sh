@@ -8,7 +8,7 @@ nvidia-smi > $T/smi.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $T/pytest.log 2>&1; echo "rc=$?" >> $T/pytest.log
 python -c "import __graft_entry__ as g; g.smoke()" > $T/smoke.log 2>&1
 timeout 600 python bench.py > $T/bench_default.json 2> $T/bench_default.err
-for w in qft20 bv33 h33 rzz33 u33 qft33 qft30 bv30 qaoa26; do
+for w in qft20 bv33 h33 rzz33 u33 qft33 qft30 bv30 qaoa26 qaoa33r3; do
   timeout 300 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu >> $T/bench_all.json 2>> $T/bench_all.err
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $T/launches_qaoa30.csv \
