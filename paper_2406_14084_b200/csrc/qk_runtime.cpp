@@ -2174,9 +2174,11 @@ int compile_program(qk_sim* s) {
     s->iplan.push_back(std::move(ip));
   }
   if (merge_sqs && !lay_identity(sigma) && !emit_restore()) return fail(QK_ESIM, "internal: swap run merge failed");
-  // lazy mode: the handle keeps the end layout; relabel mode restores it
+  // lazy and relabel modes: the handle keeps the end layout (readbacks map
+  // through it, writers and the next run restore it); QK_RELABEL_RESTORE
+  // restores it with a final permuted pass instead
   s->lay_final = ident;
-  if (lazy) {
+  if (lazy || (relabel && !getenv("QK_RELABEL_RESTORE"))) {
     s->lay_final = sigma;
     for (int q = 0; q < nb; ++q) sigma[q] = q;
   }
