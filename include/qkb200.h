@@ -106,6 +106,11 @@ int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t
  * i.e. nparam = 2^(k+1) doubles). */
 int qk_load_packed(qk_sim* sim, const int32_t* words, size_t nwords,
                    const double* params, size_t nparams);
+/* run_gate_by_gate(raw) — simulator.py:557-569: load the raw circuit (packed
+ * QK_INS_BLOCK records, gates in order) so that qk_run sweeps the whole state
+ * once per gate: no fusion, folding or relabeling. Single rank only (r == 0). */
+int qk_load_gate_by_gate(qk_sim* sim, const int32_t* words, size_t nwords,
+                         const double* params, size_t nparams);
 
 /* Program queries: number of instructions, and the final physical->logical
  * permutation replayed from the swaps (circuit.py:202-210); perm has n ints. */

@@ -44,6 +44,7 @@ _SIGS = {
     "qk_parse_text": (c_int, [ctypes.c_char_p, c_size, c_int, c_int, c_int, P(c_int32), P(c_size),
                               P(c_dbl), P(c_size), P(c_int)]),
     "qk_load_packed": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
+    "qk_load_gate_by_gate": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
     "qk_program_info": (c_int, [c_void, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int32)]),
     "qk_run": (c_int, [c_void, P(c_dbl)]),
     "qk_kernel_stats": (c_int, [c_void, P(c_dbl), c_int]),
@@ -232,6 +233,9 @@ class Handle:
 
     def load_packed(self, words, params, nparams):
         check(lib().qk_load_packed(self.ptr, iptr(words), len(words), dptr(params), nparams))
+
+    def load_gate_by_gate(self, words, params, nparams):
+        check(lib().qk_load_gate_by_gate(self.ptr, iptr(words), len(words), dptr(params), nparams))
 
     def load_text(self, text: str, c: int):
         raw = text.encode()

@@ -1113,6 +1113,7 @@ struct qk_sim {
   int n = 0, r = 0, b = 0, device = 0;
   int rank_lo = 0, count = 1;
   int L = 0, nbits = 0;  // local qubits, address bits held by this handle
+  bool gbg = false;      // loaded by qk_load_gate_by_gate: one full sweep per gate
   double* state = nullptr;      // == bufs[cur]
   double* bufs[2] = {nullptr, nullptr};  // bufs[1]: out-of-place target of fused passes
   int cur = 0;
@@ -1600,7 +1601,7 @@ int compile_program(qk_sim* s) {
   // contiguous and puts >= 5 qubits that stay in the chunk on the lowest
   // address bits, so every warp still writes whole 512-B runs.
   int Cg = 0;
-  bool relabel = s->bufs[1] && !getenv("QK_NO_FUSE") && !getenv("QK_NO_TMA");
+  bool relabel = s->bufs[1] && !s->gbg && !getenv("QK_NO_FUSE") && !getenv("QK_NO_TMA");
   bool all_chunked = true;
   for (auto& ins : s->prog) {
     if (ins.type != QK_INS_BLOCK || ins.gates.empty()) continue;
@@ -1622,7 +1623,7 @@ int compile_program(qk_sim* s) {
   // readback through it and restores the reference layout before writers.
   // It also replaces relabeling when every chunk is <= 10 qubits (the tiles
   // then stay <= 13 bits; QFT30: 0.112 s lazy vs 0.132 s relabeled).
-  const bool lazy_ok = !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") && jit_available() &&
+  const bool lazy_ok = !s->gbg && !getenv("QK_NO_LAZY") && !getenv("QK_NO_TMA") && jit_available() &&
                        nb >= (jenv ? atoi(jenv) : 20) && nb >= 16;
   // (chunks wider than 10 qubits would need tiles over 13 bits: those
   // programs execute their swaps, e.g. QAOA c12 at 33 qubits in place)
@@ -1665,7 +1666,7 @@ int compile_program(qk_sim* s) {
     return true;
   };
   const bool lazy_fold = lazy && !getenv("QK_NO_FOLD");
-  const bool fold_eager = !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
+  const bool fold_eager = !s->gbg && !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   const bool merge_sqs = !relabel && !lazy && !getenv("QK_NO_SQS_MERGE");
   std::vector<int> folded_into(s->prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
   auto remap = [&](const InstrH& ins) {
@@ -2656,6 +2657,7 @@ int qk_load_text(qk_sim* s, const char* text, size_t len, int c, int* n_instr) {
   std::vector<InstrH> prog;
   if (ps.run(text, len, &prog)) return fail(ps.code, "%s", ps.msg.c_str());
   s->prog = std::move(prog);
+  s->gbg = false;
   int rc = compile_program(s);
   if (rc) return rc;
   if (n_instr) *n_instr = (int)s->prog.size();
@@ -2670,6 +2672,31 @@ int qk_load_packed(qk_sim* s, const int32_t* words, size_t nwords, const double*
   std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
   if (rc) return fail(rc, "%s", emsg.c_str());
   s->prog = std::move(prog);
+  s->gbg = false;
+  return compile_program(s);
+}
+
+int qk_load_gate_by_gate(qk_sim* s, const int32_t* words, size_t nwords, const double* params,
+                         size_t nparams) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  if (s->r != 0) return fail(QK_EINVAL, "gate-by-gate baseline runs on a single rank");
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc;
+  std::string emsg;
+  std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
+  if (rc) return fail(rc, "%s", emsg.c_str());
+  std::vector<InstrH> one_each;
+  for (auto& ins : prog) {
+    if (ins.type != QK_INS_BLOCK) return fail(QK_EINVAL, "gate-by-gate program holds gate blocks only");
+    for (auto& g : ins.gates) {
+      InstrH b;
+      b.type = QK_INS_BLOCK;
+      b.gates.push_back(g);
+      one_each.push_back(std::move(b));
+    }
+  }
+  s->prog = std::move(one_each);
+  s->gbg = true;
   return compile_program(s);
 }
 

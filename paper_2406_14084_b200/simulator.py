@@ -404,9 +404,9 @@ class Simulator:
     def run_gate_by_gate(self, raw) -> SimResult:  # simulator.py:557-569
         if self.layout.r != 0:
             raise SimulationError("gate-by-gate baseline runs on a single rank")
-        blocks = tuple(type("GBGBlock", (), {"gates": (g,)})() for g in raw.gates)
-        words, params, npar = _lib.pack(blocks)
-        self._h.load_packed(words, params, npar)
+        block = type("GBGBlock", (), {"gates": tuple(raw.gates)})()
+        words, params, npar = _lib.pack((block,))
+        self._h.load_gate_by_gate(words, params, npar)
         self._program = None
         t0 = time.perf_counter()
         timings, _ = self._h.run()

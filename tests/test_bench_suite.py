@@ -67,8 +67,12 @@ def test_gate_by_gate_baseline_matches_block_mode(gpu):
     sim = Simulator(LayoutParams(n=20, c=c))
     block = sim.run(opt).logical_vector()
     sim.reset()
-    gbg = sim.run_gate_by_gate(qb.raw_from_optimized(opt)).physical_vector()
+    raw = qb.raw_from_optimized(opt)
+    sim.handle.stats(reset=True)
+    gbg = sim.run_gate_by_gate(raw).physical_vector()
     assert np.max(np.abs(block - gbg)) <= 1e-10
+    # the baseline sweeps the state once per gate: nothing fused or folded
+    assert sim.handle.stats()[1] == len(raw.gates)
     sim.close()
 
 
