@@ -1109,11 +1109,18 @@ void shift_pairs(const std::vector<int>& a_bits, const std::vector<int>& b_bits,
 // ---------------------------------------------------------------------------
 // handle
 
+constexpr int kFreshBits = 13;  // widest TMA chunk: qk_reset writes this prefix
+
 struct qk_sim {
   int n = 0, r = 0, b = 0, device = 0;
   int rank_lo = 0, count = 1;
   int L = 0, nbits = 0;  // local qubits, address bits held by this handle
   bool gbg = false;      // loaded by qk_load_gate_by_gate: one full sweep per gate
+  // |0...0> after qk_reset with only the first kFreshAmps amplitudes written:
+  // the first TMA pass of a run reads every other chunk as out-of-bounds zeros
+  // (no HBM reads), anything else writes the whole state first (ensure_full)
+  bool fresh = false;
+  double fresh_saved = 0;  // read bytes skipped this way (kept out of the stats)
   double* state = nullptr;      // == bufs[cur]
   double* bufs[2] = {nullptr, nullptr};  // bufs[1]: out-of-place target of fused passes
   int cur = 0;
@@ -1218,6 +1225,48 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
     s->map_ok[buf][slot] = true;
   }
   return &s->maps[buf][slot];
+}
+
+// A pass's load view of bufs[0] with only addresses < 2^kFreshBits in bounds
+// (every other box is zero-filled by the TMA unit without touching HBM): on a
+// fresh |0...0> those are the only amplitudes qk_reset wrote.
+bool fresh_map(qk_sim* s, const TmaParams& tp, CUtensorMap* out) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int rank;
+  if (tp.lazy) {
+    TileDims td{};
+    if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return false;
+    rank = td.rank;
+    for (int j = 0; j < rank; ++j) {
+      const int keep = std::max(0, std::min(td.len[j], kFreshBits - td.lo[j]));
+      dims[j] = j == 0 ? (cuuint64_t)(2 << td.len[0]) : (cuuint64_t)1 << keep;
+      if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
+      box[j] = (cuuint32_t)td.box[j];
+    }
+  } else {
+    rank = 2;
+    dims[0] = 16;
+    dims[1] = (cuuint64_t)1 << (kFreshBits - 3);
+    strides[0] = 128;
+    box[0] = 16;
+    box[1] = (cuuint32_t)tp.box_rows;
+  }
+  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, s->bufs[0], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            (tp.lazy && tp.rowbits == 2) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Write the whole |0...0> state of a fresh handle (before anything but the
+// first TMA pass reads or writes it).
+int ensure_full(qk_sim* s) {
+  if (!s->fresh) return QK_OK;
+  s->fresh = false;
+  int rc = launch_fill_zero_one(s->bufs[0], s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
+  return rc ? fail(QK_ECUDA, "state fill failed") : QK_OK;
 }
 
 // N-D strided view of `buf` for the tile of a lazy pass (qk_internal.h tile_dims)
@@ -2239,15 +2288,32 @@ int ensure_events(qk_sim* s, size_t n) {
 }
 
 int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
-  if (s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0) {
+  const bool tma_pass = s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0;
+  // a fresh state is read only by a TMA pass (it writes every chunk) through a
+  // view whose in-bounds part is the written prefix
+  CUtensorMap fmap;
+  const bool from_fresh = s->fresh && tma_pass && s->cur == 0 && !getenv("QK_NO_FRESH") &&
+                          fresh_map(s, s->tma[s->pass_tma[p]], &fmap);
+  if (!from_fresh) {
+    if (s->fresh && getenv("QK_DUMP_PLAN"))
+      fprintf(stderr, "fresh state: pass %d (tma %d) fills the whole state first\n", p, (int)tma_pass);
+    int rc = ensure_full(s);
+    if (rc) return rc;
+  }
+  if (tma_pass) {
     TmaParams& tp = s->tma[s->pass_tma[p]];
-    if (!tp.lazy) {
+    if (from_fresh) {
+      if (!tp.lazy) tp.map = fmap;
+      s->fresh = false;
+      s->fresh_saved += 16.0 * (double)(s->amps - (1ull << tp.C));
+    } else if (!tp.lazy) {
       const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
       if (!map) return fail(QK_ECUDA, "tensor map unavailable");
       tp.map = *map;
     }
     // lazy passes carry their own strided views of bufs[0] / bufs[1]
-    const CUtensorMap* lazy_map = tp.lazy ? (s->cur ? &s->lazy_map1[s->pass_tma[p]] : &tp.map) : &tp.map;
+    const CUtensorMap* lazy_map =
+        from_fresh ? &fmap : tp.lazy ? (s->cur ? &s->lazy_map1[s->pass_tma[p]] : &tp.map) : &tp.map;
     const bool flip = tp.permuted && !tp.lazy;
     tp.state = s->bufs[s->cur];
     tp.out = flip ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
@@ -2261,7 +2327,12 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
                                    (CUstream_st*)s->stream)
                     : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream);
     } else {
-      rc = launch_block_tma(&tp, s->num_sms, (CUstream_st*)s->stream);
+      TmaParams tf;
+      if (from_fresh && tp.lazy) {  // the generic kernel reads its view from the params
+        tf = tp;
+        tf.map = fmap;
+      }
+      rc = launch_block_tma(from_fresh && tp.lazy ? &tf : &tp, s->num_sms, (CUstream_st*)s->stream);
     }
     if (rc) return fail(QK_ECUDA, "tma block launch failed: %s", cudaGetErrorString((cudaError_t)rc));
     if (flip) {
@@ -2286,6 +2357,10 @@ bool fused_away(const qk_sim* s, const InstrPlan& ip) {
 
 int run_instr(qk_sim* s, const InstrPlan& ip) {
   if (ip.type != QK_INS_BLOCK && fused_away(s, ip)) return QK_OK;
+  if (ip.type != QK_INS_BLOCK) {
+    int rc = ensure_full(s);
+    if (rc) return rc;
+  }
   if (ip.type == QK_INS_BLOCK) {
     for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
       int rc = launch_pass(s, p);
@@ -2434,7 +2509,11 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
 }
 
 // Bring the state back to the reference layout (two SQS rounds at most).
-int materialize(qk_sim* s) {
+int materialize(qk_sim* s, bool keep_fresh = false) {
+  if (!keep_fresh) {
+    int rc = ensure_full(s);
+    if (rc) return rc;
+  }
   if (s->lay.empty() || lay_identity(s->lay)) return QK_OK;
   std::vector<std::pair<int, int>> rounds[2];
   restore_rounds(s->lay, rounds);
@@ -2631,7 +2710,10 @@ int qk_reset(qk_sim* s) {
   s->cur = 0;
   s->state = s->bufs[0];
   for (int q = 0; q < s->nbits; ++q) s->lay[q] = q;  // |0...0> is the same in every layout
-  int rc = launch_fill_zero_one(s->state, s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
+  // only the first chunk is written; the rest is filled on demand (ensure_full)
+  s->fresh = s->amps >= (2ull << kFreshBits) && !getenv("QK_NO_FRESH");
+  int rc = launch_fill_zero_one(s->state, s->fresh ? (1ull << kFreshBits) : s->amps, s->rank_lo == 0,
+                                (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   return QK_OK;
@@ -2726,16 +2808,20 @@ int qk_set_profiling(qk_sim* s, int per_launch) {
 int qk_run(qk_sim* s, double* timings) {
   if (!s) return fail(QK_EINVAL, "null handle");
   CUDA_TRY(cudaSetDevice(s->device));
-  int rc = materialize(s);  // the plan starts from the reference layout
+  int rc = materialize(s, true);  // the plan starts from the reference layout
   if (rc) return rc;
+  s->fresh_saved = 0;
   const auto t0 = std::chrono::steady_clock::now();
   const size_t ni = s->iplan.size();
   rc = ensure_events(s, 2 * ni + 2);
   if (rc) return rc;
+  size_t first_exec = ni;  // the instruction whose pass read the fresh state
   for (size_t i = 0; i < ni; ++i) {
     CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
+    const bool was_fresh = s->fresh;
     rc = run_instr(s, s->iplan[i]);
     if (rc) return rc;
+    if (was_fresh && !s->fresh && s->fresh_saved > 0) first_exec = i;
     CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
@@ -2755,7 +2841,7 @@ int qk_run(qk_sim* s, double* timings) {
     const int sc = xp ? 3 : c;
     s->stat_ms[sc] += ms;
     if (fused_away(s, ip)) continue;
-    s->stat_bytes[sc] += ip.bytes;
+    s->stat_bytes[sc] += ip.bytes - (i == first_exec ? s->fresh_saved : 0.0);
     s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
   }
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -2789,6 +2875,7 @@ int qk_kernel_stats(qk_sim* s, double* out, int reset) {
 int qk_sumsq(qk_sim* s, double* sumsq) {
   if (!s || !sumsq) return fail(QK_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
   int rc = launch_sumsq(s->state, s->amps, s->d_partial, s->d_scalar, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "norm launch failed");
   CUDA_TRY(cudaMemcpyAsync(sumsq, s->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
@@ -2802,6 +2889,7 @@ int qk_read_physical(qk_sim* s, int part, uint64_t off, uint64_t count, double* 
   if (part < 0 || part >= s->count || off + count > psize || off > psize)
     return fail(QK_EINVAL, "read outside partition");
   CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
   if (count && !lay_identity(s->lay)) {
     // lazy layout: gather through the bit permutation (reference index i -> lay_addr(i))
     std::vector<int> pm(s->nbits);
@@ -2848,6 +2936,7 @@ int qk_gather(qk_sim* s, const uint64_t* idx, uint64_t count, double* reim) {
     if (idx[i] < lo || idx[i] - lo >= s->amps) return fail(QK_EINVAL, "index %llu not held by this handle",
                                                           (unsigned long long)idx[i]);
   CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
   const uint64_t chunk = 1u << 22;
   int rc = ensure_scratch(s, chunk * 24);
   if (rc) return rc;
@@ -2885,6 +2974,7 @@ int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64
   if (s->n < 64 && (start + count > (1ull << s->n) || start > (1ull << s->n)))
     return fail(QK_EINVAL, "logical range out of bounds");
   CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
   const uint64_t chunk = 1u << 22;
   int rc = ensure_scratch(s, chunk * 16);
   if (rc) return rc;
@@ -3152,6 +3242,7 @@ int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set, c
 int qk_ipc_handle(qk_sim* s, void* handle128) {
   if (!s || !handle128) return fail(QK_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
   unsigned char* out = static_cast<unsigned char*>(handle128);
   memset(out, 0, 128);
   for (int b = 0; b < 2; ++b) {

@@ -401,3 +401,55 @@ def test_lazy_layout_readbacks_and_writers(gpu):
         assert np.max(np.abs(np.asarray(lazy[key]) - np.asarray(eager[key]))) <= TOL, key
     assert abs(lazy["norm"] - eager["norm"]) <= 1e-12
     assert np.max(np.abs(np.array(lazy["amp"]) - np.array(eager["amp"]))) <= TOL
+
+
+@pytest.mark.gpu
+def test_fresh_reset_readers_writers_and_first_pass(gpu):
+    """qk_reset writes only the first chunk of |0...0>: the first TMA pass reads
+    every other chunk as out-of-bounds zeros, and any other reader or writer
+    fills the whole state first. Every path must equal a handle that always
+    writes the whole state (QK_NO_FRESH)."""
+    import os
+    from conftest import ROOT
+    from paper_2406_14084_b200 import InMemSwap
+    n = 20
+    text = open(os.path.join(ROOT, "bench_circuits", "qft20_c10_r0.txt")).read()
+    e0 = np.zeros(1 << n, dtype=np.complex128)
+    e0[0] = 1
+
+    def session(env):
+        for k, v in env.items():
+            os.environ[k] = v
+        try:
+            out = {}
+            sim = Simulator(LayoutParams(n=n, c=n))
+            sim.reset()
+            out["read_after_reset"] = sim.partitions[0].amps[:]
+            sim.reset()
+            out["norm_after_reset"] = sim.handle.sumsq()
+            sim.reset()
+            sim.partitions[0].amps[3:7] = np.arange(4) + 1j         # partial writer
+            out["after_write"] = sim.partitions[0].amps[:]
+            perm = sim.load_text(text, 10)
+            sim.reset()
+            out["run"] = sim.run_loaded(perm).physical_vector()
+            # a program that starts with a swap, then gates
+            prog = [InMemSwap((0, 1), (15, 19)),
+                    GateBlock(tuple(Gate(GateKind.H, (q,), q) for q in range(10)))]
+            sim.reset()
+            out["swap_first"] = sim.run(prog).physical_vector()
+            sim.close()
+            return out
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+
+    fresh = session({})
+    full = session({"QK_NO_FRESH": "1"})
+    assert np.array_equal(fresh["read_after_reset"], e0)
+    assert abs(fresh["norm_after_reset"] - 1.0) <= 1e-15
+    want = e0.copy()
+    want[3:7] = np.arange(4) + 1j
+    assert np.array_equal(fresh["after_write"], want)
+    for key in ("read_after_reset", "after_write", "run", "swap_first"):
+        assert np.array_equal(np.asarray(fresh[key]), np.asarray(full[key])), key
