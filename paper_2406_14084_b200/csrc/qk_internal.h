@@ -137,6 +137,7 @@ struct alignas(64) TmaParams {
   int32_t lazy;                 // 1: strided tile (tbit) loaded through `map` (N-D), stored in place
   int32_t rowbits;              // lazy: contiguous row bits of the tile view (3: 128-B, 2: 64-B rows)
   int32_t needs_jit;            // 1: ops the interpreter cannot run (outer-bit table terms)
+  int32_t smax;                 // > 0: at most this many stages (leaves L1 to the diagonal tables)
   uint8_t tbit[16];             // lazy: physical address bit of every chunk-local bit (ascending)
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)
@@ -211,12 +212,13 @@ int launch_block_pass(double* state, const PassDesc* h_pass, const PassDesc* d_p
                       const PhaseDesc* d_phases, const OpDesc* d_ops, const double* d_coef,
                       const double* d_tables, uint64_t first, CUstream_st* stream);
 int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream);
-int tma_smem_bytes(int C, int M, int* ng, int* stages);
+int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax = 0);
 // load-time specialised passes (qk_jit.cpp)
 bool jit_available();
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef);
 void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles);
-int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream);
+int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream,
+               int smax = 0);
 // cluster-exchange pass: 2^xbits CTAs per cluster, nsuper supertiles
 int jit_launch_x(void* kern, const void* params, int C, int M, int xbits, uint64_t nsuper, CUstream_st* stream);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,

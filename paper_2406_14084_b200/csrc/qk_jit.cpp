@@ -319,7 +319,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       if (op.code == OP_DIAG) toff->push_back(op.table);
     }
   int ng = 0, st = 0;
-  if (tma_smem_bytes(C, M, &ng, &st) < 0) return false;
+  if (tma_smem_bytes(C, M, &ng, &st, tp.smax) < 0) return false;
   // registers: 4 per complex entry, 2^M entries per table; one table for
   // 16-amplitude threads, two for 8-amplitude threads
   const char* hz = getenv("QK_JIT_HOIST");
@@ -809,9 +809,10 @@ void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles
 }
 
 // Launch a JIT kernel: params blob = QkJitParams laid out by jit_params().
-int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream) {
+int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream,
+               int smax) {
   int ng = 0, st = 0;
-  const int smem = tma_smem_bytes(C, M, &ng, &st);
+  const int smem = tma_smem_bytes(C, M, &ng, &st, smax);
   if (smem < 0) return -1;
   const int threads = 32 + (1 << (C - M)) * ng;
   const uint64_t grid = nchunks < (uint64_t)num_sms ? nchunks : (uint64_t)num_sms;

@@ -1354,7 +1354,23 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
   tp.nphases = pd.nphases;
   tp.box_rows = box_rows;
   tp.ntma = (1 << (pd.C - 3)) / box_rows;
-  if (tma_smem_bytes(pd.C, pd.M, &tp.ng, &tp.stages) < 0) return false;
+  {
+    // Two or more diagonal tables (64 KiB each at 12 bits) are gathered per
+    // amplitude; with two 64-KiB stages instead of three the L1 keeps them
+    // (QAOA30's 3-table passes: 6.7 -> 5.9 ms; light 1-table passes lose ~0.2 ms).
+    // Three-phase passes with dense 2x2 gates gain too (~0.2 ms each).
+    int ndiag = 0, nmat = 0;
+    for (int ph = 0; ph < pd.nphases; ++ph) {
+      const PhaseDesc& D = hp.phases[pd.phase0 + ph];
+      for (int o = D.op_begin; o < D.op_end; ++o) {
+        ndiag += hp.ops[o].code == OP_DIAG;
+        nmat += hp.ops[o].code == OP_MAT;
+      }
+    }
+    const bool l1_tables = ndiag >= 2 || (pd.nphases >= 3 && nmat >= 5);
+    tp.smax = (pd.C == 12 && l1_tables && !tp.xbits && !getenv("QK_NO_SMAX")) ? 2 : 0;
+  }
+  if (tma_smem_bytes(pd.C, pd.M, &tp.ng, &tp.stages, tp.smax) < 0) return false;
   int ncoef = 0, nsteps = 0;
   for (int ph = 0; ph < pd.nphases; ++ph) {
     const PhaseDesc& D = hp.phases[pd.phase0 + ph];
@@ -2325,7 +2341,8 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       blob[18] = (uint64_t)(uintptr_t)tp.out;
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
-                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream);
+                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream,
+                                 tp.smax);
     } else {
       TmaParams tf;
       if (from_fresh && tp.lazy) {  // the generic kernel reads its view from the params

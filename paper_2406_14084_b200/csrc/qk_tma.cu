@@ -326,7 +326,7 @@ static int consumers_for(int C, int M) {
   return M == 4 ? kConsumers4 : kConsumers3;
 }
 
-int tma_smem_bytes(int C, int M, int* ng, int* stages) {
+int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax) {
   const int consumers = consumers_for(C, M);
   const int GT = 1 << (C - M);
   const int NG = GT >= consumers ? 1 : consumers / GT;
@@ -336,6 +336,8 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages) {
   int S = (int)(kSmemBudget / stage);
   S = (S / NG) * NG;
   if (S > 4 * NG) S = 4 * NG;
+  if (const char* e = getenv("QK_SMAX")) smax = atoi(e);
+  if (smax > 0) S = std::max(std::min(S, smax), NG);
   if (ng) *ng = NG;
   if (stages) *stages = S;
   if (S < 1 || (S < 2 && C != 13) || S < NG) return -1;  // C = 13: one 128-KiB stage
@@ -351,7 +353,7 @@ int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream) {
     attr = true;
   }
   int ng = 0, st = 0;
-  const int smem = tma_smem_bytes(p->C, p->M, &ng, &st);
+  const int smem = tma_smem_bytes(p->C, p->M, &ng, &st, p->smax);
   if (smem < 0) return -1;
   const uint64_t grid = p->nchunks < (uint64_t)num_sms ? p->nchunks : (uint64_t)num_sms;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
