@@ -1368,7 +1368,12 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
       }
     }
     const bool l1_tables = ndiag >= 2 || (pd.nphases >= 3 && nmat >= 5);
-    tp.smax = (pd.C == 12 && l1_tables && !tp.xbits && !getenv("QK_NO_SMAX")) ? 2 : 0;
+    // Narrower chunks with any table keep 128 KiB of stages (QFT30: 38.0 ->
+    // 34.9 ms with 8 instead of 12 16-KiB stages; 4 stages starve the loads).
+    if (!tp.xbits && !getenv("QK_NO_SMAX")) {
+      if (pd.C == 12 && l1_tables) tp.smax = 2;
+      else if (pd.C <= 11 && ndiag >= 1) tp.smax = (128 << 10) / (16 << pd.C);
+    }
   }
   if (tma_smem_bytes(pd.C, pd.M, &tp.ng, &tp.stages, tp.smax) < 0) return false;
   int ncoef = 0, nsteps = 0;
