@@ -629,7 +629,14 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     // strided tile (qk_internal.h tile_dims): one N-D box per value of the
     // iterated top tile bits; coordinates from the chunk's outer bits
     o << lazy_loads(tp, "chunk", "dst", false, "        ");
-    if (pfe ? atoi(pfe) != 0 : st <= 2) {
+    // L2 prefetch of the refill only while the tile spans few 2-MiB pages:
+    // with rows on up to 1024 pages the extra translations cost more than the
+    // prefetch hides (H33's 1024-page pass: 88 -> 65 ms without it; U33's
+    // 8-page 13-bit pass: 64 ms with it, 68 ms without). 64-B-row tiles
+    // never gain (H33's 8-page one: 50 ms without, 62 ms with).
+    int pagebits = 0;
+    for (int x = 0; x < C; ++x) pagebits += tp.tbit[x] >= 17;
+    if (pfe ? atoi(pfe) != 0 : (st <= 2 && pagebits <= 4 && tp.rowbits == 3)) {
       o << "        if (chunk + " << st << "ull * G < p.nchunks) {\n"
         << "          const u64 nchunk = chunk + " << st << "ull * G;\n"
         << lazy_loads(tp, "nchunk", nullptr, true, "          ") << "        }\n";
