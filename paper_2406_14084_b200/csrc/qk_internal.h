@@ -46,6 +46,8 @@ struct OpDesc {
   int32_t nco;            // OP_DIAG over address bits outside the chunk (folded diagonal blocks):
   uint8_t co_k[8];        //   chunk-index bit co_k[i] -> table index contribution co_v[i]
   uint16_t co_v[8];
+  uint16_t unit;          // OP_DIAG: register amplitudes j whose entry is exactly 1 for every
+                          //   thread and chunk (e.g. CP with a register control at 0)
 };
 
 struct PhaseDesc {
@@ -115,6 +117,7 @@ struct TOp {
   int8_t nco;             // OpDesc::nco / co_k / co_v (specialised kernels only)
   uint8_t co_k[8];
   uint16_t co_v[8];
+  uint16_t unit;          // OpDesc::unit (specialised kernels skip those multiplies)
 };
 
 struct TPhase {

@@ -428,16 +428,23 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           for (int k = 0; k < op.nco; ++k)  // folded diagonal gates on bits outside the chunk
             dst << " | ((u32)((chunk >> " << (int)op.co_k[k] << ") & 1ull) * " << op.co_v[k] << "u)";
           dst << ";\n";
+          // entries that are exactly 1 for every thread and chunk (op.unit) are skipped
+          auto live = [&](int j) { return !((op.unit >> j) & 1); };
           if (hz) {
-            for (int j = 0; j < NA; ++j) pro << "    tv" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
+            for (int j = 0; j < NA; ++j)
+              if (live(j)) pro << "    tv" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
             pro << "  }\n";
-            for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], tv" << ti << "[" << j << "]);\n";
+            for (int j = 0; j < NA; ++j)
+              if (live(j)) b << "    v[" << j << "] = cm(v[" << j << "], tv" << ti << "[" << j << "]);\n";
           } else if (ez) {
-            for (int j = 0; j < NA; ++j) ear << "      te" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
+            for (int j = 0; j < NA; ++j)
+              if (live(j)) ear << "      te" << ti << "[" << j << "] = __ldg(tb + (pt | " << op.pr[j] << "u));\n";
             ear << "    }\n";
-            for (int j = 0; j < NA; ++j) b << "    v[" << j << "] = cm(v[" << j << "], te" << ti << "[" << j << "]);\n";
+            for (int j = 0; j < NA; ++j)
+              if (live(j)) b << "    v[" << j << "] = cm(v[" << j << "], te" << ti << "[" << j << "]);\n";
           } else {
-            for (int j = 0; j < NA; ++j) b << "      v[" << j << "] = cm(v[" << j << "], __ldg(tb + (pt | " << op.pr[j] << "u)));\n";
+            for (int j = 0; j < NA; ++j)
+              if (live(j)) b << "      v[" << j << "] = cm(v[" << j << "], __ldg(tb + (pt | " << op.pr[j] << "u)));\n";
             b << "    }\n";
           }
           break;

@@ -761,6 +761,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
   std::vector<int64_t> run_table(runs.size(), -1);
   std::vector<std::vector<int>> run_bidx(runs.size());
   std::vector<std::vector<int>> run_obidx(runs.size());  // physical outer bit -> table bit
+  std::vector<char> run_scaled(runs.size(), 0);           // the pass scale is folded into it
   auto build_table = [&](int r, const std::vector<int>& order) -> int {
     const uint32_t S = run_support[r];
     std::vector<int> bidx(C, -1);
@@ -783,6 +784,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
       td.scale = scale.real();
       td.scale_im = scale.imag();
       scale_folded = true;
+      run_scaled[r] = 1;
     }
     for (const GateH* g : runs[r]) {
       TableGate tg{};
@@ -889,6 +891,36 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
             op.co_v[op.nco] = (uint16_t)(1u << run_obidx[it.run][O[k]]);
             ++op.nco;
           }
+        // register amplitudes whose table entry is exactly 1 whatever the
+        // thread and chunk bits: every gate of the run has entry 1 for every
+        // completion of its targets outside the register slots (a CP whose
+        // register-slot target is 0). The specialised kernel skips them.
+        if (!run_scaled[it.run] && !getenv("QK_NO_UNIT_SKIP")) {
+          for (int j = 0; j < (1 << M); ++j) {
+            bool one = true;
+            for (const GateH* g : runs[it.run]) {
+              const int nt = (int)g->t.size();
+              if (nt > 8) {
+                one = false;
+                break;
+              }
+              uint32_t fixed_mask = 0, fixed_val = 0;
+              for (int i = 0; i < nt; ++i) {
+                const int lp = loc[g->t[i]];
+                const int sl = lp >= 0 ? slot(lp) : -1;
+                if (sl >= 0) {
+                  fixed_mask |= 1u << (nt - 1 - i);
+                  if (j >> sl & 1) fixed_val |= 1u << (nt - 1 - i);
+                }
+              }
+              const std::vector<cplx> e = diag_entries(*g);
+              for (uint32_t idx = 0; idx < (1u << nt) && one; ++idx)
+                if ((idx & fixed_mask) == fixed_val && !(idx < e.size() && e[idx] == cplx(1.0, 0.0))) one = false;
+              if (!one) break;
+            }
+            if (one) op.unit |= (uint16_t)(1u << j);
+          }
+        }
       } else {
         const GateH* g = it.g;
         switch (g->kind) {
@@ -1408,6 +1440,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
           for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
           for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
           t.nco = (int8_t)op.nco;
+          t.unit = op.unit;
           for (int k = 0; k < op.nco; ++k) {
             t.co_k[k] = op.co_k[k];
             t.co_v[k] = op.co_v[k];
