@@ -582,6 +582,14 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     std::vector<int> items;
   };
   std::vector<PhaseB> phs;
+  // Positions that fill a phase's free register slots: the highest chunk
+  // positions, or for a fused (permuted) store the positions with the highest
+  // destinations, so the last phase keeps the store lanes (the lowest
+  // destinations) off its registers and needs no extra layout-only phase.
+  std::vector<int> fill_order;
+  for (int q = C - 1; q >= 0; --q) fill_order.push_back(q);
+  if (dest && !getenv("QK_FILL_HIGH"))
+    std::stable_sort(fill_order.begin(), fill_order.end(), [&](int x, int y) { return (*dest)[Q[x]] > (*dest)[Q[y]]; });
   // Dependency-aware list scheduling: gates that commute (disjoint qubits,
   // diagonal runs, a diagonal on a CX control, CX sharing only a target or
   // only a control) may run in any order. Each phase picks the register set
@@ -677,8 +685,8 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
       int best_c = -1, best_n = -1;
       for (size_t c = 0; c < cands.size(); ++c) {
         auto& R = cands[c];
-        for (int q = C - 1; q >= 0 && (int)R.size() < M; --q)  // fill with high positions
-          if (!in_r(R, q)) R.push_back(q);
+        for (int q : fill_order)
+          if ((int)R.size() < M && !in_r(R, q)) R.push_back(q);
         std::vector<char> dn = done;
         const int k = runs_with(R, dn, nullptr);
         if (k > best_n) {
@@ -714,8 +722,8 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
         for (int q : needs(items[j]))
           if ((int)pb.R.size() < M && std::find(pb.R.begin(), pb.R.end(), q) == pb.R.end())
             pb.R.push_back(q);
-      for (int q = C - 1; q >= 0 && (int)pb.R.size() < M; --q)  // fill with high positions
-        if (std::find(pb.R.begin(), pb.R.end(), q) == pb.R.end()) pb.R.push_back(q);
+      for (int q : fill_order)
+        if ((int)pb.R.size() < M && std::find(pb.R.begin(), pb.R.end(), q) == pb.R.end()) pb.R.push_back(q);
       phs.push_back(pb);
     }
     phs.back().items.push_back((int)i);
