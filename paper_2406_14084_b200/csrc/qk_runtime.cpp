@@ -590,6 +590,10 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
   for (int q = C - 1; q >= 0; --q) fill_order.push_back(q);
   if (dest && !getenv("QK_FILL_HIGH"))
     std::stable_sort(fill_order.begin(), fill_order.end(), [&](int x, int y) { return (*dest)[Q[x]] > (*dest)[Q[y]]; });
+  // the store lanes of a fused pass: positions landing on destination bits 0..lanes_req-1
+  std::vector<char> lane_pos(C, 0);
+  if (dest)
+    for (int i = 0; i < lanes_req && i < C; ++i) lane_pos[fill_order[C - 1 - i]] = 1;
   // Dependency-aware list scheduling: gates that commute (disjoint qubits,
   // diagonal runs, a diagonal on a CX control, CX sharing only a target or
   // only a control) may run in any order. Each phase picks the register set
@@ -728,7 +732,38 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     }
     phs.back().items.push_back((int)i);
   }
-  if (!sched.empty() && sched.size() < phs.size()) phs.swap(sched);
+  auto extra = [&](const std::vector<PhaseB>& v) {
+    if (!dest || v.empty()) return 0;
+    for (int q : v.back().R)
+      if (lane_pos[q]) return 1;
+    return 0;
+  };
+  if (!sched.empty() && sched.size() + extra(sched) < phs.size() + extra(phs)) phs.swap(sched);
+  if (getenv("QK_DUMP_PHASES")) {
+    fprintf(stderr, "pass C=%d dest=%d lanes:", C, dest ? 1 : 0);
+    for (int q = 0; q < C; ++q)
+      if (lane_pos[q]) fprintf(stderr, " %d", q);
+    fprintf(stderr, "\n");
+    for (auto& pb : phs) {
+      fprintf(stderr, "  R={");
+      for (int q : pb.R) fprintf(stderr, "%d%s ", q, lane_pos[q] ? "*" : "");
+      fprintf(stderr, "} items:");
+      for (int ii : pb.items) {
+        const Item& it = items[ii];
+        if (it.type == 1) {
+          fprintf(stderr, " D[");
+          for (int q = 0; q < C; ++q)
+            if (run_support[it.run] >> q & 1) fprintf(stderr, "%d,", q);
+          fprintf(stderr, "]");
+        } else {
+          fprintf(stderr, " g%d(", (int)it.g->kind);
+          for (int t : it.g->t) fprintf(stderr, "%d,", loc[t]);
+          fprintf(stderr, ")");
+        }
+      }
+      fprintf(stderr, "\n");
+    }
+  }
   if (phs.empty() && !dest) return QK_OK;  // no gates at all: nothing to do
   if (dest) {
     // fused (permuted) store: the 5 positions landing on destination bits
