@@ -227,6 +227,8 @@ int jit_launch_x(void* kern, const void* params, int C, int M, int xbits, uint64
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,
                         const double* d_entries, double* d_pool, CUstream_st* stream);
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* d, CUstream_st* stream);
+// out of place into the second buffer (relabeled programs)
+int launch_sqs_oop(const double* src, double* dst, const SqsDesc* h, CUstream_st* stream);
 int launch_sqs_bulk(double* state, const SqsDesc* h, int num_sms, CUstream_st* stream);
 int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p, const int* q,
                      int np, const int* a, const int* b, int k, CUstream_st* stream);

@@ -480,6 +480,82 @@ __global__ void __launch_bounds__(256) k_sqs_async(double2* __restrict__ state, 
   }
 }
 
+// Out-of-place variant (second buffer): every destination tile X takes the
+// permuted source tile Y = X ^ swap once, so there are no pairs, no skipped
+// units and the reads and writes go to different buffers.
+__global__ void __launch_bounds__(256) k_sqs_oop(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                 const __grid_constant__ SqsDesc S) {
+  extern __shared__ double2 sm[];
+  const int nv = S.nv, w = S.w;
+  const uint32_t tile = 1u << nv;
+  const uint64_t nunits = 1ull << S.nouter;
+  const int lane = threadIdx.x & 31;
+  const uint32_t e0 = threadIdx.x;
+  const int per = tile > 256 ? (int)(tile >> 8) : 1;
+  const bool active = e0 < tile;
+  const uint32_t wmask = (1u << w) - 1;
+  uint64_t off[4];
+  uint32_t pe[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const uint32_t e = e0 + 256u * m;
+    uint64_t o = e & wmask;
+    for (int b = w; b < nv; ++b) o |= (uint64_t)((e >> b) & 1u) << S.vpos[b];
+    off[m] = o;
+    uint32_t q = e;
+    for (int k = 0; k < S.nvp; ++k) {
+      const uint32_t d = ((q >> S.va[k]) ^ (q >> S.vb[k])) & 1u;
+      q ^= (d << S.va[k]) | (d << S.vb[k]);
+    }
+    pe[m] = swz(q);
+  }
+  for (uint64_t X = blockIdx.x; X < nunits; X += gridDim.x) {
+    uint64_t c = 0;
+    if (lane < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane]) ^ (X >> S.ob[lane])) & 1ull;
+      c = (d << S.oa[lane]) | (d << S.ob[lane]);
+    }
+    if (lane + 32 < S.nop) {
+      const uint64_t d = ((X >> S.oa[lane + 32]) ^ (X >> S.ob[lane + 32])) & 1ull;
+      c |= (d << S.oa[lane + 32]) | (d << S.ob[lane + 32]);
+    }
+    const uint64_t Y = X ^ warp_or64(c);
+    uint64_t cx = 0, cy = 0;
+    if (lane < S.nouter) {
+      cx = ((X >> lane) & 1ull) << S.opos[lane];
+      cy = ((Y >> lane) & 1ull) << S.opos[lane];
+    }
+    if (lane + 32 < S.nouter) {
+      cx |= ((X >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+      cy |= ((Y >> (lane + 32)) & 1ull) << S.opos[lane + 32];
+    }
+    const uint64_t bx = warp_or64(cx), by = warp_or64(cy);
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (m < per && active) cp_async16(sm + swz(e0 + 256u * m), src + by + off[m]);
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (m < per && active) st_g(dst + bx + off[m], sm[pe[m]]);
+    __syncthreads();
+  }
+}
+
+int launch_sqs_oop(const double* src, double* dst, const SqsDesc* h, CUstream_st* stream) {
+  const uint64_t units = 1ull << h->nouter;
+  const size_t smem = (size_t)16u << h->nv;
+  // many more CTAs than fit (8 per SM): the block scheduler balances the
+  // tail better than a persistent grid (QAOA30 SQS: 60.1 ms in place,
+  // 59.0 ms here at 12 per SM, 54.9 ms at 64 per SM, 67 ms with one unit each)
+  static const int per_sm = getenv("QK_SQS_OOP_CTAS") ? atoi(getenv("QK_SQS_OOP_CTAS")) : 64;
+  uint64_t grid = 148ull * per_sm;
+  if (grid > units) grid = units;
+  k_sqs_oop<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const double2*>(src), reinterpret_cast<double2*>(dst), *h);
+  return (int)cudaGetLastError();
+}
+
 int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* /*d*/, CUstream_st* stream) {
   if (!getenv("QK_SQS_REG")) {
     const uint64_t units = 1ull << h->nouter;
@@ -489,7 +565,9 @@ int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* /*d*/, CUstream_s
       cudaFuncSetAttribute(k_sqs_async, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (16 << 10));
       attr2 = true;
     }
-    uint64_t grid = 148ull * 7;
+    // oversubscribed like k_sqs_oop (7 fit per SM): QAOA33r3's SQS 2.48 -> 2.32 s
+    static const int per_sm = getenv("QK_SQS_CTAS") ? atoi(getenv("QK_SQS_CTAS")) : 64;
+    uint64_t grid = 148ull * per_sm;
     if (grid > units) grid = units;
     k_sqs_async<<<(unsigned)grid, 256, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
         reinterpret_cast<double2*>(state), *h);

@@ -1194,6 +1194,7 @@ struct qk_sim {
   // |0...0> after qk_reset with only the first kFreshAmps amplitudes written:
   // the first TMA pass of a run reads every other chunk as out-of-bounds zeros
   // (no HBM reads), anything else writes the whole state first (ensure_full)
+  bool oop_sqs = false;  // relabeled program: unfused SQS permute into the second buffer
   bool fresh = false;
   double fresh_saved = 0;  // read bytes skipped this way (kept out of the stats)
   double* state = nullptr;      // == bufs[cur]
@@ -2324,6 +2325,7 @@ int compile_program(qk_sim* s) {
   // lazy and relabel modes: the handle keeps the end layout (readbacks map
   // through it, writers and the next run restore it); QK_RELABEL_RESTORE
   // restores it with a final permuted pass instead
+  s->oop_sqs = relabel;
   s->lay_final = ident;
   if (lazy || (relabel && !getenv("QK_RELABEL_RESTORE"))) {
     s->lay_final = sigma;
@@ -2470,6 +2472,14 @@ int run_instr(qk_sim* s, const InstrPlan& ip) {
     int rc = -2;
     if (getenv("QK_SQS_BULK") && s->nbits >= 16)  // bulk-copy variant: 512-B copies are TMA-op bound
       rc = launch_sqs_bulk(s->state, &s->hp.sqs[ip.sqs], s->num_sms, (CUstream_st*)s->stream);
+    if (rc == -2 && s->bufs[1] && s->oop_sqs && !getenv("QK_SQS_INPLACE")) {
+      // relabeled programs own a second buffer: permute into it and flip
+      rc = launch_sqs_oop(s->state, s->bufs[s->cur ^ 1], &s->hp.sqs[ip.sqs], (CUstream_st*)s->stream);
+      if (!rc) {
+        s->cur ^= 1;
+        s->state = s->bufs[s->cur];
+      }
+    }
     if (rc == -2) rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "sqs launch failed: %s", cudaGetErrorString((cudaError_t)rc));
     return QK_OK;
