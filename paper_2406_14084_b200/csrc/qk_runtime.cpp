@@ -1985,12 +1985,42 @@ int compile_program(qk_sim* s) {
             if (compile_pass(tmp, own, T, nb, 0, em, &dp, inT[2] ? 3 : 2) || tmp.passes.empty()) return 99;
             return tmp.passes.back().nphases;
           };
+          // The picks take the free row bits; the other wanted qubits then
+          // take the lowest remaining tile positions in order, so the next
+          // tile has fewer strided runs and pages (QK_NO_PACK: rows only).
+          const bool pack = !getenv("QK_NO_PACK");
           auto make = [&](const std::vector<int>& pick) {
             std::vector<int> dp = ident;
-            for (size_t k = 0; k < pick.size() && k < low.size(); ++k) {
-              dp[low[k]] = pick[k];
-              dp[pick[k]] = low[k];
+            std::vector<char> used(nb, 0), taken(nb, 0);
+            size_t k = 0;
+            for (int r : low)
+              if (k < pick.size()) {
+                dp[pick[k]] = r;
+                used[pick[k]] = taken[r] = 1;
+                ++k;
+              }
+            std::vector<int> slots, srcs;
+            for (int x : T)
+              if (!taken[x] && !(x < 3 && !std::count(low.begin(), low.end(), x))) slots.push_back(x);
+            for (int x : T)
+              if (x < 3 && !std::count(low.begin(), low.end(), x)) used[x] = 1;  // needed row bits stay
+            if (pack)
+              for (int x : want)
+                if (!used[x]) {
+                  srcs.push_back(x);
+                  used[x] = 1;
+                }
+            for (int x : T)
+              if (!used[x]) srcs.push_back(x);
+            if (srcs.size() != slots.size()) {  // should not happen: rows only
+              dp = ident;
+              for (size_t j = 0; j < pick.size() && j < low.size(); ++j) {
+                dp[low[j]] = pick[j];
+                dp[pick[j]] = low[j];
+              }
+              return dp;
             }
+            for (size_t j = 0; j < srcs.size(); ++j) dp[srcs[j]] = slots[j];
             return dp;
           };
           std::vector<std::vector<int>> cands;
@@ -2014,10 +2044,12 @@ int compile_program(qk_sim* s) {
         }
         // fold the diagonal-only blocks up to the next other block: their
         // qubits sit (after the lazy swaps in between) at sig3[t], i.e. at
-        // dphys[sig3[t]] before this pass's store permutation
+        // dinv[sig3[t]] before this pass's store permutation dphys
         std::vector<GateH> folded;
         std::vector<size_t> folded_at;
         if (lazy_fold) {
+          std::vector<int> dinv(nb);
+          for (int q = 0; q < nb; ++q) dinv[dphys[q]] = q;
           std::vector<int> sig3(nb);
           for (int q = 0; q < nb; ++q) sig3[q] = dphys[sigma[q]];
           for (size_t j = ii + 1; j < s->prog.size(); ++j) {
@@ -2027,7 +2059,7 @@ int compile_program(qk_sim* s) {
               if (!diag_block(nx)) break;
               for (auto& g : nx.gates) {
                 GateH m = g;
-                for (int& t : m.t) t = dphys[sig3[t]];
+                for (int& t : m.t) t = dinv[sig3[t]];
                 folded.push_back(m);
               }
               folded_at.push_back(j);
