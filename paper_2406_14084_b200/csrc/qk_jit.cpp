@@ -303,6 +303,58 @@ std::string lazy_loads(const TmaParams& tp, const char* cv, const char* dst, boo
 
 }  // namespace
 
+// Shared-memory slices of per-chunk diagonal tables (12-bit passes with the
+// table-aware chunk order). A table's chunk bits (co_v) are its top index
+// bits, so the entries one chunk reads are one contiguous slice of
+// 2^(inner bits). With the chunk order a CTA keeps the same slices over long
+// stretches; staged in shared memory they stop being L2 gathers.
+// Returns the slice size (entries) per table slot (0 = not staged).
+std::vector<int> slice_plan(const TmaParams& tp, int st) {
+  std::vector<int> out;
+  // Measured: in-place QAOA33 (21 chunk bits, ~14k chunks per CTA) 1.69 ->
+  // 1.63 s; QAOA30 (18 chunk bits) loses 0.165 -> 0.174 s, so only large states
+  const bool on = tp.C >= 12 && !tp.xbits && tp.nbits - tp.C >= 20 && !getenv("QK_NO_SLICES") &&
+                  !getenv("QK_NO_CORDER");
+  long budget = (long)(218 << 10) - (long)st * (16L << tp.C);
+  // a reload happens whenever the staged tables' chunk bits change: keep at
+  // least 2^6 consecutive chunks per slice set (the low counter bits)
+  const int nouter = tp.nbits - tp.C;
+  const char* mr = getenv("QK_SLICE_RUN");
+  const int min_run = mr ? atoi(mr) : 6;
+  uint64_t cmask = 0;
+  for (int ph = 0; ph < tp.nphases; ++ph)
+    for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) {
+      const TOp& op = tp.ops[o];
+      if (op.code != OP_DIAG) continue;
+      uint32_t inner = 0;
+      for (int k = 0; k < 12; ++k) inner |= op.tcontrib[k];
+      for (int j = 0; j < 16; ++j) inner |= op.pr[j];
+      int ents = 1;
+      while ((uint32_t)ents <= inner) ents <<= 1;
+      bool outer_top = true;
+      for (int k = 0; k < op.nco; ++k) outer_top = outer_top && op.co_v[k] >= (uint32_t)ents;
+      uint64_t m2 = cmask;
+      for (int k = 0; k < op.nco; ++k) m2 |= 1ull << op.co_k[k];
+      if (on && op.nco > 0 && outer_top && (long)ents * 16 <= budget &&
+          nouter - __builtin_popcountll(m2) >= min_run) {
+        out.push_back(ents);
+        budget -= (long)ents * 16;
+        cmask = m2;
+      } else {
+        out.push_back(0);
+      }
+    }
+  return out;
+}
+
+int jit_slice_bytes(const TmaParams& tp) {
+  int ng = 0, st = 0;
+  if (tma_smem_bytes(tp.C, tp.M, &ng, &st, tp.smax) < 0) return 0;
+  int b = 0;
+  for (int e : slice_plan(tp, st)) b += e * 16;
+  return b;
+}
+
 // Emit the source of one pass. Returns false when the structure is outside
 // what the generator covers (the caller keeps the interpreter).
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
@@ -343,6 +395,25 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           if (h) --left;
           if (e) --eleft;
         }
+  }
+  // shared-memory slices (one consumer group only: the reload is a group barrier)
+  std::vector<int> slices = ng == 1 ? slice_plan(tp, st) : std::vector<int>();
+  slices.resize(hoisted.size(), 0);
+  std::vector<int> slice_off(slices.size(), 0);
+  uint64_t smask = 0;
+  {
+    int off = 0, t = 0;
+    for (int ph = 0; ph < tp.nphases; ++ph)
+      for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) {
+        const TOp& op = tp.ops[o];
+        if (op.code != OP_DIAG) continue;
+        if (hoisted[t] || early[t]) slices[t] = 0;
+        slice_off[t] = off;
+        off += slices[t];
+        if (slices[t])
+          for (int k = 0; k < op.nco; ++k) smask |= 1ull << op.co_k[k];
+        ++t;
+      }
   }
   std::ostringstream ear;  // per-iteration early table loads
   for (size_t t = 0; t < hoisted.size(); ++t)
@@ -418,6 +489,18 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           // once before the chunk loop and stay in registers.
           const int ti = tab_i++;
           const bool hz = hoisted[ti], ez = early[ti];
+          if (slices[ti] > 0) {
+            // this chunk's slice sits in shared memory (reloaded when the chunk's table bits change)
+            b << "    { const double2* tb = sl + " << slice_off[ti] << ";\n";
+            b << "      const u32 pt = 0u";
+            for (int k = 0; k < T; ++k)
+              if (op.tcontrib[k]) b << " | (((tid >> " << k << ") & 1u) * " << op.tcontrib[k] << "u)";
+            b << ";\n";
+            for (int j = 0; j < NA; ++j)
+              if (!((op.unit >> j) & 1)) b << "      v[" << j << "] = cm(v[" << j << "], tb[pt | " << op.pr[j] << "u]);\n";
+            b << "    }\n";
+            break;
+          }
           std::ostringstream& dst = hz ? pro : (ez ? ear : b);
           const std::string ind = hz ? "  " : "    ";
           if (ez) ear << "    double2 te" << ti << "[" << NA << "];\n";
@@ -707,13 +790,36 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "  const int g = ct >> " << T << ";\n"
     << "  const u32 tid = ct & " << (GT - 1) << "u;\n"
     << pro.str()
-    << "  const int bar_id = 1 + g;\n"
-    << "  for (u64 i = g;; i += " << ng << ") {\n"
+    << "  const int bar_id = 1 + g;\n";
+  if (smask) {
+    o << "  double2* sl = (double2*)(base + " << (size_t)st * (16u << C) + 16 * st << "ull);\n"
+      << "  u64 skey = ~0ull;\n";
+  }
+  o << "  for (u64 i = g;; i += " << ng << ") {\n"
     << "    if (!" << chunk_ok("i") << ") break;\n"
     << "    const u64 chunk = " << chunk_of("i") << ";\n"
     << "    const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
-    << "    double2* sm = (double2*)(base + (size_t)s * stage_bytes);\n"
-    << ear.str()
+    << "    double2* sm = (double2*)(base + (size_t)s * stage_bytes);\n";
+  if (smask) {
+    // every thread passed the previous chunk's last barrier after its table reads
+    o << "    if ((chunk & " << smask << "ull) != skey) {\n";
+    int t = 0;
+    for (int ph = 0; ph < tp.nphases; ++ph)
+      for (int o2 = tp.ph[ph].op_begin; o2 < tp.ph[ph].op_end; ++o2) {
+        const TOp& op = tp.ops[o2];
+        if (op.code != OP_DIAG) continue;
+        if (slices[t] > 0) {
+          o << "      { const double2* src = p.tabs + p.toff[" << t << "] + (0ull";
+          for (int k = 0; k < op.nco; ++k)
+            o << " | ((u64)((chunk >> " << (int)op.co_k[k] << ") & 1ull) * " << op.co_v[k] << "ull)";
+          o << ");\n        for (u32 e = tid; e < " << slices[t] << "u; e += " << GT << "u) sl[" << slice_off[t]
+            << " + e] = __ldg(src + e); }\n";
+        }
+        ++t;
+      }
+    o << "      skey = chunk & " << smask << "ull;\n      gbar(bar_id, " << GT << ");\n    }\n";
+  }
+  o << ear.str()
     << "    mbar_wait(full + s, round & 1u);\n"
     << b.str()
     << "  }\n}\n";
@@ -864,9 +970,11 @@ void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles
 
 // Launch a JIT kernel: params blob = QkJitParams laid out by jit_params().
 int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream,
-               int smax) {
+               int smax, int extra_smem) {
   int ng = 0, st = 0;
-  const int smem = tma_smem_bytes(C, M, &ng, &st, smax);
+  const int smem0 = tma_smem_bytes(C, M, &ng, &st, smax);
+  if (smem0 < 0) return -1;
+  const int smem = smem0 + extra_smem;
   if (smem < 0) return -1;
   const int threads = 32 + (1 << (C - M)) * ng;
   const uint64_t grid = nchunks < (uint64_t)num_sms ? nchunks : (uint64_t)num_sms;

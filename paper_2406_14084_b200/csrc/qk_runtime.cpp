@@ -2517,7 +2517,7 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
                     : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream,
-                                 tp.smax);
+                                 tp.smax, jit_slice_bytes(tp));
     } else {
       TmaParams tf;
       if (from_fresh && tp.lazy) {  // the generic kernel reads its view from the params

@@ -453,3 +453,39 @@ def test_fresh_reset_readers_writers_and_first_pass(gpu):
     assert np.array_equal(fresh["after_write"], want)
     for key in ("read_after_reset", "after_write", "run", "swap_first"):
         assert np.array_equal(np.asarray(fresh[key]), np.asarray(full[key])), key
+
+
+@pytest.mark.gpu
+def test_wide_chunk_lazy_layout_at_33_qubits(gpu):
+    """QAOA33 c12 with 8 rank partitions in one 128-GiB handle: the lazy layout
+    with fix-up swaps, the table-aware chunk order and the shared-memory table
+    slices (states of >= 2^32 amplitudes only) against the eager mode that
+    executes every swap (sampled physical amplitudes and the norm)."""
+    import gc
+    import os
+    from conftest import ROOT
+    text = open(os.path.join(ROOT, "bench_circuits", "qaoa33_c12_r3.txt")).read()
+    n, r = 33, 3
+    idx = np.random.default_rng(11).integers(0, 1 << n, size=1 << 16, dtype=np.uint64)
+
+    def session(env):
+        for k, v in env.items():
+            os.environ[k] = v
+        try:
+            sim = Simulator(LayoutParams(n=n, c=n - r, r=r))
+            perm = sim.load_text(text, 12)
+            sim.reset()
+            res = sim.run_loaded(perm)
+            out = (sim.handle.gather(idx), res.norm())
+            sim.close()
+            del res, sim
+            gc.collect()
+            return out
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+
+    lazy = session({})
+    eager = session({"QK_NO_LAZY12": "1"})
+    assert np.max(np.abs(lazy[0] - eager[0])) <= TOL
+    assert abs(lazy[1] - eager[1]) <= 1e-12
