@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/qkb200.h"
@@ -1515,6 +1517,55 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
   return true;
 }
 
+// jit_source is a pure function of the pass structure: reloading a program
+// (or a program sharing pass structures) reuses the generated source instead
+// of rebuilding ~100 KB of text per pass (3.8 ms for QAOA30's 24 passes).
+// Key: the TmaParams bytes without the tensor map and device pointers.
+bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
+                       std::vector<double>* coef) {
+  struct Val {
+    bool ok;
+    std::string src;
+    std::vector<long long> toff;
+    std::vector<double> coef;
+  };
+  static std::mutex mu;
+  static std::unordered_map<std::string, Val> cache;
+  TmaParams k = tp;
+  memset(&k.map, 0, sizeof k.map);
+  k.tabs = nullptr;
+  k.state = nullptr;
+  k.out = nullptr;
+  std::string key(reinterpret_cast<const char*>(&k), sizeof k);
+  // environment switches the generator (and tma_smem_bytes) reads
+  for (const char* e : {"QK_JIT_PREFETCH", "QK_JIT_HOIST", "QK_JIT_EARLY", "QK_JIT_SW128", "QK_NO_CORDER",
+                        "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS"}) {
+    const char* v = getenv(e);
+    key.push_back('|');
+    if (v) key.append(v);
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end() && !getenv("QK_JIT_NOCACHE")) {
+      *src = it->second.src;
+      *toff = it->second.toff;
+      *coef = it->second.coef;
+      return it->second.ok;
+    }
+  }
+  Val v;
+  v.ok = jit_source(tp, &v.src, &v.toff, &v.coef);
+  const bool ok = v.ok;
+  *src = v.src;
+  *toff = v.toff;
+  *coef = v.coef;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(std::move(key), std::move(v));
+  return ok;
+}
+
 int upload_plan(qk_sim* s) {
   HostPlan& hp = s->hp;
   std::vector<char> buf;
@@ -1584,6 +1635,7 @@ int upload_plan(qk_sim* s) {
   const char* jenv = getenv("QK_JIT");
   const int jit_min = jenv ? atoi(jenv) : 20;   // QK_JIT=<min address bits>; QK_NO_JIT disables
   if (jit_available() && s->nbits >= jit_min) {
+    const auto tj0 = std::chrono::steady_clock::now();
     std::vector<std::string> srcs;
     std::vector<int> src_pass;
     std::vector<std::vector<long long>> toffs;
@@ -1593,7 +1645,7 @@ int upload_plan(qk_sim* s) {
       std::string src;
       std::vector<long long> toff;
       std::vector<double> coef;
-      if (!jit_source(s->tma[s->pass_tma[p]], &src, &toff, &coef)) continue;
+      if (!jit_source_cached(s->tma[s->pass_tma[p]], &src, &toff, &coef)) continue;
       if (const char* dd = getenv("QK_JIT_DUMP")) {
         const std::string path = std::string(dd) + "/pass" + std::to_string(p) + ".cu";
         if (FILE* f = fopen(path.c_str(), "w")) {
@@ -1606,8 +1658,13 @@ int upload_plan(qk_sim* s) {
       toffs.push_back(std::move(toff));
       coefs.push_back(std::move(coef));
     }
+    const auto tj1 = std::chrono::steady_clock::now();
     std::vector<void*> handles;
     jit_build(srcs, &handles);
+    if (getenv("QK_DUMP_LOAD"))
+      fprintf(stderr, "load: jit_source %.3f ms (%zu passes), jit_build %.3f ms\n",
+              std::chrono::duration<double, std::milli>(tj1 - tj0).count(), srcs.size(),
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj1).count());
     for (size_t i = 0; i < srcs.size(); ++i) {
       if (!handles[i]) continue;
       const int p = src_pass[i];
@@ -1737,6 +1794,15 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
 }
 
 int compile_program(qk_sim* s) {
+  const auto tc0 = std::chrono::steady_clock::now();
+  struct PlanTimer {
+    std::chrono::steady_clock::time_point t0;
+    ~PlanTimer() {
+      if (getenv("QK_DUMP_LOAD"))
+        fprintf(stderr, "load: compile_program total %.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } plan_timer{tc0};
   s->hp.clear();
   s->iplan.clear();
   std::string emsg;
@@ -2466,7 +2532,12 @@ int compile_program(qk_sim* s) {
     }
     fprintf(stderr, "relabel=%d Cg=%d fused SQS %d of %d\n", (int)relabel, Cg, nf, ns);
   }
-  return upload_plan(s);
+  const auto tq0 = std::chrono::steady_clock::now();
+  const int urc = upload_plan(s);
+  if (getenv("QK_DUMP_LOAD"))
+    fprintf(stderr, "load: upload_plan %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
+  return urc;
 }
 
 int ensure_events(qk_sim* s, size_t n) {
