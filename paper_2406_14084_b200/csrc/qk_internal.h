@@ -141,6 +141,7 @@ struct alignas(64) TmaParams {
   int32_t rowbits;              // lazy: contiguous row bits of the tile view (3: 128-B, 2: 64-B rows)
   int32_t needs_jit;            // 1: ops the interpreter cannot run (outer-bit table terms)
   int32_t smax;                 // > 0: at most this many stages (leaves L1 to the diagonal tables)
+  int32_t norm;                 // 1: the pass also sums |amp|^2 of what it stores (per group, to p.nrm)
   uint8_t tbit[16];             // lazy: physical address bit of every chunk-local bit (ascending)
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)
@@ -236,6 +237,8 @@ int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p,
                      int np, const int* a, const int* b, int k, CUstream_st* stream);
 int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* stream);
 int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int npos, CUstream_st* stream);
+// sum of n partials (fused-norm readback of the last pass)
+int launch_sum_final(const double* partial, int n, double* out, CUstream_st* stream);
 int launch_sumsq(const double* state, uint64_t n_amps, double* d_partial, double* d_out,
                  CUstream_st* stream);
 int launch_gather(const double* state, const uint64_t* d_idx, uint64_t count, double* d_out,

@@ -83,6 +83,7 @@ struct QkJitParams {
   double2* state;
   double2* out;
   u64 nchunks;
+  double* nrm;
   long long toff[QK_NTAB + 1];
   double coef[QK_NCOEF + 1];
 };
@@ -352,6 +353,7 @@ int jit_slice_bytes(const TmaParams& tp) {
   if (tma_smem_bytes(tp.C, tp.M, &ng, &st, tp.smax) < 0) return 0;
   int b = 0;
   for (int e : slice_plan(tp, st)) b += e * 16;
+  if (tp.norm) b += 16 * 32 * 8;  // per-warp partial sums of the fused norm
   return b;
 }
 
@@ -629,6 +631,8 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         b << "    double2* g = p.out + (chunk << " << C << ");\n";
         for (int j = 0; j < NA; ++j) b << "    st_cs(g + (lt | " << D.rloc[j] << "u), v[" << j << "]);\n";
       }
+      if (tp.norm)
+        for (int j = 0; j < NA; ++j) b << "    nacc = fma(v[" << j << "].x, v[" << j << "].x, fma(v[" << j << "].y, v[" << j << "].y, nacc));\n";
     }
     b << "    }\n";
   }
@@ -795,6 +799,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     o << "  double2* sl = (double2*)(base + " << (size_t)st * (16u << C) + 16 * st << "ull);\n"
       << "  u64 skey = ~0ull;\n";
   }
+  if (tp.norm) o << "  double nacc = 0.0;\n";
   o << "  for (u64 i = g;; i += " << ng << ") {\n"
     << "    if (!" << chunk_ok("i") << ") break;\n"
     << "    const u64 chunk = " << chunk_of("i") << ";\n"
@@ -822,7 +827,22 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   o << ear.str()
     << "    mbar_wait(full + s, round & 1u);\n"
     << b.str()
-    << "  }\n}\n";
+    << "  }\n";
+  if (tp.norm) {
+    // fused norm: per group, warp sums then the group's warps in order (deterministic)
+    size_t planned = 0;
+    for (int e : slice_plan(tp, st)) planned += (size_t)e * 16;
+    const size_t noff = (size_t)st * (16u << C) + 16 * st + planned;
+    o << "  {\n    double* red = (double*)(base + " << noff << "ull) + g * 32;\n"
+      << "    double t = nacc;\n"
+      << "    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);\n"
+      << "    if ((tid & 31u) == 0) red[tid >> 5] = t;\n"
+      << "    gbar(bar_id, " << GT << ");\n"
+      << "    if (tid == 0) {\n      double sum = 0.0;\n"
+      << "      for (int w = 0; w < " << std::max(1, GT / 32) << "; ++w) sum += red[w];\n"
+      << "      p.nrm[blockIdx.x * " << ng << " + g] = sum;\n    }\n  }\n";
+  }
+  o << "}\n";
   *src = o.str();
   return true;
 }

@@ -725,6 +725,11 @@ __global__ void k_sum_final(const double* __restrict__ partial, int n, double* _
   if (threadIdx.x == 0) *out = red[0];
 }
 
+int launch_sum_final(const double* partial, int n, double* out, CUstream_st* stream) {
+  k_sum_final<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(partial, n, out);
+  return (int)cudaGetLastError();
+}
+
 int launch_sumsq(const double* state, uint64_t n, double* d_partial, double* d_out,
                  CUstream_st* stream) {
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);

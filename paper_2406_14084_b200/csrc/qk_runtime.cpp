@@ -1197,6 +1197,11 @@ struct qk_sim {
   // the first TMA pass of a run reads every other chunk as out-of-bounds zeros
   // (no HBM reads), anything else writes the whole state first (ensure_full)
   bool oop_sqs = false;  // relabeled program: unfused SQS permute into the second buffer
+  // fused norm: the program's last data-writing pass sums |amp|^2 per consumer
+  // group into d_nrm; valid until anything writes the state
+  double* d_nrm = nullptr;
+  int norm_pass = -1, nrm_parts = 0;
+  bool norm_valid = false;
   bool fresh = false;
   double fresh_saved = 0;  // read bytes skipped this way (kept out of the stats)
   double* state = nullptr;      // == bufs[cur]
@@ -1629,6 +1634,21 @@ int upload_plan(qk_sim* s) {
       // the planner already relabeled the qubits for this pass: it must run
       if (!ip.permuted) return fail(QK_ESIM, "internal: fused pass is not executable on the TMA path");
     }
+  // the last pass that writes data carries the fused norm, unless a
+  // cross-process exchange follows it (that changes this shard's norm)
+  s->norm_pass = -1;
+  s->norm_valid = false;
+  {
+    int last = -1;
+    for (auto& ip : s->iplan) {
+      if (ip.type == QK_INS_BLOCK && ip.npass > 0) last = ip.pass0 + ip.npass - 1;
+      if (ip.type == QK_INS_CSQS && ip.sqs == -2) last = -2;
+    }
+    if (last >= 0 && s->pass_tma[last] >= 0 && !s->tma[s->pass_tma[last]].xbits && !getenv("QK_NO_FUSED_NORM")) {
+      s->tma[s->pass_tma[last]].norm = 1;
+      s->norm_pass = last;
+    }
+  }
   // specialise TMA passes of large states (compile cost amortised; cached per structure)
   s->pass_jit.assign(hp.passes.size(), nullptr);
   s->jit_blob.assign(hp.passes.size(), {});
@@ -1668,17 +1688,27 @@ int upload_plan(qk_sim* s) {
     for (size_t i = 0; i < srcs.size(); ++i) {
       if (!handles[i]) continue;
       const int p = src_pass[i];
-      // QkJitParams: map[16 words] | tabs | state | out | nchunks | toff[ntab+1] | coef[ncoef+1]
-      std::vector<uint64_t> blob(16 + 4 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
+      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | toff[ntab+1] | coef[ncoef+1]
+      std::vector<uint64_t> blob(16 + 5 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
       blob[16] = (uint64_t)(uintptr_t)s->d_pool;
       const TmaParams& tq = s->tma[s->pass_tma[p]];
       blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
-      for (size_t k = 0; k < toffs[i].size(); ++k) blob[20 + k] = (uint64_t)toffs[i][k];
-      const size_t co = 20 + toffs[i].size() + 1;
+      blob[20] = (uint64_t)(uintptr_t)s->d_nrm;
+      for (size_t k = 0; k < toffs[i].size(); ++k) blob[21 + k] = (uint64_t)toffs[i][k];
+      const size_t co = 21 + toffs[i].size() + 1;
       for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
       s->pass_jit[p] = handles[i];
       s->jit_blob[p] = std::move(blob);
     }
+  }
+  if (s->norm_pass >= 0 && !s->pass_jit[s->norm_pass]) s->norm_pass = -1;  // the interpreter sums nothing
+  if (s->norm_pass >= 0) {
+    const TmaParams& tq = s->tma[s->pass_tma[s->norm_pass]];
+    int ng = 0, st = 0;
+    tma_smem_bytes(tq.C, tq.M, &ng, &st, tq.smax);
+    const uint64_t grid = tq.nchunks < (uint64_t)s->num_sms ? tq.nchunks : (uint64_t)s->num_sms;
+    s->nrm_parts = (int)grid * ng;
+    if (s->nrm_parts > 4096) s->norm_pass = -1;
   }
   // strided-tile passes exist only as specialised kernels: without one the
   // generic register-tiled pass runs them (arbitrary chunk bits, in place)
@@ -2781,6 +2811,7 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
 
 // Bring the state back to the reference layout (two SQS rounds at most).
 int materialize(qk_sim* s, bool keep_fresh = false) {
+  s->norm_valid = false;  // every caller is about to write the state
   if (!keep_fresh) {
     int rc = ensure_full(s);
     if (rc) return rc;
@@ -2867,6 +2898,7 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   CUDA_TRY(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaMalloc(&s->d_partial, 148 * 8 * sizeof(double) + 256));
+  CUDA_TRY(cudaMalloc(&s->d_nrm, 4096 * sizeof(double)));
   s->d_scalar = s->d_partial + 148 * 8;
   int rc = launch_fill_zero_one(s->state, s->amps, rank_lo == 0, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "state init failed");
@@ -2969,6 +3001,7 @@ int qk_destroy(qk_sim* s) {
   if (s->blob) cudaFree(s->blob);
   if (s->d_pool) cudaFree(s->d_pool);
   if (s->d_partial) cudaFree(s->d_partial);
+  if (s->d_nrm) cudaFree(s->d_nrm);
   if (s->d_scratch) cudaFree(s->d_scratch);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
@@ -2980,6 +3013,7 @@ int qk_reset(qk_sim* s) {
   CUDA_TRY(cudaSetDevice(s->device));
   s->cur = 0;
   s->state = s->bufs[0];
+  s->norm_valid = false;
   for (int q = 0; q < s->nbits; ++q) s->lay[q] = q;  // |0...0> is the same in every layout
   // only the first chunk is written; the rest is filled on demand (ensure_full)
   s->fresh = s->amps >= (2ull << kFreshBits) && !getenv("QK_NO_FRESH");
@@ -3097,6 +3131,7 @@ int qk_run(qk_sim* s, double* timings) {
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
+  s->norm_valid = s->norm_pass >= 0;
   double cls[3] = {0, 0, 0};
   for (size_t i = 0; i < ni; ++i) {
     float ms = 0;
@@ -3147,7 +3182,10 @@ int qk_sumsq(qk_sim* s, double* sumsq) {
   if (!s || !sumsq) return fail(QK_EINVAL, "null argument");
   CUDA_TRY(cudaSetDevice(s->device));
   { int frc = ensure_full(s); if (frc) return frc; }
-  int rc = launch_sumsq(s->state, s->amps, s->d_partial, s->d_scalar, (CUstream_st*)s->stream);
+  // the run's last pass already summed what it stored (any later swap only permutes)
+  int rc = s->norm_valid && !getenv("QK_NO_FUSED_NORM")
+               ? launch_sum_final(s->d_nrm, s->nrm_parts, s->d_scalar, (CUstream_st*)s->stream)
+               : launch_sumsq(s->state, s->amps, s->d_partial, s->d_scalar, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "norm launch failed");
   CUDA_TRY(cudaMemcpyAsync(sumsq, s->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));

@@ -489,3 +489,34 @@ def test_wide_chunk_lazy_layout_at_33_qubits(gpu):
     eager = session({"QK_NO_LAZY12": "1"})
     assert np.max(np.abs(lazy[0] - eager[0])) <= TOL
     assert abs(lazy[1] - eager[1]) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_fused_norm_matches_full_sum_and_invalidates(gpu):
+    """The run's last pass sums |amp|^2 of what it stores; qk_sumsq then only
+    adds the per-group partials. It must equal the full-state sum, and any
+    later writer must fall back to the full sum."""
+    import os
+    from conftest import ROOT
+    for name, n, c in (("qaoa24_c12_r0.txt", 24, 12), ("qft20_c10_r0.txt", 20, 10)):
+        text = open(os.path.join(ROOT, "bench_circuits", name)).read()
+        sim = Simulator(LayoutParams(n=n, c=n))
+        perm = sim.load_text(text, c)
+        sim.reset()
+        sim.run_loaded(perm)
+        fused = sim.handle.sumsq()
+        os.environ["QK_NO_FUSED_NORM"] = "1"
+        try:
+            full = sim.handle.sumsq()
+        finally:
+            os.environ.pop("QK_NO_FUSED_NORM")
+        assert abs(fused - full) <= 1e-12, (name, fused, full)
+        sim.partitions[0].amps[0:1] = np.array([3.0 + 4.0j])   # a writer: |a0|^2 becomes 25
+        after = sim.handle.sumsq()
+        os.environ["QK_NO_FUSED_NORM"] = "1"
+        try:
+            want = sim.handle.sumsq()
+        finally:
+            os.environ.pop("QK_NO_FUSED_NORM")
+        assert after == want and after > 20.0
+        sim.close()
