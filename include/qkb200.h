@@ -76,7 +76,8 @@ int qk_create_shard(int n, int r, int b, int device, int rank_lo, int count, qk_
 
 int qk_destroy(qk_sim* sim);
 
-/* Simulator.reset — simulator.py:439-442 */
+/* Simulator.reset — simulator.py:439-442. Writes |0...0>; only the first 2^13
+ * amplitudes go to HBM here, the next pass or reader fills the rest. */
 int qk_reset(qk_sim* sim);
 
 /* Layout queries */
@@ -135,7 +136,9 @@ int qk_kernel_stats(qk_sim* sim, double* out, int reset);
 int qk_set_profiling(qk_sim* sim, int per_launch);
 
 /* SimResult.norm — simulator.py:393-397 (this handle's partitions only; the
- * multi-process mirror sums squares across ranks). sumsq = sum |a|^2. */
+ * multi-process mirror sums squares across ranks). sumsq = sum |a|^2. Right
+ * after qk_run it adds the partial sums the program's last pass produced while
+ * storing; after any write it reads the whole state. */
 int qk_sumsq(qk_sim* sim, double* sumsq);
 
 /* Physical amplitudes of partition `part` (0-based within the handle),
