@@ -159,6 +159,18 @@ int qk_read_logical(qk_sim* sim, const int32_t* perm, const uint64_t* logical_id
 int qk_read_logical_range(qk_sim* sim, const int32_t* perm, uint64_t start, uint64_t count,
                           double* reim);
 
+/* <phi|psi> of this handle's amplitudes with the product state
+ * phi = (x)_q (f_q[0] |0> + f_q[1] |1>) over LOGICAL qubits q: factors holds 4n
+ * doubles, (f_q[0].re, f_q[0].im, f_q[1].re, f_q[1].im) per logical qubit; perm
+ * is the final permutation (pos -> logical qubit, circuit.py:202-210; NULL =
+ * identity). Every analytic answer the reference's own tests pin is a product
+ * state (QFT|0> and H layers uniform, BV a basis state, test_oracle.py:32-42;
+ * U/RZZ layers), so this gives the normalised fidelity
+ * |<phi|psi>|^2 / (<phi|phi> <psi|psi>) at sizes the CPU reference cannot run
+ * (SURVEY.md §8(c)). One HBM read of the state. out = (re, im). A shard
+ * returns its part of the sum (the mirror adds the shards). */
+int qk_overlap_product(qk_sim* sim, const int32_t* perm, const double* factors, double* out);
+
 /* Kernel-level entry points (unit parity with the reference functions). */
 /* apply_gate_block(partition, block, c, cl, row_start, row_stop) — simulator.py:338-357;
  * block given in packed form (one QK_INS_BLOCK record). rows of 2^c. */

@@ -55,6 +55,7 @@ _SIGS = {
     "qk_gather": (c_int, [c_void, P(c_u64), c_u64, P(c_dbl)]),
     "qk_read_logical": (c_int, [c_void, P(c_int32), P(c_u64), c_u64, P(c_dbl)]),
     "qk_read_logical_range": (c_int, [c_void, P(c_int32), c_u64, c_u64, P(c_dbl)]),
+    "qk_overlap_product": (c_int, [c_void, P(c_int32), P(c_dbl), P(c_dbl)]),
     "qk_apply_block": (c_int, [c_void, c_int, P(c_int32), c_size, P(c_dbl), c_size, c_int, c_u64,
                                c_u64]),
     "qk_sqs": (c_int, [c_void, c_int, P(c_int32), P(c_int32), c_int, c_int, c_u64, c_u64]),
@@ -224,6 +225,10 @@ class Handle:
         self._keep = None
 
     def __del__(self):
+        self.free()
+
+    def free(self):
+        """Destroy the native handle (device state and plans) now."""
         if getattr(self, "ptr", None) and self.ptr.value and _lib is not None:
             _lib.qk_destroy(self.ptr)
             self.ptr = c_void(None)
@@ -298,6 +303,16 @@ class Handle:
             check(lib().qk_read_logical_range(self.ptr, iptr(pm), start, count,
                                               out.ctypes.data_as(P(c_dbl))))
         return out
+
+    def overlap_product(self, perm, factors) -> complex:
+        """<phi|psi> with the product state phi = (x)_q (f_q0|0> + f_q1|1>) over
+        logical qubits; factors is (n, 2) complex (qk_overlap_product)."""
+        pm = np.ascontiguousarray(perm if perm is not None else range(self.n), dtype=np.int32)
+        f = np.ascontiguousarray(np.asarray(factors, dtype=np.complex128).reshape(self.n, 2))
+        out = np.zeros(2, dtype=np.float64)
+        check(lib().qk_overlap_product(self.ptr, iptr(pm), f.view(np.float64).ctypes.data_as(P(c_dbl)),
+                                       dptr(out)))
+        return complex(out[0], out[1])
 
     def apply_block(self, part, words, params, nparams, c, row_start, row_stop):
         check(lib().qk_apply_block(self.ptr, part, iptr(words), len(words), dptr(params), nparams,

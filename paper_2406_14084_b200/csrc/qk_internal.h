@@ -246,4 +246,9 @@ int launch_gather(const double* state, const uint64_t* d_idx, uint64_t count, do
 int launch_gather_logical(const double* state, const int* perm, int n, uint64_t start,
                           uint64_t count, double* d_out, CUstream_st* stream);
 int launch_fill_zero_one(double* state, uint64_t n_amps, int set_first, CUstream_st* stream);
+// <phi|psi> against a product state: d_tabs = 4 x 1024 conj factor tables, d_work
+// overlap_scratch_bytes() bytes; the result (re, im) lands at d_work + 2*148*8
+int overlap_scratch_bytes();
+int launch_overlap(const double* state, uint64_t n_amps, const double* d_tabs, double* d_work,
+                   CUstream_st* stream);
 }  // namespace qk

@@ -785,6 +785,81 @@ int launch_gather_logical(const double* state, const int* perm, int n, uint64_t 
   return (int)cudaGetLastError();
 }
 
+// Overlap <phi|psi> of the state with a product state (analytic parity at
+// sizes beyond the CPU reference): conj(phi_j) is the product
+// of four 1024-entry tables, one per 10-bit group of the memory index j
+// (built on the host from the per-qubit factors and the layout). Deterministic
+// two-level reduction like k_sumsq.
+constexpr int kOvBlocks = 148 * 8;
+
+__global__ void __launch_bounds__(256) k_overlap(const double2* __restrict__ s, uint64_t n,
+                                                 const double2* __restrict__ tabs,
+                                                 double2* __restrict__ partial) {
+  extern __shared__ double2 T[];  // 4 x 1024
+  for (int i = threadIdx.x; i < 4096; i += blockDim.x) T[i] = tabs[i];
+  __syncthreads();
+  double re = 0.0, im = 0.0;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (uint64_t)gridDim.x * blockDim.x) {
+    const double2 a = T[j & 1023], b = T[1024 + ((j >> 10) & 1023)];
+    const double2 c = T[2048 + ((j >> 20) & 1023)], d = T[3072 + ((j >> 30) & 1023)];
+    const double2 ab = make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+    const double2 cd = make_double2(c.x * d.x - c.y * d.y, c.x * d.y + c.y * d.x);
+    const double2 f = make_double2(ab.x * cd.x - ab.y * cd.y, ab.x * cd.y + ab.y * cd.x);
+    const double2 v = s[j];
+    re = fma(f.x, v.x, fma(-f.y, v.y, re));
+    im = fma(f.x, v.y, fma(f.y, v.x, im));
+  }
+  __shared__ double rr[256], ri[256];
+  rr[threadIdx.x] = re;
+  ri[threadIdx.x] = im;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      rr[threadIdx.x] += rr[threadIdx.x + w];
+      ri[threadIdx.x] += ri[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = make_double2(rr[0], ri[0]);
+}
+
+__global__ void k_overlap_final(const double2* __restrict__ partial, int n, double2* __restrict__ out) {
+  __shared__ double rr[256], ri[256];
+  double re = 0.0, im = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    re += partial[i].x;
+    im += partial[i].y;
+  }
+  rr[threadIdx.x] = re;
+  ri[threadIdx.x] = im;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      rr[threadIdx.x] += rr[threadIdx.x + w];
+      ri[threadIdx.x] += ri[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = make_double2(rr[0], ri[0]);
+}
+
+int overlap_scratch_bytes() { return (4096 + kOvBlocks + 1) * 16; }
+
+int launch_overlap(const double* state, uint64_t n, const double* d_tabs, double* d_work, CUstream_st* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16);
+    attr = true;
+  }
+  double2* part = reinterpret_cast<double2*>(d_work);
+  k_overlap<<<kOvBlocks, 256, 4096 * 16, st>>>(reinterpret_cast<const double2*>(state), n,
+                                               reinterpret_cast<const double2*>(d_tabs), part);
+  k_overlap_final<<<1, 256, 0, st>>>(part, kOvBlocks, part + kOvBlocks);
+  return (int)cudaGetLastError();
+}
+
 __global__ void k_set_one(double2* s) { s[0] = make_double2(1.0, 0.0); }
 
 int launch_fill_zero_one(double* state, uint64_t n, int set_first, CUstream_st* stream) {

@@ -1644,9 +1644,20 @@ int upload_plan(qk_sim* s) {
       if (ip.type == QK_INS_BLOCK && ip.npass > 0) last = ip.pass0 + ip.npass - 1;
       if (ip.type == QK_INS_CSQS && ip.sqs == -2) last = -2;
     }
-    if (last >= 0 && s->pass_tma[last] >= 0 && !s->tma[s->pass_tma[last]].xbits && !getenv("QK_NO_FUSED_NORM")) {
-      s->tma[s->pass_tma[last]].norm = 1;
-      s->norm_pass = last;
+    // (temporary one-block plans of the kernel-level entry points run with an
+    // empty iplan, so `last` always indexes this plan's passes)
+    if (last >= 0 && last < (int)s->pass_tma.size() && s->pass_tma[last] >= 0 &&
+        !s->tma[s->pass_tma[last]].xbits && !getenv("QK_NO_FUSED_NORM")) {
+      TmaParams& tq = s->tma[s->pass_tma[last]];
+      int ng = 0, st = 0;
+      tma_smem_bytes(tq.C, tq.M, &ng, &st, tq.smax);
+      const uint64_t grid = tq.nchunks < (uint64_t)s->num_sms ? tq.nchunks : (uint64_t)s->num_sms;
+      // the partials buffer holds 4096 doubles and the kernel's reduction area 16 groups
+      if (ng <= 16 && grid * (uint64_t)ng <= 4096) {
+        tq.norm = 1;
+        s->norm_pass = last;
+        s->nrm_parts = (int)grid * ng;
+      }
     }
   }
   // specialise TMA passes of large states (compile cost amortised; cached per structure)
@@ -1702,14 +1713,6 @@ int upload_plan(qk_sim* s) {
     }
   }
   if (s->norm_pass >= 0 && !s->pass_jit[s->norm_pass]) s->norm_pass = -1;  // the interpreter sums nothing
-  if (s->norm_pass >= 0) {
-    const TmaParams& tq = s->tma[s->pass_tma[s->norm_pass]];
-    int ng = 0, st = 0;
-    tma_smem_bytes(tq.C, tq.M, &ng, &st, tq.smax);
-    const uint64_t grid = tq.nchunks < (uint64_t)s->num_sms ? tq.nchunks : (uint64_t)s->num_sms;
-    s->nrm_parts = (int)grid * ng;
-    if (s->nrm_parts > 4096) s->norm_pass = -1;
-  }
   // strided-tile passes exist only as specialised kernels: without one the
   // generic register-tiled pass runs them (arbitrary chunk bits, in place)
   for (size_t p = 0; p < hp.passes.size(); ++p)
@@ -3277,6 +3280,57 @@ int qk_read_logical(qk_sim* s, const int32_t* perm, const uint64_t* lidx, uint64
   return qk_gather(s, phys.data(), count, reim);
 }
 
+int qk_overlap_product(qk_sim* s, const int32_t* perm, const double* factors, double* out) {
+  if (!s || !factors || !out) return fail(QK_EINVAL, "null argument");
+  std::vector<int> pm(s->n);
+  for (int q = 0; q < s->n; ++q) pm[q] = perm ? perm[q] : q;
+  {
+    std::vector<int> seen(s->n, 0);
+    for (int q = 0; q < s->n; ++q) {
+      if (pm[q] < 0 || pm[q] >= s->n || seen[pm[q]]) return fail(QK_EINVAL, "permutation is not a bijection");
+      seen[pm[q]] = 1;
+    }
+  }
+  CUDA_TRY(cudaSetDevice(s->device));
+  { int frc = ensure_full(s); if (frc) return frc; }
+  // factor of memory bit p: reference bit q with lay[q] == p -> logical qubit pm[q]
+  std::vector<cplx> mf(40 * 2, cplx(1.0, 0.0));
+  for (int p = 0; p < 40; ++p) mf[2 * p + 1] = cplx(0.0, 0.0);
+  for (int q = 0; q < s->nbits; ++q) {
+    const double* f = factors + 4 * pm[q];
+    const int p = s->lay.empty() ? q : s->lay[q];
+    mf[2 * p] = std::conj(cplx(f[0], f[1]));
+    mf[2 * p + 1] = std::conj(cplx(f[2], f[3]));
+  }
+  cplx cst(1.0, 0.0);
+  const uint64_t base = (uint64_t)s->rank_lo << s->L;
+  for (int q = s->nbits; q < s->n; ++q) {
+    const double* f = factors + 4 * pm[q];
+    cst *= ((base >> q) & 1) ? std::conj(cplx(f[2], f[3])) : std::conj(cplx(f[0], f[1]));
+  }
+  std::vector<cplx> tabs(4096);
+  for (int g = 0; g < 4; ++g)
+    for (int v = 0; v < 1024; ++v) {
+      cplx t(1.0, 0.0);
+      for (int b = 0; b < 10; ++b) t *= mf[2 * (10 * g + b) + ((v >> b) & 1)];
+      tabs[1024 * g + v] = t;
+    }
+  int rc = ensure_scratch(s, (size_t)overlap_scratch_bytes() + 4096 * 16);
+  if (rc) return rc;
+  double* d_tabs = (double*)s->d_scratch;
+  double* d_work = d_tabs + 2 * 4096;
+  CUDA_TRY(cudaMemcpyAsync(d_tabs, tabs.data(), 4096 * 16, cudaMemcpyHostToDevice, s->stream));
+  rc = launch_overlap(s->state, s->amps, d_tabs, d_work, (CUstream_st*)s->stream);
+  if (rc) return fail(QK_ECUDA, "overlap launch failed");
+  double res[2];
+  CUDA_TRY(cudaMemcpyAsync(res, d_work + 2 * 148 * 8, 16, cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const cplx o = cst * cplx(res[0], res[1]);
+  out[0] = o.real();
+  out[1] = o.imag();
+  return QK_OK;
+}
+
 int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64_t count, double* reim) {
   if (!s || !perm || (count && !reim)) return fail(QK_EINVAL, "null argument");
   if (s->count != (1 << s->r)) return fail(QK_EINVAL, "logical range readback needs the whole state");
@@ -3378,7 +3432,9 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
   if (row_start >= row_stop) return QK_OK;
   // chunk = [0, c) of the partition, outer = [c, L): CTA index == row
   HostPlan keep = std::move(s->hp);
+  std::vector<InstrPlan> keep_ip = std::move(s->iplan);
   s->hp.clear();
+  s->iplan.clear();
   std::vector<int> Q;
   for (int p = 0; p < c; ++p) Q.push_back(p);
   std::vector<const GateH*> gs;
@@ -3386,6 +3442,7 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
   rc = compile_pass(s->hp, gs, Q, s->L, 0, emsg);
   if (rc) {
     s->hp = std::move(keep);
+    s->iplan = std::move(keep_ip);
     return fail(rc, "%s", emsg.c_str());
   }
   rc = upload_plan(s);
@@ -3402,6 +3459,7 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
     }
   }
   s->hp = std::move(keep);
+  s->iplan = std::move(keep_ip);
   int rc2 = upload_plan(s);
   return rc ? rc : rc2;
 }
@@ -3416,7 +3474,9 @@ int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const dou
   if (rc) return fail(rc, "%s", emsg.c_str());
   if (prog.size() != 1 || prog[0].type != QK_INS_BLOCK) return fail(QK_EINVAL, "expected one gate block");
   HostPlan keep = std::move(s->hp);
+  std::vector<InstrPlan> keep_ip = std::move(s->iplan);
   s->hp.clear();
+  s->iplan.clear();
   InstrPlan ip;
   // force the memory-level grouping by compiling gate by gate as singleton blocks
   rc = QK_OK;
@@ -3429,6 +3489,7 @@ int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const dou
   }
   if (rc) {
     s->hp = std::move(keep);
+    s->iplan = std::move(keep_ip);
     return fail(rc, "%s", emsg.c_str());
   }
   rc = upload_plan(s);
@@ -3438,6 +3499,7 @@ int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const dou
     if (e != cudaSuccess) rc = fail(QK_ECUDA, "%s", cudaGetErrorString(e));
   }
   s->hp = std::move(keep);
+  s->iplan = std::move(keep_ip);
   int rc2 = upload_plan(s);
   return rc ? rc : rc2;
 }

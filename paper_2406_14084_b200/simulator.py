@@ -170,13 +170,14 @@ def bitshift(t, a_bits, b_bits, cl: int, n_local: int):
 # kernel-level entry points (unit parity with the reference functions)
 
 _scratch: dict = {}
+_MAX_TILE = 13        # widest chunk one register-tiled block pass holds (qk_internal.h kMaxC)
 
 
 def _scratch_handle(n: int, r: int = 0) -> _lib.Handle:
     key = (n, r)
     h = _scratch.get(key)
     if h is None:
-        if len(_scratch) > 16:
+        if len(_scratch) >= 4:          # bounded: each is a device state
             _scratch.clear()
         h = _lib.Handle(n, r, n - r)
         _scratch[key] = h
@@ -204,20 +205,47 @@ def apply_gate_block(partition: StatePartition, block, c: int, cl: int,
 
 
 def apply_gate_full(amps, gate, part: int = 0, parts: int = 1) -> None:
-    """simulator.py:360-376 — memory-level single gate over the whole array
-    (the `part/parts` split is a thread partition; the GPU pass covers all)."""
-    if part != 0:
-        return
-    words, params, npar = _lib.pack([type("B", (), {"gates": (gate,)})()])
-    data = np.array(amps) if isinstance(amps, DeviceAmps) else amps
-    h = _scratch_handle(_log2_size(data))
-    h.write(0, 0, data)
-    h.apply_gate_full(words, params, npar)
-    out = h.read(0, 0, len(data))
-    if isinstance(amps, DeviceAmps):
-        amps[:] = out
+    """simulator.py:360-376 — memory-level single gate: rows of
+    2^(max target + 1) amplitudes, optionally only the aligned slice `part` of
+    `parts` (units lo..hi, as the reference splits them). Runs as the device
+    block pass over that row range (apply_gate_2d is the same gate on every row)."""
+    n_local = _log2_size(amps)
+    width = max(gate.targets) + 1
+    if width > n_local:
+        raise ValueError(f"gate target {max(gate.targets)} beyond {n_local} local qubits")
+    n_units = len(amps) >> width
+    if n_units >= parts > 1:
+        lo, hi = n_units * part // parts, n_units * (part + 1) // parts
+        if lo == hi:
+            return
     else:
-        amps[...] = out
+        if part != 0:
+            return
+        lo, hi = 0, n_units
+    words, params, npar = _lib.pack([type("B", (), {"gates": (gate,)})()])
+    if width <= _MAX_TILE:
+        if isinstance(amps, DeviceAmps):
+            amps.handle.apply_block(amps.part, words, params, npar, width, lo, hi)
+            return
+        h = _scratch_handle(n_local)
+        h.write(0, 0, amps)
+        h.apply_block(0, words, params, npar, width, lo, hi)
+        amps[...] = h.read(0, 0, len(amps))
+        return
+    # wider than one tile: the memory-level device pass over each 2^width row
+    unit = 1 << width
+    h = _scratch_handle(width)
+    for row in range(lo, hi):
+        if isinstance(amps, DeviceAmps):
+            h.write(0, 0, amps.handle.read(amps.part, row * unit, unit))
+        else:
+            h.write(0, 0, amps[row * unit:(row + 1) * unit])
+        h.apply_gate_full(words, params, npar)
+        out = h.read(0, 0, unit)
+        if isinstance(amps, DeviceAmps):
+            amps.handle.write(amps.part, row * unit, out)
+        else:
+            amps[row * unit:(row + 1) * unit] = out
 
 
 def in_memory_swap(amps, out_set, in_set, cl: int, start: int = 0,
@@ -322,6 +350,29 @@ class SimResult:                              # simulator.py:383-407
             return self.logical_vector()[start:start + count]
         return h.read_logical_range(self.final_permutation, start, count)
 
+    def release(self) -> None:
+        """Free the device state behind these partitions now (instead of at GC)."""
+        h = _shared_handle(self.partitions)
+        if h is not None:
+            h.free()
+
+    def fidelity_product(self, factors) -> float:
+        """Normalised fidelity |<phi|psi>|^2 / (<phi|phi><psi|psi>) with the product
+        state phi = (x)_q (f_q0|0> + f_q1|1>) over logical qubits (qk_overlap_product):
+        one device read of the state, for analytic parity at any size."""
+        h = _shared_handle(self.partitions)
+        f = np.asarray(factors, dtype=np.complex128).reshape(-1, 2)
+        if h is None:
+            v = self.logical_vector()
+            phi = np.ones(1, dtype=np.complex128)
+            for q in range(f.shape[0]):
+                phi = np.concatenate([phi * f[q, 0], phi * f[q, 1]])
+            ov = np.vdot(phi, v)
+        else:
+            ov = h.overlap_product(self.final_permutation, f)
+        nphi = float(np.prod(np.sum(np.abs(f) ** 2, axis=1)))
+        return abs(ov) ** 2 / (nphi * self.norm() ** 2)
+
     def amplitude(self, logical_index: int) -> complex:
         h = _shared_handle(self.partitions)
         n = len(self.final_permutation)
@@ -356,8 +407,15 @@ class Simulator:
     def reset(self) -> None:                  # simulator.py:439-442
         self._h.reset()
 
-    def close(self) -> None:                  # simulator.py:444-447 (state stays readable)
-        pass
+    def close(self) -> None:                  # simulator.py:444-447
+        """Like the reference, close() ends the executor but keeps the state
+        readable: `simulate` closes the Simulator before returning a SimResult
+        whose partitions alias it (simulator.py:555, 572-578). The device
+        memory goes when the last view is dropped, or at once with release()."""
+
+    def release(self) -> None:
+        """Free the device state now (16 B x 2^N); every view of it becomes invalid."""
+        self._h.free()
 
     def __enter__(self):
         return self

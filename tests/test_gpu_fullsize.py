@@ -1,0 +1,199 @@
+"""Parity at the bench sizes, on the DEFAULT execution path (lazy layout,
+diagonal folding, fused norm, table-aware order — whatever `bench.py` runs).
+
+* 26-30 qubits: the reference simulator itself was run on the full state in the
+  build container (`oracle/gen_golden_large.py`, reference
+  `Simulator.run`, simulator.py:529-555); 65,538 sampled physical amplitudes,
+  the norm and the final permutation are committed under tests/golden/. The GPU
+  result must match them within 1e-10 (north_star).
+* 33 qubits (C3; the CPU reference would need 128 GiB of host RAM): every
+  circuit has a product-state answer (QFT|0> and the H layer are uniform, BV
+  returns to |0..0>, test_oracle.py:32-42; the RZZ layer is a phase on |0..0>;
+  the U layer is (x)_q U_q|0>). The normalised fidelity over the WHOLE state is
+  computed on the device (qk_overlap_product) and must be >= 1 - 1e-12; 65,536
+  random logical amplitudes must match the analytic values within 1e-10.
+"""
+import gc
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+from paper_2406_14084_b200 import (Gate, GateBlock, GateKind, LayoutParams, Simulator,
+                                   StatePartition, apply_gate_block, apply_gate_full, gate_matrix,
+                                   parse_optimized)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _text(name):
+    with open(os.path.join(ROOT, "bench_circuits", name + ".txt")) as fh:
+        return fh.read()
+
+
+def _run_default(name, n, c, r=0):
+    sim = Simulator(LayoutParams(n=n, c=n - r, r=r))
+    perm = sim.load_text(_text(name), c)
+    sim.reset()
+    return sim, sim.run_loaded(perm)
+
+
+@pytest.mark.parametrize("name", ["qaoa26_c12_r0", "qft30_c10_r0", "bv30_c10_r0",
+                                  "qaoa30_c12_r0"])
+def test_reference_full_size(gpu, name):
+    path = os.path.join(GOLDEN, f"large_{name}.npz")
+    if not os.path.exists(path):
+        pytest.fail(f"missing fixture {path} (python oracle/gen_golden_large.py {name})")
+    g = np.load(path)
+    info = json.loads(str(g["info"]))
+    n, c, r = info["n"], info["c"], info["r"]
+    sim, res = _run_default(name, n, c, r)
+    assert tuple(res.final_permutation) == tuple(int(x) for x in g["perm"])
+    got = sim.handle.gather(g["idx"].astype(np.uint64))
+    err = float(np.max(np.abs(got - g["amps"])))
+    nrm = res.norm()
+    print(f"\n  {name}: {g['idx'].size} sampled amplitudes, max |gpu-ref| = {err:.3e}, "
+          f"norm {nrm!r} vs ref {float(g['norm'])!r}")
+    assert err <= TOL, err
+    assert abs(nrm - float(g["norm"])) <= 1e-12
+    # a second run on the same handle (continues from the end layout) must
+    # equal a fresh one
+    sim.reset()
+    res = sim.run_loaded(res.final_permutation)
+    again = sim.handle.gather(g["idx"].astype(np.uint64))
+    assert np.array_equal(again, got)
+    sim.release()
+    gc.collect()
+
+
+def _product_factors(name, n):
+    """Per logical qubit (f0, f1) of the analytic answer, and the exact a_0."""
+    opt = parse_optimized(_text(name), LayoutParams(n=n, c=n))
+    gates = [g for ins in opt.instructions for g in getattr(ins, "gates", ())]
+    f = np.zeros((n, 2), dtype=np.complex128)
+    fam = name.split("_")[0].rstrip("0123456789")
+    if fam in ("qft", "h"):
+        f[:] = 2 ** -0.5
+    elif fam in ("bv", "rzz"):
+        f[:, 0] = 1.0
+    elif fam == "u":
+        us = [g for g in gates if g.kind == GateKind.U]
+        assert len(us) == n
+        for g in us:   # gen_gate_layer: gate id q acts on logical qubit q
+            f[g.gid] = gate_matrix(Gate(GateKind.U, (0,), 0, g.params))[:, 0]
+    else:
+        raise AssertionError(name)
+    a0 = complex(np.prod(f[:, 0]))
+    if fam == "rzz":   # diagonal layer: |0..0> times the product of the entries [0, 0]
+        a0 = complex(np.prod([gate_matrix(g)[0, 0] for g in gates]))
+    return f, a0
+
+
+@pytest.mark.parametrize("name", ["qft33_c10_r0", "h33_c10_r0", "bv33_c10_r0", "rzz33_c10_r0",
+                                  "u33_c10_r0"])
+def test_analytic_33_qubits(gpu, name):
+    n = 33
+    f, a0 = _product_factors(name, n)
+    sim, res = _run_default(name, n, 10)
+    fid = res.fidelity_product(f)
+    nrm = res.norm()
+    rng = np.random.default_rng(21)
+    idx = np.unique(np.concatenate([rng.integers(0, 1 << n, 1 << 16, dtype=np.int64),
+                                    [0, (1 << n) - 1]]))
+    got = sim.handle.read_logical(res.final_permutation, idx.astype(np.uint64))
+    want = np.ones(idx.size, dtype=np.complex128)
+    for q in range(n):
+        want *= np.where((idx >> q) & 1, f[q, 1], f[q, 0])
+    if name.startswith("rzz"):
+        want = want * a0
+    err = float(np.max(np.abs(got - want)))
+    print(f"\n  {name}: 1-fidelity = {1 - fid:.3e}, norm-1 = {nrm - 1:.3e}, "
+          f"max |gpu-analytic| over {idx.size} amps = {err:.3e}, a0 = {got[0]!r}")
+    assert fid >= 1 - 1e-12, fid
+    assert abs(nrm - 1.0) <= 1e-10
+    assert err <= TOL
+    assert abs(got[0] - a0) <= TOL
+    sim.release()
+    del res, sim
+    gc.collect()
+
+
+def test_overlap_product_matches_dense(gpu):
+    """qk_overlap_product against numpy on a random 2^16 state (both layouts)."""
+    rng = np.random.default_rng(4)
+    n = 16
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    f = rng.normal(size=(n, 2)) + 1j * rng.normal(size=(n, 2))
+    perm = tuple(int(x) for x in rng.permutation(n))
+    with Simulator(LayoutParams(n=n, c=n)) as sim:
+        sim.partitions[0].amps[:] = v
+        got = sim.handle.overlap_product(perm, f)
+    # logical index l -> physical p: bit pos of p = bit perm[pos] of l
+    lidx = np.arange(1 << n)
+    phys = np.zeros_like(lidx)
+    for pos, q in enumerate(perm):
+        phys |= ((lidx >> q) & 1) << pos
+    phi = np.ones(1 << n, dtype=np.complex128)
+    for q in range(n):
+        phi *= np.where((lidx >> q) & 1, f[q, 1], f[q, 0])
+    want = np.vdot(phi, v[phys])
+    assert abs(got - want) <= 1e-9 * abs(want)
+
+
+def test_kernel_level_entry_points_after_run(gpu):
+    """apply_gate_block / apply_gate_full on a Simulator partition
+    after run() must not disturb the loaded program (temporary one-block plans)
+    and must match the same ops on a host copy."""
+    text = _text("qaoa24_c12_r0")
+    n = 24
+    sim = Simulator(LayoutParams(n=n, c=n))
+    perm = sim.load_text(text, 12)
+    sim.reset()
+    first = sim.run_loaded(perm).physical_vector()
+    host = StatePartition(0, first.copy())
+    blk = GateBlock((Gate(GateKind.H, (3,), 0), Gate(GateKind.RZZ, (0, 5), 1, (0.7,)),
+                     Gate(GateKind.U, (2,), 2, (0.1, 0.2, 0.3))))
+    apply_gate_block(sim.partitions[0], blk, c=6, cl=2, row_start=5, row_stop=1000)
+    apply_gate_block(host, blk, c=6, cl=2, row_start=5, row_stop=1000)
+    g = Gate(GateKind.RX, (9,), 3, (0.4,))
+    apply_gate_full(sim.partitions[0].amps, g, part=1, parts=3)
+    apply_gate_full(host.amps, g, part=1, parts=3)
+    assert np.max(np.abs(np.asarray(sim.partitions[0].amps) - host.amps)) <= TOL
+    sim.reset()
+    again = sim.run_loaded(perm).physical_vector()   # the program survived
+    assert np.array_equal(again, first)
+    assert abs(sim.handle.sumsq() - 1.0) <= 1e-12
+
+
+def test_apply_gate_full_parts_follow_reference_slices(gpu):
+    """apply_gate_full(part, parts) touches only units [lo, hi) of the
+    reference split (simulator.py:360-376); the union over parts is the whole."""
+    from oracle import quokka_oracle as orc
+    rng = np.random.default_rng(8)
+    n = 12
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    for g in (Gate(GateKind.H, (4,), 0), Gate(GateKind.CX, (7, 2), 1),
+              Gate(GateKind.CP, (1, 10), 2, (0.9,))):
+        whole = v.copy()
+        apply_gate_full(whole, g)
+        pieces = v.copy()
+        for k in range(5):
+            one = v.copy()
+            apply_gate_full(one, g, part=k, parts=5)
+            unit = 1 << (max(g.targets) + 1)
+            units = (1 << n) // unit
+            if units >= 5:
+                lo, hi = units * k // 5, units * (k + 1) // 5
+            else:                  # too few units: part 0 takes the whole array
+                lo, hi = (0, units) if k == 0 else (0, 0)
+            changed = np.nonzero(one != v)[0]
+            assert changed.size == 0 or (changed.min() >= lo * unit and changed.max() < hi * unit)
+            pieces[lo * unit:hi * unit] = one[lo * unit:hi * unit]
+        assert np.array_equal(pieces, whole)
+        want = orc.dense_apply(v.copy(), orc.OGate(g.kind.value, g.targets, g.gid, g.params), n)
+        assert np.max(np.abs(whole - want)) <= TOL
+    assert math.isfinite(float(np.abs(v).sum()))
