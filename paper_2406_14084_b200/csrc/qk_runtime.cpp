@@ -1725,6 +1725,28 @@ int upload_plan(qk_sim* s) {
         if (tq.dpos[x] != tq.tbit[x]) return fail(QK_ESIM, "lazy pass needs the specialised kernel (NVRTC)");
       s->pass_tma[p] = -1;
     }
+  if (getenv("QK_DUMP_TABLES"))
+    for (size_t p = 0; p < hp.passes.size(); ++p) {
+      if (s->pass_tma[p] < 0) continue;
+      const TmaParams& tq = s->tma[s->pass_tma[p]];
+      fprintf(stderr, "pass %zu C=%d M=%d phases=%d smax=%d tbit=", p, tq.C, tq.M, tq.nphases, tq.smax);
+      for (int k = 0; k < tq.C; ++k) fprintf(stderr, "%d,", tq.tbit[k]);
+      fprintf(stderr, "\n");
+      for (int ph = 0; ph < tq.nphases; ++ph)
+        for (int o = tq.ph[ph].op_begin; o < tq.ph[ph].op_end; ++o) {
+          const TOp& op = tq.ops[o];
+          if (op.code != OP_DIAG) {
+            fprintf(stderr, "   ph%d op%d code=%d\n", ph, o, op.code);
+            continue;
+          }
+          int bits = -1;
+          for (auto& td : hp.tables)
+            if (td.out == op.table) bits = td.bits;
+          fprintf(stderr, "   ph%d op%d DIAG bits=%d nco=%d co_k=", ph, o, bits, op.nco);
+          for (int k = 0; k < op.nco; ++k) fprintf(stderr, "%d,", op.co_k[k]);
+          fprintf(stderr, "\n");
+        }
+    }
   if (getenv("QK_DUMP_PLAN"))
     for (size_t i = 0; i < s->iplan.size(); ++i) {
       const InstrPlan& ip = s->iplan[i];
