@@ -12,9 +12,12 @@
  * (little endian); the top r bits select the rank partition
  * (circuit.py:157-163, simulator.py:415-419). A handle created
  * with qk_create holds all 2^r partitions on one device, contiguous; a handle
- * created with qk_create_shard holds the partitions [rank_lo, rank_lo+count)
- * of a multi-process job (one process per GPU) and reaches its peers' state
- * through CUDA IPC mappings over NVLink (qk_ipc_handle / qk_ipc_open).
+ * created with qk_create_multi splits them over several devices driven by one
+ * process; a handle created with qk_create_shard holds the partitions
+ * [rank_lo, rank_lo+count) of a multi-process job (one process per GPU) and
+ * reaches its peers' state through CUDA IPC mappings over NVLink
+ * (qk_ipc_handle / qk_ipc_open). Cross-shard CSQS synchronise on flags in
+ * peer memory (device-side barrier), never through the host.
  *
  * Return value of every int function: QK_OK (0) or a negative status; the
  * thread-local message is available from qk_last_error(). The Python mirror
@@ -73,6 +76,19 @@ int qk_create(int n, int r, int b, int device, qk_sim** out);
 /* Multi-process shard: this process owns ranks [rank_lo, rank_lo + count),
  * count a power of two dividing 2^r, held contiguously on `device`. */
 int qk_create_shard(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out);
+
+/* One process, several GPUs (the reference's single-process Simulator for
+ * states larger than one device, simulator.py:422-447, cli.py:154-172): the
+ * 2^r rank partitions are split over ndev devices (a power of two <= 2^r;
+ * devs may repeat an id, which puts several members on one device). Member k
+ * holds ranks [k*2^r/ndev, (k+1)*2^r/ndev) on devs[k]; the members reach each
+ * other's HBM through peer access (NVLink), and a CSQS whose rank bits cross
+ * members is a direct peer-memory exchange between device-side barriers. One
+ * host thread drives all devices (a stream per device). Every other entry
+ * point accepts the returned handle like a single-device one; qk_kernel_stats
+ * reports member 0 (all members run the same passes) and qk_mark_elapsed the
+ * slowest device. */
+int qk_create_multi(int n, int r, int b, const int* devs, int ndev, qk_sim** out);
 
 int qk_destroy(qk_sim* sim);
 

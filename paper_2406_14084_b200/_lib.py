@@ -37,6 +37,7 @@ _SIGS = {
     "qk_device_count": (c_int, [P(c_int)]),
     "qk_create": (c_int, [c_int, c_int, c_int, c_int, P(c_void)]),
     "qk_create_shard": (c_int, [c_int, c_int, c_int, c_int, c_int, c_int, P(c_void)]),
+    "qk_create_multi": (c_int, [c_int, c_int, c_int, P(c_int), c_int, P(c_void)]),
     "qk_destroy": (c_int, [c_void]),
     "qk_reset": (c_int, [c_void]),
     "qk_layout": (c_int, [c_void, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int)]),
@@ -210,14 +211,19 @@ def csqs_plan(n: int, r: int, count: int, shard: int, local_set, rank_set):
 class Handle:
     """Owner of one qk_sim*; frees the device state when garbage collected."""
 
-    def __init__(self, n: int, r: int, b: int, device: int = 0, rank_lo: int = 0, count: int = 0):
+    def __init__(self, n: int, r: int, b: int, device: int = 0, rank_lo: int = 0, count: int = 0,
+                 devices=None):
         self.ptr = c_void(None)
         L = lib()
-        if count:
+        self.devices = tuple(devices) if devices else (device,)
+        if devices and len(devices) > 1:
+            devs = (c_int * len(devices))(*devices)
+            check(L.qk_create_multi(n, r, b, devs, len(devices), ctypes.byref(self.ptr)))
+        elif count:
             check(L.qk_create_shard(n, r, b, device, rank_lo, count, ctypes.byref(self.ptr)))
         else:
             check(L.qk_create(n, r, b, device, ctypes.byref(self.ptr)))
-        self.n, self.r, self.b, self.device = n, r, b, device
+        self.n, self.r, self.b, self.device = n, r, b, self.devices[0]
         self.rank_lo = rank_lo
         self.count = count or (1 << r)
         self.local = n - r

@@ -19,6 +19,12 @@
 
 namespace qk {
 
+// Function attributes (max dynamic shared memory, ...) are per device: a
+// launcher sets them once for every device it runs on (one process may drive
+// several GPUs, qk_create_multi). Returns true the first time for the
+// current device.
+bool first_on_device(unsigned long long* mask);
+
 constexpr int kMaxC = 13;        // 2^13 complex128 = 128 KiB of shared memory per CTA
 constexpr int kMaxM = 4;         // register qubits per thread (16 amplitudes)
 constexpr int kMaxOuter = 48;    // address bits outside the chunk
@@ -237,6 +243,10 @@ int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p,
                      int np, const int* a, const int* b, int k, CUstream_st* stream);
 int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* stream);
 int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int npos, CUstream_st* stream);
+int preload_exchange_kernels();  // force-load (lazy loading) every kernel an exchange step launches
+// device-side barrier of the shards of one exchange (flag arrays in peer memory)
+int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx, int n, int me,
+                        unsigned long long epoch, int* err, CUstream_st* stream);
 // sum of n partials (fused-norm readback of the last pass)
 int launch_sum_final(const double* partial, int n, double* out, CUstream_st* stream);
 int launch_sumsq(const double* state, uint64_t n_amps, double* d_partial, double* d_out,

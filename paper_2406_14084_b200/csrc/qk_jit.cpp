@@ -24,6 +24,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <set>
 #include <mutex>
 #include <sstream>
 #include <string>
@@ -998,6 +999,17 @@ int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, i
   if (smem < 0) return -1;
   const int threads = 32 + (1 << (C - M)) * ng;
   const uint64_t grid = nchunks < (uint64_t)num_sms ? nchunks : (uint64_t)num_sms;
+  {  // library kernels take their function attributes per device
+    static std::mutex mu;
+    static std::set<std::pair<void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({kern, dev}).second) {
+      cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaGetLastError();
+    }
+  }
   void* args[] = {const_cast<void*>(params)};
   cudaError_t e = cudaLaunchKernel((const void*)kern, dim3((unsigned)grid), dim3(threads), args, smem,
                                    reinterpret_cast<cudaStream_t>(stream));

@@ -21,6 +21,14 @@
 
 namespace qk {
 
+bool first_on_device(unsigned long long* mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const unsigned long long bit = 1ull << dev;
+  const unsigned long long old = __atomic_fetch_or(mask, bit, __ATOMIC_ACQ_REL);
+  return !(old & bit);
+}
+
 // ---------------------------------------------------------------------------
 // helpers
 
@@ -224,15 +232,14 @@ int launch_block_pass(double* state, const PassDesc* h, const PassDesc* d_pass,
   const int C = h->C, M = h->M;
   const unsigned threads = 1u << (C - M);
   const size_t smem = h->nphases > 1 ? ((size_t)16 << C) : 0;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static unsigned long long attr_set = 0;
+  if (first_on_device(&attr_set)) {
     const int mx = 16 << kMaxC;
     cudaFuncSetAttribute(k_block_pass<1, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_block_pass<2, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_block_pass<3, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_block_pass<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_block_pass<4, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr_set = true;
   }
   const uint64_t total = h->ncta;
   const uint64_t max_grid = 1ull << 30;
@@ -560,11 +567,9 @@ int launch_sqs(double* state, const SqsDesc* h, const SqsDesc* /*d*/, CUstream_s
   if (!getenv("QK_SQS_REG")) {
     const uint64_t units = 1ull << h->nouter;
     const size_t smem = (size_t)2 * (16u << h->nv);
-    static bool attr2 = false;
-    if (!attr2) {
+    static unsigned long long attr2 = 0;
+    if (first_on_device(&attr2))
       cudaFuncSetAttribute(k_sqs_async, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (16 << 10));
-      attr2 = true;
-    }
     // oversubscribed like k_sqs_oop (7 fit per SM): QAOA33r3's SQS 2.48 -> 2.32 s
     static const int per_sm = getenv("QK_SQS_CTAS") ? atoi(getenv("QK_SQS_CTAS")) : 64;
     uint64_t grid = 148ull * per_sm;
@@ -629,14 +634,81 @@ int launch_sqs_range(double* state, uint64_t start, uint64_t stop, const int* p,
 // ---------------------------------------------------------------------------
 // segment exchange (either pointer may be a peer mapping over NVLink)
 
-__global__ void k_swap_seg(double2* __restrict__ a, double2* __restrict__ b, uint64_t n) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const double2 x = ld_g(a + i);
-    const double2 y = ld_g(b + i);
-    st_g(a + i, y);
-    st_g(b + i, x);
+// Segment exchange. Every thread keeps 4 independent 16-B loads of each side
+// in flight before it stores (the remote side is NVLink peer memory, ~2 us
+// away): the grid needs ~1.8 MB in flight to fill a 900 GB/s link.
+constexpr int kSwapUnroll = 4;
+
+__global__ void __launch_bounds__(256) k_swap_seg(double2* __restrict__ a, double2* __restrict__ b, uint64_t n) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * kSwapUnroll) {
+    double2 x[kSwapUnroll], y[kSwapUnroll];
+#pragma unroll
+    for (int u = 0; u < kSwapUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n) {
+        x[u] = ld_g(a + i);
+        y[u] = ld_g(b + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSwapUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < n) {
+        st_g(a + i, y[u]);
+        st_g(b + i, x[u]);
+      }
+    }
   }
+}
+
+// Device-side barrier between the shards of one exchange (no host round
+// trip): shard `me` publishes `epoch` into slot `me` of every peer's flag
+// array (system-scope release), then waits until each peer has published it
+// into its own array. Stream order puts every earlier kernel of this shard
+// before the release. A peer that never arrives (dead process) trips a 60-s
+// timeout that sets *err instead of hanging the GPU.
+struct PeerFlags {
+  int32_t n, me;
+  int32_t idx[64];
+  unsigned long long* remote[64];  // peer idx[k]'s flag array (mapped over NVLink / IPC)
+};
+
+__global__ void k_peer_barrier(unsigned long long* __restrict__ mine, const __grid_constant__ PeerFlags pf,
+                               unsigned long long epoch, int* __restrict__ err) {
+  const int k = threadIdx.x;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  if (k < pf.n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.remote[k] + pf.me), "l"(epoch) : "memory");
+  if (k < pf.n) {
+    unsigned long long t0, t, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + pf.idx[k]) : "memory");
+      if (v >= epoch) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 60000000000ull) {
+        atomicExch(err, 1);
+        break;
+      }
+      __nanosleep(200);
+    }
+  }
+  __syncwarp();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx, int n, int me,
+                        unsigned long long epoch, int* err, CUstream_st* stream) {
+  if (n > 64 || n < 0) return -1;
+  PeerFlags pf{};
+  pf.n = n;
+  pf.me = me;
+  for (int k = 0; k < n; ++k) {
+    pf.idx[k] = idx[k];
+    pf.remote[k] = remote[k];
+  }
+  k_peer_barrier<<<1, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(mine, pf, epoch, err);
+  return (int)cudaGetLastError();
 }
 
 // Strided segment exchange: element t of the segment sits at
@@ -647,15 +719,29 @@ struct SwapRuns {
   uint8_t src[24], dst[24], len[24];
 };
 
-__global__ void k_swap_strided(double2* __restrict__ a, double2* __restrict__ b, uint64_t n,
-                               const __grid_constant__ SwapRuns R) {
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t off = 0;
-    for (int k = 0; k < R.n; ++k) off |= ((t >> R.src[k]) & ((1ull << R.len[k]) - 1)) << R.dst[k];
-    const double2 x = ld_g(a + off);
-    const double2 y = ld_g(b + off);
-    st_g(a + off, y);
-    st_g(b + off, x);
+__global__ void __launch_bounds__(256) k_swap_strided(double2* __restrict__ a, double2* __restrict__ b, uint64_t n,
+                                                      const __grid_constant__ SwapRuns R) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < n; t0 += stride * kSwapUnroll) {
+    double2 x[kSwapUnroll], y[kSwapUnroll];
+    uint64_t off[kSwapUnroll];
+#pragma unroll
+    for (int u = 0; u < kSwapUnroll; ++u) {
+      const uint64_t t = t0 + u * stride;
+      off[u] = 0;
+      for (int k = 0; k < R.n; ++k) off[u] |= ((t >> R.src[k]) & ((1ull << R.len[k]) - 1)) << R.dst[k];
+      if (t < n) {
+        x[u] = ld_g(a + off[u]);
+        y[u] = ld_g(b + off[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kSwapUnroll; ++u) {
+      if (t0 + u * stride < n) {
+        st_g(a + off[u], y[u]);
+        st_g(b + off[u], x[u]);
+      }
+    }
   }
 }
 
@@ -674,16 +760,30 @@ int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int np
     k = e;
   }
   const uint64_t blocks = (n + 255) / 256;
-  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  const unsigned grid = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
   k_swap_strided<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), n, R);
   return (int)cudaGetLastError();
 }
 
+// With lazy module loading (the CUDA 12 default) the first launch of a kernel
+// loads it, and a load may wait for the kernels running on the device. A
+// member enqueueing its first swap while its own barrier kernel already spins
+// for a member the host has not reached yet would then deadlock. Every kernel
+// an exchange step launches is therefore loaded when the handle is created.
+int preload_exchange_kernels() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {(const void*)k_peer_barrier, (const void*)k_swap_seg, (const void*)k_swap_strided,
+                       (const void*)k_sqs, (const void*)k_sqs_async, (const void*)k_sqs_oop};
+  for (const void* f : fns)
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return (int)cudaGetLastError();
+  return 0;
+}
+
 int launch_swap_segments(double* a, double* b, uint64_t n, CUstream_st* stream) {
   if (!n) return 0;
   const uint64_t blocks = (n + 255) / 256;
-  const unsigned grid = (unsigned)(blocks < 148 * 16 ? blocks : 148 * 16);
+  const unsigned grid = (unsigned)(blocks < 148 * 8 ? blocks : 148 * 8);
   k_swap_seg<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), n);
   return (int)cudaGetLastError();
@@ -848,11 +948,8 @@ int overlap_scratch_bytes() { return (4096 + kOvBlocks + 1) * 16; }
 
 int launch_overlap(const double* state, uint64_t n, const double* d_tabs, double* d_work, CUstream_st* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * 16);
   double2* part = reinterpret_cast<double2*>(d_work);
   k_overlap<<<kOvBlocks, 256, 4096 * 16, st>>>(reinterpret_cast<const double2*>(state), n,
                                                reinterpret_cast<const double2*>(d_tabs), part);

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <complex>
 #include <deque>
+#include <map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1256,7 +1257,20 @@ struct qk_sim {
   std::vector<double*> peers;   // by shard index: the peer's bufs[0]
   std::vector<double*> peers1;  // the peer's bufs[1] (double-buffered shards)
   int nshards = 1, shard = 0;
+  // device-side exchange barrier: flag array behind bufs[0] (one slot per
+  // shard), the peers' arrays through their mappings, and a per-handle epoch
+  // (every shard runs the same exchanges, so the epochs agree)
+  unsigned long long* flags = nullptr;
+  std::vector<unsigned long long*> peer_flags;
+  unsigned long long epoch = 0;
+  int* d_err = nullptr;
+  bool ipc_mapped = false;     // peers[] came from cudaIpcOpenMemHandle (closed at destroy)
+  // group handle (qk_create_multi): one member shard per device, this
+  // handle owns them and holds no state of its own
+  std::vector<qk_sim*> members;
 };
+
+constexpr size_t kFlagBytes = 4096;  // 64 shards x 8 B, padded
 
 namespace {
 
@@ -2512,6 +2526,11 @@ int compile_program(qk_sim* s) {
       } else {
         ip.sqs = -2;  // cross-process exchange over the current layout (strided segments)
         ip.xlay = sigma;
+        {  // algorithmic NVLink bytes sent by this shard: 16 B x 2^L x (1 - 2^-S) per partition
+          int so = 0;
+          for (int q : ins.b) so += q - s->L >= held_rank_bits;
+          ip.bytes = 16.0 * std::ldexp(1.0, s->L) * s->count * (1.0 - std::ldexp(1.0, -so));
+        }
         bool id = true;
         for (int q = 0; q < nb; ++q) id = id && sigma[q] == q;
         if (!id && !strided_x) {
@@ -2720,7 +2739,7 @@ struct Seg {
 
 int csqs_plan(int n, int r, int count, int shard, const std::vector<int>& local_set,
               const std::vector<int>& rank_set, std::vector<Seg>& segs, std::vector<int>& in_a,
-              std::vector<int>& in_b) {
+              std::vector<int>& in_b, std::vector<int>* group = nullptr) {
   const int L = n - r;
   const int held = __builtin_ctz((unsigned)count);
   std::vector<int> loc = local_set, rk = rank_set;
@@ -2746,6 +2765,13 @@ int csqs_plan(int n, int r, int count, int shard, const std::vector<int>& local_
   const uint64_t run = part >> so;
   int x = 0;
   for (int k = 0; k < so; ++k) x |= ((shard >> sbit[k]) & 1) << k;
+  if (group)
+    for (int y = 0; y < (1 << so); ++y) {  // every shard this one exchanges with (symmetric)
+      if (y == x) continue;
+      int peer = shard;
+      for (int k = 0; k < so; ++k) peer = (peer & ~(1 << sbit[k])) | (((y >> k) & 1) << sbit[k]);
+      group->push_back(peer);
+    }
   for (int pi = 0; pi < count; ++pi) {
     for (int y = 0; y < (1 << so); ++y) {
       if (y == x) continue;
@@ -2772,16 +2798,36 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   if (s->nshards <= 1 || (int)s->peers.size() < s->nshards)
     return fail(QK_ESIM, "cross-rank swap needs the peer shards' state (qk_ipc_open)");
   std::vector<Seg> segs;
-  std::vector<int> in_a, in_b;
-  int rc = csqs_plan(s->n, s->r, s->count, s->shard, ip.a, ip.b, segs, in_a, in_b);
+  std::vector<int> in_a, in_b, group;
+  int rc = csqs_plan(s->n, s->r, s->count, s->shard, ip.a, ip.b, segs, in_a, in_b, &group);
   if (rc) return rc;
   for (auto& sg : segs)
     if (!(s->cur ? s->peers1 : s->peers)[sg.peer])
       return fail(QK_ESIM, "peer shard %d not mapped (qk_ipc_open)", (int)sg.peer);
-  if (s->barrier) {
+  // Device-side barrier (default): the shards of the exchange group meet on
+  // flags in each other's memory, stream-ordered; the host never waits. The
+  // host-callback barrier (two stream syncs + two host barriers) stays as a
+  // debugging fallback (QK_HOST_BARRIER).
+  bool dev_bar = !getenv("QK_HOST_BARRIER");
+  std::vector<unsigned long long*> rflags;
+  for (int p : group) {
+    if (!s->peer_flags[p]) dev_bar = false;
+    rflags.push_back(s->peer_flags[p]);
+  }
+  if (!dev_bar && !s->barrier) return fail(QK_ESIM, "cross-rank swap needs a barrier between the shards");
+  auto meet = [&]() -> int {
+    if (dev_bar) {
+      if (launch_peer_barrier(s->flags, rflags.data(), group.data(), (int)group.size(), s->shard, ++s->epoch,
+                              s->d_err, (CUstream_st*)s->stream))
+        return fail(QK_ECUDA, "peer barrier launch failed");
+      return QK_OK;
+    }
     CUDA_TRY(cudaStreamSynchronize(s->stream));
     if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
-  }
+    return QK_OK;
+  };
+  rc = meet();
+  if (rc) return rc;
   const bool ident_lay = ip.xlay.empty() || lay_identity(ip.xlay);
   auto lay_of = [&](uint64_t i) {
     if (ident_lay) return i;
@@ -2807,10 +2853,8 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
     }
     if (rc) return fail(QK_ECUDA, "peer exchange failed");
   }
-  if (s->barrier) {
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
-    if (s->barrier(s->barrier_ctx)) return fail(QK_ESIM, "barrier callback failed");
-  }
+  rc = meet();
+  if (rc) return rc;
   if (!in_a.empty()) {
     HostPlan tmp;
     if (!ident_lay) {  // in-shard pairs act on the bits' current positions
@@ -2829,8 +2873,16 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
     }
     rc = launch_sqs(s->state, &tmp.sqs[0], nullptr, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "in-shard swap failed");
-    CUDA_TRY(cudaStreamSynchronize(s->stream));
   }
+  return QK_OK;
+}
+
+// after a synchronize: did a peer barrier time out?
+int check_peer_error(qk_sim* s) {
+  if (!s->d_err || s->nshards <= 1) return QK_OK;
+  int e = 0;
+  CUDA_TRY(cudaMemcpy(&e, s->d_err, sizeof e, cudaMemcpyDeviceToHost));
+  if (e) return fail(QK_ESIM, "a peer shard did not reach the exchange barrier within 60 s");
   return QK_OK;
 }
 
@@ -2874,7 +2926,7 @@ uint64_t lay_addr(const qk_sim* s, uint64_t i) {
   return j;
 }
 
-int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out) {
+int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_sim** out, int second = -1) {
   if (!out) return fail(QK_EINVAL, "null output handle");
   *out = nullptr;
   if (n < 0 || r < 0 || r > n) return fail(QK_EINVAL, "need 0 <= R <= N, got R=%d, N=%d", r, n);
@@ -2903,7 +2955,7 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   s->amps = (size_t)1 << nbits;
   s->nshards = (1 << r) / count;
   s->shard = rank_lo / count;
-  cudaError_t e = cudaMalloc(&s->bufs[0], need);
+  cudaError_t e = cudaMalloc(&s->bufs[0], need + kFlagBytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     delete s;
@@ -2914,7 +2966,8 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   for (int q = 0; q < nbits; ++q) s->lay[q] = q;
   s->lay_final = s->lay;
   // second buffer for out-of-place fused block+SQS passes when it fits comfortably
-  if (!getenv("QK_INPLACE") && 2.0 * (double)need <= 0.90 * (double)free_b) {
+  // (second: -1 decide here, 0 never, 1 always — a group decides for all its members)
+  if (second != 0 && !getenv("QK_INPLACE") && (second == 1 || 2.0 * (double)need <= 0.90 * (double)free_b)) {
     if (cudaMalloc(&s->bufs[1], need) != cudaSuccess) {
       cudaGetLastError();
       s->bufs[1] = nullptr;
@@ -2924,6 +2977,11 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   CUDA_TRY(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaMalloc(&s->d_partial, 148 * 8 * sizeof(double) + 256));
   CUDA_TRY(cudaMalloc(&s->d_nrm, 4096 * sizeof(double)));
+  if (preload_exchange_kernels()) return fail(QK_ECUDA, "kernel preload failed");
+  CUDA_TRY(cudaMalloc(&s->d_err, 256));
+  CUDA_TRY(cudaMemsetAsync(s->d_err, 0, 256, s->stream));
+  s->flags = (unsigned long long*)((char*)s->bufs[0] + need);
+  CUDA_TRY(cudaMemsetAsync(s->flags, 0, kFlagBytes, s->stream));
   s->d_scalar = s->d_partial + 148 * 8;
   int rc = launch_fill_zero_one(s->state, s->amps, rank_lo == 0, (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "state init failed");
@@ -2932,6 +2990,8 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   s->peers1.assign(s->nshards, nullptr);
   s->peers[s->shard] = s->bufs[0];
   s->peers1[s->shard] = s->bufs[1];
+  s->peer_flags.assign(s->nshards, nullptr);
+  s->peer_flags[s->shard] = s->flags;
   *out = s;
   return QK_OK;
 }
@@ -2981,10 +3041,155 @@ std::vector<InstrH> unpack(const int32_t* w, size_t nw, const double* p, size_t 
   return out;
 }
 
+// ---- one run of the loaded program, in three steps (a group handle
+// interleaves its members' steps so that one host thread drives all GPUs)
+
+int run_prepare(qk_sim* s, size_t* first_exec) {
+  CUDA_TRY(cudaSetDevice(s->device));
+  int rc = materialize(s, true);  // the plan starts from the reference layout
+  if (rc) return rc;
+  s->fresh_saved = 0;
+  *first_exec = s->iplan.size();  // the instruction whose pass read the fresh state
+  return ensure_events(s, 2 * s->iplan.size() + 2);
+}
+
+int run_step(qk_sim* s, size_t i, size_t* first_exec) {
+  CUDA_TRY(cudaSetDevice(s->device));
+  CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
+  const bool was_fresh = s->fresh;
+  int rc = run_instr(s, s->iplan[i]);
+  if (rc) return rc;
+  if (was_fresh && !s->fresh && s->fresh_saved > 0) *first_exec = i;
+  CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
+  return QK_OK;
+}
+
+// after the steps: wait, check the exchanges, adopt the end layout and add
+// this run's per-class device times (ms) to cls and to the kernel stats
+int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
+  CUDA_TRY(cudaSetDevice(s->device));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  int rc = check_peer_error(s);
+  if (rc) return rc;
+  if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
+  s->norm_valid = s->norm_pass >= 0;
+  const size_t ni = s->iplan.size();
+  for (size_t i = 0; i < ni; ++i) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
+    const int c = s->iplan[i].type;
+    if (getenv("QK_DUMP_TIMES"))
+      fprintf(stderr, "instr %zu type %d pass0 %d passes %d permuted %d fused %d: %.3f ms\n", i, c, s->iplan[i].pass0, s->iplan[i].npass,
+              (int)s->iplan[i].permuted, (int)fused_away(s, s->iplan[i]), ms);
+    cls[c] += ms;
+    const InstrPlan& ip = s->iplan[i];
+    const bool xp = c == QK_INS_BLOCK && ip.npass > 0 && s->pass_tma[ip.pass0 + ip.npass - 1] >= 0 &&
+                    s->tma[s->pass_tma[ip.pass0 + ip.npass - 1]].xbits > 0;
+    const int sc = xp ? 3 : c;
+    s->stat_ms[sc] += ms;
+    if (fused_away(s, ip)) continue;
+    s->stat_bytes[sc] += ip.bytes - (i == first_exec ? s->fresh_saved : 0.0);
+    s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
+  }
+  return QK_OK;
+}
+
+bool is_group(const qk_sim* s) { return s && !s->members.empty(); }
+
+// Group handle (qk_create_multi): member k holds ranks [k*cnt, (k+1)*cnt) on
+// its device; members reach each other's HBM directly (peer access over
+// NVLink), so a cross-member CSQS is the same exchange as between processes,
+// with the device-side barrier and no host round trip. The host enqueues
+// instruction i on every member before instruction i+1 on any, so a member's
+// exchange barrier never waits on work that is not yet enqueued.
+int group_run(qk_sim* g, double* timings) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t nm = g->members.size();
+  std::vector<size_t> first(nm, 0);
+  for (size_t k = 0; k < nm; ++k) {
+    int rc = run_prepare(g->members[k], &first[k]);
+    if (rc) return rc;
+  }
+  const size_t ni = g->members[0]->iplan.size();
+  for (size_t i = 0; i < ni; ++i)
+    for (size_t k = 0; k < nm; ++k) {
+      int rc = run_step(g->members[k], i, &first[k]);
+      if (rc) return rc;
+    }
+  double cls[3] = {0, 0, 0};
+  for (size_t k = 0; k < nm; ++k) {
+    double ck[3] = {0, 0, 0};
+    int rc = run_finish(g->members[k], first[k], ck);
+    if (rc) return rc;
+    for (int c = 0; c < 3; ++c) cls[c] = std::max(cls[c], ck[c]);  // max over devices
+  }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (timings) {
+    timings[0] = cls[0] * 1e-3;
+    timings[1] = cls[1] * 1e-3;
+    timings[2] = cls[2] * 1e-3;
+    timings[3] = wall;
+  }
+  return QK_OK;
+}
+
+// cross_rank_swap on a group handle: enqueue every member's exchange before
+// waiting on any (each one's device barrier waits for the others)
+int group_csqs(qk_sim* g, const int32_t* local_set, const int32_t* rank_set, int S) {
+  std::vector<int> a(local_set, local_set + S), b(rank_set, rank_set + S);
+  for (qk_sim* m : g->members) {
+    CUDA_TRY(cudaSetDevice(m->device));
+    int rc = materialize(m);
+    if (rc) return rc;
+    rc = check_csqs(m, a, b);
+    if (rc) return rc;
+  }
+  if (S == 0) return QK_OK;
+  qk_sim* m0 = g->members[0];
+  const int held = m0->nbits - m0->L;
+  bool local_only = true;
+  for (int q : b)
+    if (q - m0->L >= held) local_only = false;
+  if (local_only) {
+    for (qk_sim* m : g->members) {
+      int rc = qk_csqs(m, local_set, rank_set, S);
+      if (rc) return rc;
+    }
+    return QK_OK;
+  }
+  InstrPlan ip;
+  ip.type = QK_INS_CSQS;
+  ip.a = a;
+  ip.b = b;
+  ip.csqs_s = S;
+  for (qk_sim* m : g->members) {
+    CUDA_TRY(cudaSetDevice(m->device));
+    int rc = exchange_cross(m, ip);
+    if (rc) return rc;
+  }
+  for (qk_sim* m : g->members) {
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaStreamSynchronize(m->stream));
+    int rc = check_peer_error(m);
+    if (rc) return rc;
+  }
+  return QK_OK;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // C ABI
+
+// a group handle forwards the call to every member (in member order)
+#define QK_GROUP_ALL(call)                 \
+  if (is_group(s)) {                       \
+    for (qk_sim* m : s->members) {         \
+      int rc_ = (call);                    \
+      if (rc_) return rc_;                 \
+    }                                      \
+    return QK_OK;                          \
+  }
 
 extern "C" {
 
@@ -3010,17 +3215,101 @@ int qk_create_shard(int n, int r, int b, int device, int rank_lo, int count, qk_
   return create_common(n, r, b, device, rank_lo, count, out);
 }
 
+int qk_create_multi(int n, int r, int b, const int* devs, int ndev, qk_sim** out) {
+  if (!out) return fail(QK_EINVAL, "null output handle");
+  *out = nullptr;
+  if (!devs || ndev < 1 || (ndev & (ndev - 1))) return fail(QK_EINVAL, "device count %d must be a power of two", ndev);
+  if (r < 0 || r > 30 || ndev > (1 << r))
+    return fail(QK_EINVAL, "%d devices need at least log2(%d) rank qubits, got R=%d", ndev, ndev, r);
+  if (n - r < 0 || n > 62) return fail(QK_EINVAL, "need 0 <= R <= N, got R=%d, N=%d", r, n);
+  const int cnt = (1 << r) / ndev;
+  const int nbits = n - r + __builtin_ctz((unsigned)cnt);
+  const double need = std::ldexp(16.0, nbits);
+  // second buffers for every member or for none (the plans must agree): each
+  // device must hold 2 x (its members' states) within 90% of its free memory
+  int second = getenv("QK_INPLACE") ? 0 : 1;
+  std::map<int, int> per_dev;
+  for (int k = 0; k < ndev; ++k) per_dev[devs[k]]++;
+  for (auto& kv : per_dev) {
+    CUDA_TRY(cudaSetDevice(kv.first));
+    size_t free_b = 0, total_b = 0;
+    CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    if ((double)kv.second * need > 0.97 * (double)free_b)
+      return fail(QK_ENOMEM, "cannot allocate state: %.0f bytes required", std::ldexp(16.0, n));
+    if (2.0 * kv.second * need > 0.90 * (double)free_b) second = 0;
+  }
+  qk_sim* g = new qk_sim();
+  g->n = n;
+  g->r = r;
+  g->b = b;
+  g->device = devs[0];
+  g->rank_lo = 0;
+  g->count = 1 << r;
+  g->L = n - r;
+  g->nbits = n;
+  g->amps = (size_t)1 << n;
+  for (int k = 0; k < ndev; ++k) {
+    qk_sim* m = nullptr;
+    int rc = create_common(n, r, b, devs[k], k * cnt, cnt, &m, second);
+    if (rc) {
+      std::string msg = qk_last_error();
+      for (qk_sim* x : g->members) qk_destroy(x);
+      delete g;
+      return fail(rc, "%s", msg.c_str());
+    }
+    g->members.push_back(m);
+  }
+  // direct peer access between the members' devices (NVLink), then every
+  // member sees every other member's buffers and barrier flags
+  for (int a = 0; a < ndev; ++a)
+    for (int c = 0; c < ndev; ++c) {
+      if (devs[a] == devs[c]) continue;
+      int ok = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&ok, devs[a], devs[c]));
+      if (!ok) {
+        for (qk_sim* x : g->members) qk_destroy(x);
+        delete g;
+        return fail(QK_ECUDA, "device %d cannot access device %d (no peer path)", devs[a], devs[c]);
+      }
+      CUDA_TRY(cudaSetDevice(devs[a]));
+      cudaError_t e = cudaDeviceEnablePeerAccess(devs[c], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        for (qk_sim* x : g->members) qk_destroy(x);
+        delete g;
+        return fail(QK_ECUDA, "peer access %d -> %d: %s", devs[a], devs[c], cudaGetErrorString(e));
+      }
+      cudaGetLastError();
+    }
+  for (int a = 0; a < ndev; ++a)
+    for (int c = 0; c < ndev; ++c) {
+      g->members[a]->peers[c] = g->members[c]->bufs[0];
+      g->members[a]->peers1[c] = g->members[c]->bufs[1];
+      g->members[a]->peer_flags[c] = g->members[c]->flags;
+    }
+  *out = g;
+  return QK_OK;
+}
+
 int qk_destroy(qk_sim* s) {
   if (!s) return QK_OK;
+  if (is_group(s)) {
+    for (qk_sim* m : s->members) qk_destroy(m);
+    delete s;
+    return QK_OK;
+  }
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto e : s->events) cudaEventDestroy(e);
   for (auto e : s->marks)
     if (e) cudaEventDestroy(e);
-  for (size_t i = 0; i < s->peers.size(); ++i)
-    if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
-  for (size_t i = 0; i < s->peers1.size(); ++i)
-    if ((int)i != s->shard && s->peers1[i]) cudaIpcCloseMemHandle(s->peers1[i]);
+  if (s->ipc_mapped) {
+    for (size_t i = 0; i < s->peers.size(); ++i)
+      if ((int)i != s->shard && s->peers[i]) cudaIpcCloseMemHandle(s->peers[i]);
+    for (size_t i = 0; i < s->peers1.size(); ++i)
+      if ((int)i != s->shard && s->peers1[i]) cudaIpcCloseMemHandle(s->peers1[i]);
+  }
+  if (s->d_err) cudaFree(s->d_err);
   if (s->bufs[0]) cudaFree(s->bufs[0]);
   if (s->bufs[1]) cudaFree(s->bufs[1]);
   if (s->blob) cudaFree(s->blob);
@@ -3035,6 +3324,7 @@ int qk_destroy(qk_sim* s) {
 
 int qk_reset(qk_sim* s) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_reset(m));
   CUDA_TRY(cudaSetDevice(s->device));
   s->cur = 0;
   s->state = s->bufs[0];
@@ -3061,6 +3351,7 @@ int qk_layout(const qk_sim* s, int* n, int* r, int* b, int* rank_lo, int* count)
 
 int qk_load_text(qk_sim* s, const char* text, size_t len, int c, int* n_instr) {
   if (!s || (!text && len)) return fail(QK_EINVAL, "null argument");
+  QK_GROUP_ALL(qk_load_text(m, text, len, c, n_instr));
   CUDA_TRY(cudaSetDevice(s->device));
   Parser ps;
   ps.n = s->n;
@@ -3078,6 +3369,7 @@ int qk_load_text(qk_sim* s, const char* text, size_t len, int c, int* n_instr) {
 
 int qk_load_packed(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_load_packed(m, words, nwords, params, nparams));
   CUDA_TRY(cudaSetDevice(s->device));
   int rc;
   std::string emsg;
@@ -3114,6 +3406,7 @@ int qk_load_gate_by_gate(qk_sim* s, const int32_t* words, size_t nwords, const d
 
 int qk_program_info(const qk_sim* s, int* n_instr, int* n_blocks, int* n_sqs, int* n_csqs, int32_t* perm) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  if (is_group(s)) return qk_program_info(s->members[0], n_instr, n_blocks, n_sqs, n_csqs, perm);
   int nb = 0, ns = 0, nc = 0;
   for (auto& i : s->prog) {
     nb += i.type == QK_INS_BLOCK;
@@ -3131,50 +3424,25 @@ int qk_program_info(const qk_sim* s, int* n_instr, int* n_blocks, int* n_sqs, in
 
 int qk_set_profiling(qk_sim* s, int per_launch) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_set_profiling(m, per_launch));
   s->per_launch = per_launch;
   return QK_OK;
 }
 
 int qk_run(qk_sim* s, double* timings) {
   if (!s) return fail(QK_EINVAL, "null handle");
-  CUDA_TRY(cudaSetDevice(s->device));
-  int rc = materialize(s, true);  // the plan starts from the reference layout
-  if (rc) return rc;
-  s->fresh_saved = 0;
+  if (is_group(s)) return group_run(s, timings);
   const auto t0 = std::chrono::steady_clock::now();
-  const size_t ni = s->iplan.size();
-  rc = ensure_events(s, 2 * ni + 2);
+  size_t first_exec = 0;
+  int rc = run_prepare(s, &first_exec);
   if (rc) return rc;
-  size_t first_exec = ni;  // the instruction whose pass read the fresh state
-  for (size_t i = 0; i < ni; ++i) {
-    CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
-    const bool was_fresh = s->fresh;
-    rc = run_instr(s, s->iplan[i]);
+  for (size_t i = 0; i < s->iplan.size(); ++i) {
+    rc = run_step(s, i, &first_exec);
     if (rc) return rc;
-    if (was_fresh && !s->fresh && s->fresh_saved > 0) first_exec = i;
-    CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
   }
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
-  s->norm_valid = s->norm_pass >= 0;
   double cls[3] = {0, 0, 0};
-  for (size_t i = 0; i < ni; ++i) {
-    float ms = 0;
-    CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
-    const int c = s->iplan[i].type;
-    if (getenv("QK_DUMP_TIMES"))
-      fprintf(stderr, "instr %zu type %d pass0 %d passes %d permuted %d fused %d: %.3f ms\n", i, c, s->iplan[i].pass0, s->iplan[i].npass,
-              (int)s->iplan[i].permuted, (int)fused_away(s, s->iplan[i]), ms);
-    cls[c] += ms;
-    const InstrPlan& ip = s->iplan[i];
-    const bool xp = c == QK_INS_BLOCK && ip.npass > 0 && s->pass_tma[ip.pass0 + ip.npass - 1] >= 0 &&
-                    s->tma[s->pass_tma[ip.pass0 + ip.npass - 1]].xbits > 0;
-    const int sc = xp ? 3 : c;
-    s->stat_ms[sc] += ms;
-    if (fused_away(s, ip)) continue;
-    s->stat_bytes[sc] += ip.bytes - (i == first_exec ? s->fresh_saved : 0.0);
-    s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
-  }
+  rc = run_finish(s, first_exec, cls);
+  if (rc) return rc;
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   if (timings) {
     timings[0] = cls[0] * 1e-3;
@@ -3187,6 +3455,11 @@ int qk_run(qk_sim* s, double* timings) {
 
 int qk_kernel_stats(qk_sim* s, double* out, int reset) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  if (is_group(s)) {  // every member runs the same passes: report member 0 (one device), reset all
+    int rc = qk_kernel_stats(s->members[0], out, reset);
+    for (size_t k = 1; !rc && reset && k < s->members.size(); ++k) rc = qk_kernel_stats(s->members[k], nullptr, 1);
+    return rc;
+  }
   if (out)
     for (int c = 0; c < 3; ++c) {
       out[2 * c] = s->stat_ms[c];
@@ -3205,6 +3478,17 @@ int qk_kernel_stats(qk_sim* s, double* out, int reset) {
 
 int qk_sumsq(qk_sim* s, double* sumsq) {
   if (!s || !sumsq) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {
+    double acc = 0.0;
+    for (qk_sim* m : s->members) {
+      double v = 0.0;
+      int rc = qk_sumsq(m, &v);
+      if (rc) return rc;
+      acc += v;
+    }
+    *sumsq = acc;
+    return QK_OK;
+  }
   CUDA_TRY(cudaSetDevice(s->device));
   { int frc = ensure_full(s); if (frc) return frc; }
   // the run's last pass already summed what it stored (any later swap only permutes)
@@ -3219,6 +3503,11 @@ int qk_sumsq(qk_sim* s, double* sumsq) {
 
 int qk_read_physical(qk_sim* s, int part, uint64_t off, uint64_t count, double* reim) {
   if (!s || (!reim && count)) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {
+    const int cnt = s->members[0]->count;
+    if (part < 0 || part >= s->count) return fail(QK_EINVAL, "read outside partition");
+    return qk_read_physical(s->members[part / cnt], part % cnt, off, count, reim);
+  }
   const uint64_t psize = 1ull << s->L;
   if (part < 0 || part >= s->count || off + count > psize || off > psize)
     return fail(QK_EINVAL, "read outside partition");
@@ -3250,6 +3539,11 @@ int qk_read_physical(qk_sim* s, int part, uint64_t off, uint64_t count, double* 
 
 int qk_write_physical(qk_sim* s, int part, uint64_t off, uint64_t count, const double* reim) {
   if (!s || (!reim && count)) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {
+    const int cnt = s->members[0]->count;
+    if (part < 0 || part >= s->count) return fail(QK_EINVAL, "write outside partition");
+    return qk_write_physical(s->members[part / cnt], part % cnt, off, count, reim);
+  }
   const uint64_t psize = 1ull << s->L;
   if (part < 0 || part >= s->count || off + count > psize || off > psize)
     return fail(QK_EINVAL, "write outside partition");
@@ -3264,6 +3558,27 @@ int qk_write_physical(qk_sim* s, int part, uint64_t off, uint64_t count, const d
 
 int qk_gather(qk_sim* s, const uint64_t* idx, uint64_t count, double* reim) {
   if (!s || (count && (!idx || !reim))) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {  // split by owning member, gather, scatter back
+    std::vector<std::vector<uint64_t>> sel(s->members.size()), pos(s->members.size());
+    for (uint64_t i = 0; i < count; ++i) {
+      const uint64_t k = idx[i] >> s->members[0]->nbits;
+      if (k >= s->members.size()) return fail(QK_EINVAL, "index %llu not held by this handle", (unsigned long long)idx[i]);
+      sel[k].push_back(idx[i]);
+      pos[k].push_back(i);
+    }
+    std::vector<double> buf;
+    for (size_t k = 0; k < s->members.size(); ++k) {
+      if (sel[k].empty()) continue;
+      buf.resize(2 * sel[k].size());
+      int rc = qk_gather(s->members[k], sel[k].data(), sel[k].size(), buf.data());
+      if (rc) return rc;
+      for (size_t j = 0; j < sel[k].size(); ++j) {
+        reim[2 * pos[k][j]] = buf[2 * j];
+        reim[2 * pos[k][j] + 1] = buf[2 * j + 1];
+      }
+    }
+    return QK_OK;
+  }
   if (!count) return QK_OK;
   const uint64_t lo = (uint64_t)s->rank_lo << s->L;
   for (uint64_t i = 0; i < count; ++i)
@@ -3304,6 +3619,19 @@ int qk_read_logical(qk_sim* s, const int32_t* perm, const uint64_t* lidx, uint64
 
 int qk_overlap_product(qk_sim* s, const int32_t* perm, const double* factors, double* out) {
   if (!s || !factors || !out) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {
+    double acc[2] = {0.0, 0.0};
+    for (qk_sim* m : s->members) {
+      double v[2];
+      int rc = qk_overlap_product(m, perm, factors, v);
+      if (rc) return rc;
+      acc[0] += v[0];
+      acc[1] += v[1];
+    }
+    out[0] = acc[0];
+    out[1] = acc[1];
+    return QK_OK;
+  }
   std::vector<int> pm(s->n);
   for (int q = 0; q < s->n; ++q) pm[q] = perm ? perm[q] : q;
   {
@@ -3355,6 +3683,18 @@ int qk_overlap_product(qk_sim* s, const int32_t* perm, const double* factors, do
 
 int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64_t count, double* reim) {
   if (!s || !perm || (count && !reim)) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) {
+    if (s->n < 64 && (start + count > (1ull << s->n) || start > (1ull << s->n)))
+      return fail(QK_EINVAL, "logical range out of bounds");
+    std::vector<uint64_t> phys(count);
+    for (uint64_t i = 0; i < count; ++i) {
+      const uint64_t l = start + i;
+      uint64_t p = 0;
+      for (int q = 0; q < s->n; ++q) p |= ((l >> perm[q]) & 1ull) << q;
+      phys[i] = p;
+    }
+    return qk_gather(s, phys.data(), count, reim);
+  }
   if (s->count != (1 << s->r)) return fail(QK_EINVAL, "logical range readback needs the whole state");
   if (s->n < 64 && (start + count > (1ull << s->n) || start > (1ull << s->n)))
     return fail(QK_EINVAL, "logical range out of bounds");
@@ -3430,6 +3770,11 @@ int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t
 int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, const double* params,
                    size_t nparams, int c, uint64_t row_start, uint64_t row_stop) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  if (is_group(s)) {
+    const int cnt = s->members[0]->count;
+    if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
+    return qk_apply_block(s->members[part / cnt], part % cnt, words, nwords, params, nparams, c, row_start, row_stop);
+  }
   { int mrc = materialize(s); if (mrc) return mrc; }
   if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
   if (c < 1 || c > s->L) return fail(QK_EINVAL, "bad chunk width %d", c);
@@ -3488,6 +3833,7 @@ int qk_apply_block(qk_sim* s, int part, const int32_t* words, size_t nwords, con
 
 int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_apply_gate_full(m, words, nwords, params, nparams));
   { int mrc = materialize(s); if (mrc) return mrc; }
   CUDA_TRY(cudaSetDevice(s->device));
   int rc;
@@ -3529,6 +3875,11 @@ int qk_apply_gate_full(qk_sim* s, const int32_t* words, size_t nwords, const dou
 int qk_sqs(qk_sim* s, int part, const int32_t* out_set, const int32_t* in_set, int k, int cl,
            uint64_t start, uint64_t stop) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  if (is_group(s)) {
+    const int cnt = s->members[0]->count;
+    if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
+    return qk_sqs(s->members[part / cnt], part % cnt, out_set, in_set, k, cl, start, stop);
+  }
   { int mrc = materialize(s); if (mrc) return mrc; }
   if (part < 0 || part >= s->count) return fail(QK_EINVAL, "bad partition %d", part);
   std::vector<int> a(out_set, out_set + k), b(in_set, in_set + k);
@@ -3571,6 +3922,7 @@ int qk_sqs(qk_sim* s, int part, const int32_t* out_set, const int32_t* in_set, i
 
 int qk_csqs(qk_sim* s, const int32_t* local_set, const int32_t* rank_set, int S) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  if (is_group(s)) return group_csqs(s, local_set, rank_set, S);
   { int mrc = materialize(s); if (mrc) return mrc; }
   std::vector<int> a(local_set, local_set + S), b(rank_set, rank_set + S);
   int rc = check_csqs(s, a, b);
@@ -3588,6 +3940,9 @@ int qk_csqs(qk_sim* s, const int32_t* local_set, const int32_t* rank_set, int S)
     if (q - s->L >= held) local_only = false;
   if (!local_only) {
     rc = exchange_cross(s, ip);
+    if (rc) return rc;
+    CUDA_TRY(cudaStreamSynchronize(s->stream));
+    rc = check_peer_error(s);
     if (rc) return rc;
   } else {
     HostPlan tmp;
@@ -3634,6 +3989,7 @@ int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set, c
 
 int qk_ipc_handle(qk_sim* s, void* handle128) {
   if (!s || !handle128) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) return fail(QK_EINVAL, "a multi-device handle maps its members itself");
   CUDA_TRY(cudaSetDevice(s->device));
   { int frc = ensure_full(s); if (frc) return frc; }
   unsigned char* out = static_cast<unsigned char*>(handle128);
@@ -3649,6 +4005,7 @@ int qk_ipc_handle(qk_sim* s, void* handle128) {
 
 int qk_ipc_open(qk_sim* s, int peer, const void* handle128) {
   if (!s || !handle128) return fail(QK_EINVAL, "null argument");
+  if (is_group(s)) return fail(QK_EINVAL, "a multi-device handle maps its members itself");
   if (peer < 0 || peer >= s->nshards) return fail(QK_EINVAL, "bad peer shard %d", peer);
   if (peer == s->shard) return QK_OK;
   CUDA_TRY(cudaSetDevice(s->device));
@@ -3666,6 +4023,8 @@ int qk_ipc_open(qk_sim* s, int peer, const void* handle128) {
     void* p = nullptr;
     CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     (b ? s->peers1 : s->peers)[peer] = (double*)p;
+    if (!b) s->peer_flags[peer] = (unsigned long long*)((char*)p + ((size_t)16 << s->nbits));
+    s->ipc_mapped = true;
   }
   return QK_OK;
 }
@@ -3679,6 +4038,7 @@ int qk_set_barrier(qk_sim* s, qk_barrier_fn fn, void* ctx) {
 
 int qk_mark(qk_sim* s, int slot) {
   if (!s || slot < 0 || slot >= 8) return fail(QK_EINVAL, "bad marker slot");
+  QK_GROUP_ALL(qk_mark(m, slot));
   CUDA_TRY(cudaSetDevice(s->device));
   if (!s->marks[slot]) CUDA_TRY(cudaEventCreate(&s->marks[slot]));
   CUDA_TRY(cudaEventRecord(s->marks[slot], s->stream));
@@ -3686,6 +4046,17 @@ int qk_mark(qk_sim* s, int slot) {
 }
 
 int qk_mark_elapsed(qk_sim* s, int a, int b, double* ms) {
+  if (is_group(s)) {  // the bracket of the slowest device
+    double mx = 0.0;
+    for (qk_sim* m : s->members) {
+      double v = 0.0;
+      int rc = qk_mark_elapsed(m, a, b, &v);
+      if (rc) return rc;
+      mx = std::max(mx, v);
+    }
+    *ms = mx;
+    return QK_OK;
+  }
   if (!s || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !s->marks[a] || !s->marks[b])
     return fail(QK_EINVAL, "bad marker slots");
   CUDA_TRY(cudaEventSynchronize(s->marks[b]));
@@ -3697,6 +4068,7 @@ int qk_mark_elapsed(qk_sim* s, int a, int b, double* ms) {
 
 int qk_sync(qk_sim* s) {
   if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_sync(m));
   CUDA_TRY(cudaSetDevice(s->device));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   return QK_OK;

@@ -174,11 +174,8 @@ int launch_sqs_bulk(double* state, const SqsDesc* h, int num_sms, CUstream_st* s
   if (stages > kStageMax) stages = kStageMax;
   if (stages < 2) return -2;
   const size_t smem = stages * stage_bytes + 2 * stages * 8;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sqs_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) cudaFuncSetAttribute(k_sqs_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   const uint64_t units = 1ull << h->nouter;
   const uint64_t grid = units < (uint64_t)num_sms ? units : (uint64_t)num_sms;
   k_sqs_bulk<<<(unsigned)grid, 32 * (1 + kConsumerWarps), smem, reinterpret_cast<cudaStream_t>(stream)>>>(

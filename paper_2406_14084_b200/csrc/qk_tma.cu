@@ -345,12 +345,11 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax) {
 }
 
 int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream) {
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;
+  if (first_on_device(&attr)) {
     cudaFuncSetAttribute(k_block_tma<4, 32 + kConsumers4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_block_tma<3, 32 + kConsumers3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_block_tma<4, 32 + 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
   }
   int ng = 0, st = 0;
   const int smem = tma_smem_bytes(p->C, p->M, &ng, &st, p->smax);

@@ -124,9 +124,36 @@ class SimConfig:                              # simulator.py:49-52
     workers_per_rank: int = 1
 
 
-def init_state(layout: LayoutParams, device: int = 0) -> list:
+def _device_list(layout: LayoutParams, device: int, devices):
+    """Devices for a state: `devices` if given, else $QK_DEVICES (e.g. "0,1,2,3";
+    an id may repeat), else None (one device; see _open_handle)."""
+    import os
+    if devices is None and os.environ.get("QK_DEVICES"):
+        devices = [int(x) for x in os.environ["QK_DEVICES"].split(",") if x.strip()]
+    return list(devices) if devices else None
+
+
+def _open_handle(layout: LayoutParams, device: int = 0, devices=None) -> _lib.Handle:
+    """One handle for the whole 2^N state. A state that does not fit `device`
+    is split over the visible GPUs (largest power of two <= min(#GPUs, 2^R)),
+    one host thread driving them all, like the reference's single-process
+    Simulator over 2^R ranks (simulator.py:422-447)."""
+    devs = _device_list(layout, device, devices)
+    if devs and len(devs) > 1:
+        return _lib.Handle(layout.n, layout.r, layout.b, devices=devs)
+    try:
+        return _lib.Handle(layout.n, layout.r, layout.b, devs[0] if devs else device)
+    except SimulationError:
+        ndev = min(_lib.device_count(), 1 << layout.r)
+        k = 1 << (ndev.bit_length() - 1) if ndev > 0 else 0
+        if devs or k < 2:
+            raise
+        return _lib.Handle(layout.n, layout.r, layout.b, devices=list(range(k)))
+
+
+def init_state(layout: LayoutParams, device: int = 0, devices=None) -> list:
     """simulator.py:62-74 — |0...0> split across 2^R partitions, resident in HBM."""
-    h = _lib.Handle(layout.n, layout.r, layout.b, device)
+    h = _open_handle(layout, device, devices)
     return [StatePartition(r, DeviceAmps(h, r)) for r in range(layout.num_ranks)]
 
 
@@ -386,15 +413,19 @@ class SimResult:                              # simulator.py:383-407
 class Simulator:
     """Executes optimized instruction streams on a B200 (simulator.py:422-569).
 
-    All 2^R simulated ranks live contiguously in one HBM allocation;
-    `workers_per_rank` is accepted for API parity and has no effect on the
-    result (the reference guarantees bit-identical output for any value).
+    All 2^R simulated ranks live contiguously in one HBM allocation, or, when
+    the state does not fit one GPU (or `devices` / $QK_DEVICES name several),
+    split over several GPUs driven by this one process (qk_create_multi;
+    cross-GPU CSQS over NVLink peer memory). `workers_per_rank` is accepted for
+    API parity and has no effect on the result (the reference guarantees
+    bit-identical output for any value).
     """
 
-    def __init__(self, layout: LayoutParams, workers_per_rank: int = 1, device: int = 0):
+    def __init__(self, layout: LayoutParams, workers_per_rank: int = 1, device: int = 0,
+                 devices=None):
         self.layout = layout
         self.workers_per_rank = max(1, int(workers_per_rank))
-        self._h = _lib.Handle(layout.n, layout.r, layout.b, device)
+        self._h = _open_handle(layout, device, devices)
         self.partitions = [StatePartition(r, DeviceAmps(self._h, r))
                            for r in range(layout.num_ranks)]
         self._program = None

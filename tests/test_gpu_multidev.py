@@ -1,0 +1,120 @@
+"""GPU: one process driving several devices through one handle (qk_create_multi,
+the reference's single-process Simulator over 2^R ranks, simulator.py:422-447).
+
+The box has one B200, so the members are placed on the SAME device
+(devices=[0, 0] / [0, 0, 0, 0]): every member still owns its own allocation,
+stream, plan and barrier flags, the exchanges still read and write the other
+member's memory through its pointer, and the device-side barrier still orders
+the members' streams. Only the NVLink link speed is not exercised.
+
+Parity: random instruction streams against the CPU oracle (permutations
+bit-exact, amplitudes <= 1e-10), cross_rank_swap on the group partitions
+bit-exact against the oracle, and the 33-qubit R=1 QFT/BV/H circuits (two
+2^32-amplitude members, in place) against their analytic product states
+through the device-side fidelity (>= 1 - 1e-12).
+"""
+import gc
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from oracle import quokka_oracle as orc
+from paper_2406_14084_b200 import (CrossRankSwap, LayoutParams, OptimizedCircuit, SimConfig,
+                                   Simulator, cross_rank_swap, init_state, serialize_optimized)
+from test_gpu_parity import _random_stream
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.mark.parametrize("mode", ["default", "inplace", "interp"])
+@pytest.mark.parametrize("seed", range(8))
+def test_group_random_streams_vs_oracle(gpu, seed, mode):
+    env = {"inplace": {"QK_INPLACE": "1", "QK_JIT": "0"}, "interp": {"QK_JIT": "99"}}.get(mode, {})
+    os.environ.update(env)
+    try:
+        rng = np.random.default_rng(4100 + seed)
+        n = int(rng.integers(6, 15))
+        r = int(rng.integers(1, 4))
+        L = n - r
+        c = int(rng.integers(1, min(L, 12) + 1))
+        layout = LayoutParams(n=n, c=L, r=r, cl=min(2, L), b=L)
+        ins = ()
+        while not any(isinstance(i, CrossRankSwap) for i in ins):
+            ins = _random_stream(rng, n, r, c, int(rng.integers(4, 16)))
+        text = serialize_optimized(OptimizedCircuit(n, layout, ins))
+        want, perm, _ = orc.simulate_text(text, n, L, r=r, b=L)
+        for ndev in sorted({2, min(4, 1 << r)}):
+            sim = Simulator(layout, devices=[0] * ndev)
+            res = sim.run(ins)
+            assert tuple(res.final_permutation) == perm
+            err = float(np.max(np.abs(res.physical_vector() - want)))
+            assert err <= TOL, (seed, mode, ndev, n, r, c, err)
+            assert abs(res.norm() - np.linalg.norm(want)) <= 1e-12
+            # a second run on the same handle continues from the end layout
+            sim.reset()
+            again = sim.run(ins).physical_vector()
+            assert np.max(np.abs(again - want)) <= TOL
+            sim.release()
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+
+
+def test_group_cross_rank_swap_bit_exact(gpu):
+    rng = np.random.default_rng(12)
+    for n, r, s in ((8, 1, 1), (9, 2, 2), (10, 3, 1), (10, 3, 3), (11, 2, 1)):
+        L = n - r
+        layout = LayoutParams(n=n, c=1, r=r, cl=0, b=L)
+        v = np.arange(1 << n).astype(np.complex128)
+        rank = tuple(int(x) for x in np.sort(rng.choice(np.arange(L, n), size=s, replace=False)))
+        local = tuple(range(L - s, L))
+        for ndev in sorted({2, min(4, 1 << r)}):
+            parts = init_state(layout, devices=[0] * ndev)
+            for k, p in enumerate(parts):
+                p.amps[:] = v[k << L:(k + 1) << L]
+            cross_rank_swap(parts, local, rank, layout)
+            got = np.concatenate([np.asarray(p.amps) for p in parts])
+            ref = [v[k << L:(k + 1) << L].copy() for k in range(1 << r)]
+            orc.cross_rank_swap(ref, local, rank, n, r, L)
+            assert np.array_equal(got, np.concatenate(ref)), (n, r, s, ndev)
+
+
+def _factors(name, n):
+    f = np.zeros((n, 2), dtype=np.complex128)
+    if name.startswith(("qft", "h")):
+        f[:] = 2 ** -0.5
+    else:
+        f[:, 0] = 1.0
+    return f
+
+
+@pytest.mark.parametrize("name", ["qft33_c10_r1", "bv33_c10_r1", "h33_c10_r1"])
+def test_group_33_qubits_two_members(gpu, name):
+    """Two 2^32-amplitude members (64 GiB each, in place) on one device: the
+    CSQS of the reference optimizer's R=1 stream exchange 32 GiB segments."""
+    n, r = 33, 1
+    text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
+    sim = Simulator(LayoutParams(n=n, c=n - r, r=r), devices=[0, 0])
+    perm = sim.load_text(text, 10)
+    sim.reset()
+    res = sim.run_loaded(perm)
+    f = _factors(name, n)
+    fid = res.fidelity_product(f)
+    rng = np.random.default_rng(3)
+    idx = np.unique(rng.integers(0, 1 << n, 4096, dtype=np.int64))
+    got = sim.handle.read_logical(res.final_permutation, idx.astype(np.uint64))
+    want = np.ones(idx.size, dtype=np.complex128)
+    for q in range(n):
+        want *= np.where((idx >> q) & 1, f[q, 1], f[q, 0])
+    st = sim.handle.stats()
+    print(f"\n  {name} on 2 members: 1-fidelity {1 - fid:.3e}, max err {np.max(np.abs(got - want)):.3e}, "
+          f"xrs {res.timings['xrs']:.4f} s over {int(st[5])} exchanges, {st[8] / 2**30:.1f} GiB sent")
+    assert fid >= 1 - 1e-12
+    assert np.max(np.abs(got - want)) <= TOL
+    assert st[5] >= 1 and st[8] > 0
+    sim.release()
+    del res, sim
+    gc.collect()

@@ -19,6 +19,12 @@ METRICS = [
     ("launch__block_size", "block"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("smsp__inst_executed.sum", "warp instructions"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit rate %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("l1tex__throughput.avg.pct_of_peak_sustained_active", "L1 throughput %"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("l1tex__t_bytes_pipe_lsu_mem_global_op_ld.sum", "global load bytes (L1)"),
+    ("l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum", "local (spill) load bytes"),
 ]
 
 
