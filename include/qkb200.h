@@ -64,6 +64,10 @@ typedef struct qk_sim qk_sim;
 
 /* library / device info */
 int qk_version(void);
+/* 1 when NVRTC is loadable: block passes of states >= 2^20 amplitudes are then
+ * specialised per structure at load time (diagonal folding, lazy layout). With
+ * 0 they run on the generic interpreter; the runtime warns once on stderr. */
+int qk_jit_available(void);
 const char* qk_last_error(void);
 int qk_device_count(int* count);
 

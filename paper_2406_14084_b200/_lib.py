@@ -33,6 +33,7 @@ BARRIER_FN = ctypes.CFUNCTYPE(c_int, c_void)
 
 _SIGS = {
     "qk_version": (c_int, []),
+    "qk_jit_available": (c_int, []),
     "qk_last_error": (ctypes.c_char_p, []),
     "qk_device_count": (c_int, [P(c_int)]),
     "qk_create": (c_int, [c_int, c_int, c_int, c_int, P(c_void)]),
@@ -130,6 +131,11 @@ def iptr(a: np.ndarray):
 
 def uptr(a: np.ndarray):
     return a.ctypes.data_as(P(c_u64))
+
+
+def jit_available() -> bool:
+    """NVRTC present: large-state passes are specialised at load (qk_jit_available)."""
+    return bool(lib().qk_jit_available())
 
 
 def device_count() -> int:

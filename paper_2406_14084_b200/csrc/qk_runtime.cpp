@@ -1679,6 +1679,14 @@ int upload_plan(qk_sim* s) {
   s->jit_blob.assign(hp.passes.size(), {});
   const char* jenv = getenv("QK_JIT");
   const int jit_min = jenv ? atoi(jenv) : 20;   // QK_JIT=<min address bits>; QK_NO_JIT disables
+  if (!jit_available() && !getenv("QK_NO_JIT") && s->nbits >= jit_min) {
+    static bool warned = false;
+    if (!warned)
+      fprintf(stderr,
+              "qkb200: NVRTC (libnvrtc.so.12) not found: the specialised block passes, diagonal folding and the "
+              "lazy layout are off; large states run on the generic interpreter (about 2x slower)\n");
+    warned = true;
+  }
   if (jit_available() && s->nbits >= jit_min) {
     const auto tj0 = std::chrono::steady_clock::now();
     std::vector<std::string> srcs;
@@ -3194,6 +3202,8 @@ int group_csqs(qk_sim* g, const int32_t* local_set, const int32_t* rank_set, int
 extern "C" {
 
 int qk_version(void) { return 1; }
+
+int qk_jit_available(void) { return jit_available() ? 1 : 0; }
 const char* qk_last_error(void) { return g_err.c_str(); }
 
 int qk_device_count(int* count) {

@@ -4,9 +4,11 @@ circuit.py:157-163). Gate blocks and SQS are shard-local; a CSQS whose rank
 bits cross shards is a peer-to-peer segment exchange over NVLink: every shard
 maps its peers' HBM state through CUDA IPC (qk_ipc_handle / qk_ipc_open) and
 the swap kernel reads and writes peer memory directly
-(qk_runtime.cpp: csqs_plan / exchange_cross). torch.distributed is plumbing
-only: the IPC handle all-gather, the barrier around each exchange, and the
-cross-shard reductions of the readback.
+(qk_runtime.cpp: csqs_plan / exchange_cross). The shards of an exchange meet
+on flags in each other's memory (a device-side barrier on the stream), so the
+host never waits inside a run. torch.distributed is plumbing only: the IPC
+handle all-gather and the cross-shard reductions of the readback. (The host
+barrier callback is registered too; it only runs under QK_HOST_BARRIER=1.)
 """
 from __future__ import annotations
 
@@ -48,6 +50,13 @@ class ShardedSimulator:
         self._cb = _lib.BARRIER_FN(self._barrier)
         _lib.check(_lib.lib().qk_set_barrier(self.h.ptr, self._cb, None))
         self.perm = tuple(range(n))
+
+    def close(self) -> None:
+        """Free this shard's state now. Collective: a peer's memory is only
+        released once every shard has closed its IPC mapping of it, so the
+        shards must all close before any of them allocates again."""
+        self.h.free()
+        self._dist.barrier(group=self.group)
 
     def _barrier(self, _ctx) -> int:
         try:
@@ -95,6 +104,19 @@ class ShardedSimulator:
 
     def norm(self) -> float:
         return math.sqrt(float(self._allreduce(np.array([self.h.sumsq()]))[0]))
+
+    def overlap_product(self, perm, factors) -> complex:
+        """<phi|psi> with a product state over logical qubits (qk_overlap_product),
+        summed over the shards."""
+        part = self.h.overlap_product(perm, factors)
+        tot = self._allreduce(np.array([part.real, part.imag]))
+        return complex(tot[0], tot[1])
+
+    def fidelity_product(self, perm, factors) -> float:
+        """Normalised fidelity with the product state (see SimResult.fidelity_product)."""
+        f = np.asarray(factors, dtype=np.complex128).reshape(-1, 2)
+        nphi = float(np.prod(np.sum(np.abs(f) ** 2, axis=1)))
+        return abs(self.overlap_product(perm, f)) ** 2 / (nphi * self.norm() ** 2)
 
     def logical_amplitudes(self, perm, count: int, start: int = 0) -> np.ndarray:
         """First `count` logical amplitudes (simulator.py:410-419), gathered on

@@ -133,3 +133,25 @@ def test_pack_round_trip():
     words, params, npar = _lib.pack(opt.instructions)
     assert words.dtype == np.int32 and npar == 6   # six RZZ angles
     assert words[0] == _lib.INS_BLOCK and words[1] == 3
+
+
+def test_bench_configs_cover_baseline_and_match_between_arms():
+    """bench.py: N>1 runs BASELINE C4/C5 (QFT 34/35/36 at 2/4/8 GPUs, 2^33
+    amplitudes per GPU; BV/H/QAOA 36 at 8), every circuit is committed, and
+    both arms print the same `config` for the same run."""
+    import os
+    import bench
+    for fam, by_n in bench.MULTI.items():
+        for world, stem in by_n.items():
+            f2, n, c, r = bench.parse_stem(stem)
+            assert f2 == fam and (1 << r) == world and n - r == 33, stem
+            assert os.path.exists(os.path.join(bench.CIRCUITS, stem + ".txt")), stem
+    assert bench.MULTI["qft"] == {2: "qft34_c10_r1", 4: "qft35_c10_r2", 8: "qft36_c10_r3"}
+    for world, wl in ((1, "qaoa30"), (2, "qft"), (8, "qaoa")):
+        args = type("A", (), {"circuit": None, "workload": wl})()
+        name, fname, n, c, r, fam = bench.pick(args, world)
+        cfg = bench.config_of(name, fname, n, c, r, world)
+        assert cfg == bench.config_of(*bench.pick(args, world)[:5], world)
+        assert cfg["state_bytes_per_gpu"] == 16 << (n - r)
+    assert bench.analytic_factors("qaoa", 4) is None
+    assert abs(np.prod(bench.analytic_factors("qft", 6)[:, 0]) - 2 ** -3) < 1e-15
