@@ -379,7 +379,7 @@ def run_single(args):
     st = h.stats()
     dev_per_step = sum(times) / args.steps
     value = dev_bracket / args.steps                 # CUDA events around K steps (incl. reset)
-    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st
+    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st[:12]
     peak, peak_kind = peaks()
     achieved_block = bb / (block_ms * 1e-3) / 1e9 if block_ms else 0.0
     achieved_sqs = sb / (sqs_ms * 1e-3) / 1e9 if sqs_ms else 0.0
@@ -485,7 +485,7 @@ def run_multi(args, world, rank, local):
 
     value = allmax(dev_s) / args.steps
     st = sim.stats()
-    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st
+    block_ms, block_n, sqs_ms, sqs_n, xrs_ms, xrs_n, bb, sb, xb, x_ms, x_n, x_b = st[:12]
     peak, peak_kind = peaks()
     achieved_block = bb / (block_ms * 1e-3) / 1e9 if block_ms else 0.0
     xrs_gbs = xb / (xrs_ms * 1e-3) / 1e9 if xrs_ms else 0.0
@@ -516,6 +516,7 @@ def run_multi(args, world, rank, local):
               "detail": {"blocks_s": block_ms * 1e-3 / args.steps, "sqs_s": sqs_ms * 1e-3 / args.steps,
                          "xrs_s": xrs_ms * 1e-3 / args.steps,
                          "xrs_exchanges_per_step": xrs_n / args.steps,
+                         "xrs_overlapped_per_step": float(st[12]) / args.steps,
                          "nvlink_bytes_sent_per_gpu_per_step": xb / args.steps,
                          "xrs_gbs_per_gpu": xrs_gbs,
                          "xrs_note": "algorithmic NVLink bytes sent (16 B x 2^L x (1-2^-S)) / exchange time incl. barrier waits",

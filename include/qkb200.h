@@ -149,7 +149,9 @@ int qk_run(qk_sim* sim, double* timings);
  * xrs_ms, xrs_launches. Also algorithmic bytes: out[6] block bytes, out[7]
  * sqs bytes, out[8] xrs bytes. out[9..11] = ms, launches and
  * bytes of the cluster-exchange block passes (block + full chunk swap in one
- * pass), which out[0..1] and out[6] exclude; out must hold 12 doubles. */
+ * pass), which out[0..1] and out[6] exclude. out[12] = cross-shard exchanges
+ * that ran overlapped with their neighbour passes (comm stream; xrs_ms is then
+ * the exchange's own span). out must hold 16 doubles. */
 int qk_kernel_stats(qk_sim* sim, double* out, int reset);
 
 /* Enable per-launch event timing (1) or per-instruction-class timing only (0). */
@@ -223,6 +225,14 @@ int qk_csqs_plan(int n, int r, int count, int shard, const int32_t* local_set,
                  const int32_t* rank_set, int s, uint64_t* segs, size_t* nseg,
                  int32_t* local_pairs, int* nlocal);
 int qk_ipc_open(qk_sim* sim, int peer_shard, const void* handle64);
+/* Pipeline every cross-shard CSQS with its neighbour passes (1) or not (0):
+ * the pass before, the exchange (on a second stream) and the pass after run
+ * in parts split on a bit outside both tiles, so the NVLink transfer of one
+ * part overlaps the HBM passes of the others. Applies to programs loaded
+ * afterwards. Default: on for a qk_create_multi handle whose devices are all
+ * distinct, off otherwise (the multi-process mirror enables it when every
+ * shard has its own GPU). QK_OVERLAP=1 / QK_NO_OVERLAP=1 override. */
+int qk_set_overlap(qk_sim* sim, int enable);
 typedef int (*qk_barrier_fn)(void* ctx);
 int qk_set_barrier(qk_sim* sim, qk_barrier_fn fn, void* ctx);
 

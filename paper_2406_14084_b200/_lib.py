@@ -68,6 +68,7 @@ _SIGS = {
                              P(c_size), P(c_int32), P(c_int)]),
     "qk_ipc_open": (c_int, [c_void, c_int, c_void]),
     "qk_set_barrier": (c_int, [c_void, BARRIER_FN, c_void]),
+    "qk_set_overlap": (c_int, [c_void, c_int]),
     "qk_mark": (c_int, [c_void, c_int]),
     "qk_mark_elapsed": (c_int, [c_void, c_int, c_int, P(c_dbl)]),
     "qk_sync": (c_int, [c_void]),
@@ -271,7 +272,7 @@ class Handle:
         return {"gate": float(t[0]), "ims": float(t[1]), "xrs": float(t[2])}, float(t[3])
 
     def stats(self, reset=False):
-        out = np.zeros(12, dtype=np.float64)
+        out = np.zeros(16, dtype=np.float64)
         check(lib().qk_kernel_stats(self.ptr, dptr(out), int(reset)))
         return out
 

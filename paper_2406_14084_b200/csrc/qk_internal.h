@@ -245,8 +245,8 @@ int launch_swap_segments(double* a, double* b, uint64_t n_amps, CUstream_st* str
 int launch_swap_strided(double* a, double* b, uint64_t n, const int* pos, int npos, CUstream_st* stream);
 int preload_exchange_kernels();  // force-load (lazy loading) every kernel an exchange step launches
 // device-side barrier of the shards of one exchange (flag arrays in peer memory)
-int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx, int n, int me,
-                        unsigned long long epoch, int* err, CUstream_st* stream);
+int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx,
+                        const unsigned long long* epochs, int n, int me, int* err, CUstream_st* stream);
 // sum of n partials (fused-norm readback of the last pass)
 int launch_sum_final(const double* partial, int n, double* out, CUstream_st* stream);
 int launch_sumsq(const double* state, uint64_t n_amps, double* d_partial, double* d_out,

@@ -85,6 +85,7 @@ struct QkJitParams {
   double2* out;
   u64 nchunks;
   double* nrm;
+  u64 split;  // sub-launch over part of the chunks (qk_insert); 0 = every chunk
   long long toff[QK_NTAB + 1];
   double coef[QK_NCOEF + 1];
 };
@@ -122,6 +123,18 @@ __device__ __forceinline__ void gbar(int id, int n) { asm volatile("bar.sync %0,
 __device__ __forceinline__ void st_cs(double2* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory"); }
 __device__ __forceinline__ u32 swz(u32 i) { return i ^ ((i >> 3) & 7u); }
+// split word: bits 0..1 n, bits 2+6k.. position k (chunk-index bit, ascending),
+// bit 20+k its value, bit 23 accumulate the fused norm. The compact counter c
+// enumerates the chunks whose n fixed bits hold those values.
+__device__ __forceinline__ u64 qk_insert(u64 c, u64 w) {
+  const int n = (int)(w & 3ull);
+  for (int k = 0; k < n; ++k) {
+    const int pos = (int)((w >> (2 + 6 * k)) & 63ull);
+    const u64 v = (w >> (20 + k)) & 1ull;
+    c = ((c >> pos) << (pos + 1)) | (v << pos) | (c & ((1ull << pos) - 1ull));
+  }
+  return c;
+}
 __device__ __forceinline__ void hb(double2& a, double2& b) {
   a.x += b.x; a.y += b.y; b.x = fma(-2.0, b.x, a.x); b.y = fma(-2.0, b.y, a.y); }
 __device__ __forceinline__ void xb(double2& a, double2& b) { double2 t = a; a = b; b = t; }
@@ -722,15 +735,20 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     o << ";\n}\n";
   }
   // counter -> chunk for iteration i of this CTA; `nxt` = the chunk st iterations later
+  // (split sub-launches, the passes next to an overlapped exchange, walk the
+  // grid-stride order over their part of the chunks)
   auto chunk_of = [&](const char* iv) {
     std::ostringstream c;
-    if (corder) c << "cmap(blockIdx.x * PER + " << iv << ")";
-    else c << "(blockIdx.x + " << iv << " * G)";
+    c << "(p.split ? qk_insert(blockIdx.x + " << iv << " * G, p.split) : ";
+    if (corder) c << "cmap(blockIdx.x * PER + " << iv << "))";
+    else c << "(blockIdx.x + " << iv << " * G))";
     return c.str();
   };
   auto chunk_ok = [&](const char* iv) {
     std::ostringstream c;
-    if (corder) c << "(" << iv << " < PER && blockIdx.x * PER + " << iv << " < p.nchunks)";
+    if (corder)
+      c << "(p.split ? (blockIdx.x + " << iv << " * G < p.nchunks) : (" << iv << " < PER && blockIdx.x * PER + " << iv
+        << " < p.nchunks))";
     else c << "(blockIdx.x + " << iv << " * G < p.nchunks)";
     return c.str();
   };
@@ -841,7 +859,8 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "    gbar(bar_id, " << GT << ");\n"
       << "    if (tid == 0) {\n      double sum = 0.0;\n"
       << "      for (int w = 0; w < " << std::max(1, GT / 32) << "; ++w) sum += red[w];\n"
-      << "      p.nrm[blockIdx.x * " << ng << " + g] = sum;\n    }\n  }\n";
+      << "      if ((p.split >> 23) & 1ull) p.nrm[blockIdx.x * " << ng << " + g] += sum;\n"
+      << "      else p.nrm[blockIdx.x * " << ng << " + g] = sum;\n    }\n  }\n";
   }
   o << "}\n";
   *src = o.str();

@@ -672,12 +672,14 @@ struct PeerFlags {
   int32_t n, me;
   int32_t idx[64];
   unsigned long long* remote[64];  // peer idx[k]'s flag array (mapped over NVLink / IPC)
+  unsigned long long epoch[64];    // this pair's meeting count (both sides count alike)
 };
 
 __global__ void k_peer_barrier(unsigned long long* __restrict__ mine, const __grid_constant__ PeerFlags pf,
-                               unsigned long long epoch, int* __restrict__ err) {
+                               int* __restrict__ err) {
   const int k = threadIdx.x;
   asm volatile("fence.acq_rel.sys;" ::: "memory");
+  const unsigned long long epoch = k < pf.n ? pf.epoch[k] : 0ull;
   if (k < pf.n) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(pf.remote[k] + pf.me), "l"(epoch) : "memory");
   if (k < pf.n) {
     unsigned long long t0, t, v;
@@ -697,8 +699,8 @@ __global__ void k_peer_barrier(unsigned long long* __restrict__ mine, const __gr
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
-int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx, int n, int me,
-                        unsigned long long epoch, int* err, CUstream_st* stream) {
+int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* remote, const int* idx,
+                        const unsigned long long* epochs, int n, int me, int* err, CUstream_st* stream) {
   if (n > 64 || n < 0) return -1;
   PeerFlags pf{};
   pf.n = n;
@@ -706,8 +708,9 @@ int launch_peer_barrier(unsigned long long* mine, unsigned long long* const* rem
   for (int k = 0; k < n; ++k) {
     pf.idx[k] = idx[k];
     pf.remote[k] = remote[k];
+    pf.epoch[k] = epochs[k];
   }
-  k_peer_barrier<<<1, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(mine, pf, epoch, err);
+  k_peer_barrier<<<1, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(mine, pf, err);
   return (int)cudaGetLastError();
 }
 

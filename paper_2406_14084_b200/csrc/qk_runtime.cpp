@@ -392,6 +392,15 @@ struct InstrPlan {
   int csqs_s = 0;            // multi-process CSQS
   std::vector<int> a, b;
   double bytes = 0;          // algorithmic HBM bytes
+  // cross-process CSQS pipelined with its neighbour passes (set at upload):
+  // the pass before (ovl_p), the exchange and the pass after (ovl_q) all run
+  // in 2^ovl_k parts split on the same physical bits ovl_f (outside both
+  // tiles and outside the exchanged bits), so part f of the exchange (comm
+  // stream) overlaps part f+1 of the pass before and part f-1 of the pass after
+  int ovl_p = -1, ovl_q = -1, ovl_k = 0;
+  int ovl_f[2] = {0, 0};          // split bits (physical)
+  int ovl_cp[2] = {0, 0};         // their chunk-index bits in ovl_p / ovl_q
+  int ovl_cq[2] = {0, 0};
 };
 
 int popc(uint64_t x) { return __builtin_popcountll(x); }
@@ -1242,6 +1251,7 @@ struct qk_sim {
   double stat_ms[4] = {0, 0, 0, 0};
   double stat_launch[4] = {0, 0, 0, 0};
   double stat_bytes[4] = {0, 0, 0, 0};
+  double stat_overlapped = 0;  // exchanges that ran overlapped with their neighbour passes
   // persistent TMA passes
   int num_sms = 148;
   bool allow_tma = true;
@@ -1262,12 +1272,20 @@ struct qk_sim {
   // (every shard runs the same exchanges, so the epochs agree)
   unsigned long long* flags = nullptr;
   std::vector<unsigned long long*> peer_flags;
-  unsigned long long epoch = 0;
   int* d_err = nullptr;
   bool ipc_mapped = false;     // peers[] came from cudaIpcOpenMemHandle (closed at destroy)
   // group handle (qk_create_multi): one member shard per device, this
   // handle owns them and holds no state of its own
   std::vector<qk_sim*> members;
+  std::vector<char> skipped;   // per instruction of the last run: a swap of the fresh |0...0> (identity)
+  // exchange overlap (QK_NO_OVERLAP disables): second stream for the peer
+  // swaps, pass -> CSQS maps, per-part events, the CSQS whose pre-pass ran split
+  cudaStream_t comm = nullptr;
+  std::vector<int> ovl_by_p, ovl_by_q;
+  cudaEvent_t ev_part[8] = {}, ev_x[8] = {};
+  int ovl_live = -1;
+  int overlap = 0;  // pipeline exchanges with their neighbour passes (peers on other GPUs; qk_set_overlap)
+  std::vector<unsigned long long> pair_epoch;  // device barrier meetings per peer shard
 };
 
 constexpr size_t kFlagBytes = 4096;  // 64 shards x 8 B, padded
@@ -1585,6 +1603,8 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
   return ok;
 }
 
+void plan_overlap(qk_sim* s);
+
 int upload_plan(qk_sim* s) {
   HostPlan& hp = s->hp;
   std::vector<char> buf;
@@ -1721,14 +1741,15 @@ int upload_plan(qk_sim* s) {
     for (size_t i = 0; i < srcs.size(); ++i) {
       if (!handles[i]) continue;
       const int p = src_pass[i];
-      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | toff[ntab+1] | coef[ncoef+1]
-      std::vector<uint64_t> blob(16 + 5 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
+      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | split | toff[ntab+1] | coef[ncoef+1]
+      std::vector<uint64_t> blob(16 + 6 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
       blob[16] = (uint64_t)(uintptr_t)s->d_pool;
       const TmaParams& tq = s->tma[s->pass_tma[p]];
       blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
       blob[20] = (uint64_t)(uintptr_t)s->d_nrm;
-      for (size_t k = 0; k < toffs[i].size(); ++k) blob[21 + k] = (uint64_t)toffs[i][k];
-      const size_t co = 21 + toffs[i].size() + 1;
+      blob[21] = 0;                                                 // split word (launch_pass_part)
+      for (size_t k = 0; k < toffs[i].size(); ++k) blob[22 + k] = (uint64_t)toffs[i][k];
+      const size_t co = 22 + toffs[i].size() + 1;
       for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
       s->pass_jit[p] = handles[i];
       s->jit_blob[p] = std::move(blob);
@@ -1781,6 +1802,7 @@ int upload_plan(qk_sim* s) {
         fprintf(stderr, "\n");
       }
     }
+  plan_overlap(s);
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
                                  (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
@@ -2531,6 +2553,7 @@ int compile_program(qk_sim* s) {
           b.push_back(sigma[sb[k]]);
         }
         ip.sqs = ins.a.empty() ? -1 : compile_sqs(s->hp, a, b, nb, true);
+        ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
       } else {
         ip.sqs = -2;  // cross-process exchange over the current layout (strided segments)
         ip.xlay = sigma;
@@ -2557,7 +2580,6 @@ int compile_program(qk_sim* s) {
           ip.xlay = sigma;
         }
       }
-      ip.bytes = 32.0 * std::ldexp(1.0, nb) * (1.0 - std::ldexp(1.0, -(int)ins.a.size()));
     }
     s->iplan.push_back(std::move(ip));
   }
@@ -2631,13 +2653,17 @@ int ensure_events(qk_sim* s, size_t n) {
   return QK_OK;
 }
 
-int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0) {
+// split != 0: one part of a specialised pass (qk_jit.cpp qk_insert: the chunks
+// whose split bits hold the given values), never on a fresh state
+int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 0, uint64_t split = 0) {
   const bool tma_pass = s->allow_tma && !first && !count_override && p < (int)s->pass_tma.size() && s->pass_tma[p] >= 0;
   // a fresh state is read only by a TMA pass (it writes every chunk) through a
   // view whose in-bounds part is the written prefix
   CUtensorMap fmap;
-  const bool from_fresh = s->fresh && tma_pass && s->cur == 0 && !getenv("QK_NO_FRESH") &&
+  const bool from_fresh = !split && s->fresh && tma_pass && s->cur == 0 && !getenv("QK_NO_FRESH") &&
                           fresh_map(s, s->tma[s->pass_tma[p]], &fmap);
+  if (split && !(tma_pass && p < (int)s->pass_jit.size() && s->pass_jit[p]))
+    return fail(QK_ESIM, "internal: split launch of a pass without a specialised kernel");
   if (!from_fresh) {
     if (s->fresh && getenv("QK_DUMP_PLAN"))
       fprintf(stderr, "fresh state: pass %d (tma %d) fills the whole state first\n", p, (int)tma_pass);
@@ -2667,10 +2693,19 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       memcpy(blob.data(), lazy_map, 128);
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
+      const uint64_t nch = split ? tp.nchunks >> (split & 3) : tp.nchunks;
+      if (split) {
+        blob[19] = nch;
+        blob[21] = split;
+      }
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
-                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.nchunks, s->num_sms, (CUstream_st*)s->stream,
+                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, nch, s->num_sms, (CUstream_st*)s->stream,
                                  tp.smax, jit_slice_bytes(tp));
+      if (split) {
+        blob[19] = tp.nchunks;
+        blob[21] = 0;
+      }
     } else {
       TmaParams tf;
       if (from_fresh && tp.lazy) {  // the generic kernel reads its view from the params
@@ -2698,39 +2733,6 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip);
 
 bool fused_away(const qk_sim* s, const InstrPlan& ip) {
   return ip.lazy || (ip.fused_by >= 0 && s->iplan[ip.fused_by].permuted);
-}
-
-int run_instr(qk_sim* s, const InstrPlan& ip) {
-  if (ip.type != QK_INS_BLOCK && fused_away(s, ip)) return QK_OK;
-  if (ip.type != QK_INS_BLOCK) {
-    int rc = ensure_full(s);
-    if (rc) return rc;
-  }
-  if (ip.type == QK_INS_BLOCK) {
-    for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
-      int rc = launch_pass(s, p);
-      if (rc) return rc;
-    }
-    return QK_OK;
-  }
-  if (ip.sqs >= 0) {
-    int rc = -2;
-    if (getenv("QK_SQS_BULK") && s->nbits >= 16)  // bulk-copy variant: 512-B copies are TMA-op bound
-      rc = launch_sqs_bulk(s->state, &s->hp.sqs[ip.sqs], s->num_sms, (CUstream_st*)s->stream);
-    if (rc == -2 && s->bufs[1] && s->oop_sqs && !getenv("QK_SQS_INPLACE")) {
-      // relabeled programs own a second buffer: permute into it and flip
-      rc = launch_sqs_oop(s->state, s->bufs[s->cur ^ 1], &s->hp.sqs[ip.sqs], (CUstream_st*)s->stream);
-      if (!rc) {
-        s->cur ^= 1;
-        s->state = s->bufs[s->cur];
-      }
-    }
-    if (rc == -2) rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
-    if (rc) return fail(QK_ECUDA, "sqs launch failed: %s", cudaGetErrorString((cudaError_t)rc));
-    return QK_OK;
-  }
-  if (ip.sqs == -2) return exchange_cross(s, ip);
-  return QK_OK;
 }
 
 // Multi-process CSQS plan (simulator.py:179-235 semantics, output independent
@@ -2802,6 +2804,231 @@ int csqs_plan(int n, int r, int count, int shard, const std::vector<int>& local_
   return QK_OK;
 }
 
+// ---- exchange overlap ------------------------------------------------------
+
+// split word of part f (cpos: chunk-index bits of the split bits, in bit order of f)
+uint64_t ovl_word(const int* cpos, int k, int f, bool acc) {
+  std::vector<std::pair<int, int>> pv;
+  for (int b = 0; b < k; ++b) pv.push_back({cpos[b], (f >> b) & 1});
+  std::sort(pv.begin(), pv.end());
+  uint64_t w = (uint64_t)k;
+  for (int b = 0; b < k; ++b) {
+    w |= (uint64_t)pv[b].first << (2 + 6 * b);
+    w |= (uint64_t)pv[b].second << (20 + b);
+  }
+  if (acc) w |= 1ull << 23;
+  return w;
+}
+
+// Pass before a pipelined exchange: part by part, each followed by an event
+// the exchange of that part waits on (comm stream).
+int ovl_pre(qk_sim* s, int p, int j) {
+  const InstrPlan& ip = s->iplan[j];
+  for (int f = 0; f < (1 << ip.ovl_k); ++f) {
+    int rc = launch_pass(s, p, 0, 0, ovl_word(ip.ovl_cp, ip.ovl_k, f, p == s->norm_pass && f > 0));
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(s->ev_part[f], s->stream));
+  }
+  s->ovl_live = j;
+  return QK_OK;
+}
+
+// Pass after it: part f as soon as part f of the exchange is done.
+int ovl_post(qk_sim* s, int p, int j) {
+  const InstrPlan& ip = s->iplan[j];
+  for (int f = 0; f < (1 << ip.ovl_k); ++f) {
+    CUDA_TRY(cudaStreamWaitEvent(s->stream, s->ev_x[f], 0));
+    int rc = launch_pass(s, p, 0, 0, ovl_word(ip.ovl_cq, ip.ovl_k, f, p == s->norm_pass && f > 0));
+    if (rc) return rc;
+  }
+  s->ovl_live = -1;
+  return QK_OK;
+}
+
+// The exchange on the comm stream, part by part: wait for that part of the
+// pass before, meet the exchange group (device barrier), swap the part's
+// amplitudes of every segment, meet again, release the pass after.
+int exchange_overlapped(qk_sim* s, const InstrPlan& ip, size_t i) {
+  std::vector<Seg> segs;
+  std::vector<int> in_a, in_b, group;
+  int rc = csqs_plan(s->n, s->r, s->count, s->shard, ip.a, ip.b, segs, in_a, in_b, &group);
+  if (rc) return rc;
+  cudaStream_t cs = s->comm;
+  auto phys = [&](int q) { return ip.xlay.empty() ? q : ip.xlay[q]; };
+  auto lay_of = [&](uint64_t a) {
+    uint64_t b = 0;
+    for (int q = 0; q < s->nbits; ++q) b |= ((a >> q) & 1ull) << phys(q);
+    return b;
+  };
+  std::vector<unsigned long long*> rflags;
+  for (int p : group) rflags.push_back(s->peer_flags[p]);
+  auto meet = [&]() -> int {
+    std::vector<unsigned long long> ep;
+    for (int p : group) ep.push_back(++s->pair_epoch[p]);
+    if (launch_peer_barrier(s->flags, rflags.data(), group.data(), ep.data(), (int)group.size(), s->shard, s->d_err,
+                            (CUstream_st*)cs))
+      return fail(QK_ECUDA, "peer barrier launch failed");
+    return QK_OK;
+  };
+  for (int f = 0; f < (1 << ip.ovl_k); ++f) {
+    CUDA_TRY(cudaStreamWaitEvent(cs, s->ev_part[f], 0));
+    if (f == 0) CUDA_TRY(cudaEventRecord(s->events[2 * i], cs));
+    rc = meet();
+    if (rc) return rc;
+    uint64_t fixed = 0;
+    for (int b = 0; b < ip.ovl_k; ++b) fixed |= (uint64_t)((f >> b) & 1) << ip.ovl_f[b];
+    for (auto& sg : segs) {
+      double* peer_state = (s->cur ? s->peers1 : s->peers)[sg.peer];
+      const int k = __builtin_ctzll(sg.len);
+      std::vector<int> pos;
+      for (int q = 0; q < k; ++q) {
+        const int pq = phys(q);
+        if (pq != ip.ovl_f[0] && (ip.ovl_k < 2 || pq != ip.ovl_f[1])) pos.push_back(pq);
+      }
+      std::sort(pos.begin(), pos.end());
+      rc = launch_swap_strided(s->state + 2 * (lay_of(sg.my_off) | fixed),
+                               peer_state + 2 * (lay_of(sg.peer_off) | fixed), sg.len >> ip.ovl_k, pos.data(),
+                               (int)pos.size(), (CUstream_st*)cs);
+      if (rc) return fail(QK_ECUDA, "peer exchange failed");
+    }
+    rc = meet();
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(s->ev_x[f], cs));
+  }
+  CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], cs));
+  return QK_OK;
+}
+
+// Which CSQS can be pipelined (after the kernels are known): one partition
+// per shard, no in-shard pairs, in-place specialised passes on both sides,
+// and QK_OVL_BITS (default 1) split bits that lie outside both tiles, outside
+// the exchanged bits and among the free bits of every exchanged segment. A
+// pass serves one exchange only.
+void plan_overlap(qk_sim* s) {
+  const size_t np = s->hp.passes.size();
+  s->ovl_by_p.assign(np, -1);
+  s->ovl_by_q.assign(np, -1);
+  s->ovl_live = -1;
+  for (auto& ip : s->iplan) ip.ovl_p = ip.ovl_q = -1;
+  const int want = getenv("QK_OVL_BITS") ? atoi(getenv("QK_OVL_BITS")) : 1;
+  // on by default when the peers are other GPUs (the exchange then runs over
+  // NVLink while the passes use HBM); members sharing one GPU share its HBM
+  // and measured slower pipelined (QFT33 R=1 on one B200: 0.85 vs 0.77 s)
+  const bool on = getenv("QK_OVERLAP") ? true : s->overlap != 0;
+  if (!on || getenv("QK_NO_OVERLAP") || want < 1 || want > 2 || s->nshards <= 1 || s->count != 1) return;
+  // in place (lazy strided tile, or contiguous chunk without a permuted store)
+  auto ok_pass = [&](int p) {
+    if (p < 0 || p >= (int)np || s->pass_tma[p] < 0 || p >= (int)s->pass_jit.size() || !s->pass_jit[p]) return false;
+    const TmaParams& tq = s->tma[s->pass_tma[p]];
+    return !tq.xbits && (tq.lazy || !tq.permuted);
+  };
+  // chunk-index bit of physical bit e in pass p (-1: e is a tile bit)
+  auto cidx = [&](int p, int e) {
+    const TmaParams& tq = s->tma[s->pass_tma[p]];
+    if (!tq.lazy) return e < tq.C ? -1 : e - tq.C;  // contiguous chunk: bits 0..C-1
+    int below = 0;
+    for (int k = 0; k < tq.C; ++k) {
+      if (tq.tbit[k] == e) return -1;
+      below += tq.tbit[k] < e;
+    }
+    return e - below;
+  };
+  for (size_t j = 0; j < s->iplan.size(); ++j) {
+    InstrPlan& ip = s->iplan[j];
+    if (ip.type != QK_INS_CSQS || ip.sqs != -2) continue;
+    const int so = (int)ip.a.size();
+    int P = -1, Q = -1;
+    for (int k = (int)j - 1; k >= 0; --k) {
+      const InstrPlan& q = s->iplan[k];
+      if (q.type == QK_INS_BLOCK && q.npass > 0) { P = q.pass0 + q.npass - 1; break; }
+      if ((q.type == QK_INS_BLOCK && q.npass == 0) || (q.type != QK_INS_BLOCK && fused_away(s, q))) continue;
+      break;
+    }
+    for (size_t k = j + 1; k < s->iplan.size(); ++k) {
+      const InstrPlan& q = s->iplan[k];
+      if (q.type == QK_INS_BLOCK && q.npass > 0) { Q = q.pass0; break; }
+      if ((q.type == QK_INS_BLOCK && q.npass == 0) || (q.type != QK_INS_BLOCK && fused_away(s, q))) continue;
+      break;
+    }
+    if (getenv("QK_DUMP_PLAN")) fprintf(stderr, "overlap? csqs %zu: P=%d ok=%d Q=%d ok=%d\n", j, P, (int)ok_pass(P), Q, (int)ok_pass(Q));
+    if (!ok_pass(P) || !ok_pass(Q) || P == Q || s->ovl_by_p[P] >= 0 || s->ovl_by_q[P] >= 0 || s->ovl_by_p[Q] >= 0)
+      continue;
+    // free reference bits of every segment: 0 .. L-so-2 (the lower/higher shard
+    // halves take bit L-so-1); prefer the highest physical positions
+    std::vector<int> cand;
+    for (int q = 0; q + so + 1 < s->L; ++q) {
+      const int e = ip.xlay.empty() ? q : ip.xlay[q];
+      if (cidx(P, e) >= 0 && cidx(Q, e) >= 0 && cidx(P, e) < 64 && cidx(Q, e) < 64) cand.push_back(e);
+    }
+    std::sort(cand.rbegin(), cand.rend());
+    if ((int)cand.size() < want) continue;
+    const int k = want;
+    if ((s->tma[s->pass_tma[P]].nchunks >> k) < (uint64_t)s->num_sms ||
+        (s->tma[s->pass_tma[Q]].nchunks >> k) < (uint64_t)s->num_sms)
+      continue;  // every part keeps a full grid (the fused-norm partial slots)
+    ip.ovl_k = k;
+    for (int b = 0; b < k; ++b) {
+      ip.ovl_f[b] = cand[b];
+      ip.ovl_cp[b] = cidx(P, cand[b]);
+      ip.ovl_cq[b] = cidx(Q, cand[b]);
+    }
+    ip.ovl_p = P;
+    ip.ovl_q = Q;
+    s->ovl_by_p[P] = (int)j;
+    s->ovl_by_q[Q] = (int)j;
+    if (getenv("QK_DUMP_PLAN"))
+      fprintf(stderr, "overlap: csqs %zu pipelined with passes %d / %d in %d parts (split bit %d)\n", j, P, Q, 1 << k,
+              cand[0]);
+  }
+}
+
+int run_instr(qk_sim* s, const InstrPlan& ip, bool* skipped = nullptr, size_t idx = (size_t)-1) {
+  if (ip.type != QK_INS_BLOCK && fused_away(s, ip)) return QK_OK;
+  // a swap of |0...0> (fresh after reset, every shard alike) is the identity:
+  // bitswap(0) = 0 for SQS and CSQS (simulator.py:81-88, 179-235)
+  if (ip.type != QK_INS_BLOCK && s->fresh && !getenv("QK_NO_FRESH")) {
+    if (skipped) *skipped = true;
+    return QK_OK;
+  }
+  if (ip.type != QK_INS_BLOCK) {
+    int rc = ensure_full(s);
+    if (rc) return rc;
+  }
+  if (ip.type == QK_INS_BLOCK) {
+    for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
+      const int jp = p < (int)s->ovl_by_p.size() ? s->ovl_by_p[p] : -1;
+      const int jq = p < (int)s->ovl_by_q.size() ? s->ovl_by_q[p] : -1;
+      int rc;
+      if (jq >= 0 && s->ovl_live == jq) rc = ovl_post(s, p, jq);
+      else if (jp >= 0 && !s->fresh) rc = ovl_pre(s, p, jp);  // (a fresh pre-pass runs whole)
+      else rc = launch_pass(s, p);
+      if (rc) return rc;
+    }
+    return QK_OK;
+  }
+  if (ip.sqs >= 0) {
+    int rc = -2;
+    if (getenv("QK_SQS_BULK") && s->nbits >= 16)  // bulk-copy variant: 512-B copies are TMA-op bound
+      rc = launch_sqs_bulk(s->state, &s->hp.sqs[ip.sqs], s->num_sms, (CUstream_st*)s->stream);
+    if (rc == -2 && s->bufs[1] && s->oop_sqs && !getenv("QK_SQS_INPLACE")) {
+      // relabeled programs own a second buffer: permute into it and flip
+      rc = launch_sqs_oop(s->state, s->bufs[s->cur ^ 1], &s->hp.sqs[ip.sqs], (CUstream_st*)s->stream);
+      if (!rc) {
+        s->cur ^= 1;
+        s->state = s->bufs[s->cur];
+      }
+    }
+    if (rc == -2) rc = launch_sqs(s->state, &s->hp.sqs[ip.sqs], s->d_sqs + ip.sqs, (CUstream_st*)s->stream);
+    if (rc) return fail(QK_ECUDA, "sqs launch failed: %s", cudaGetErrorString((cudaError_t)rc));
+    return QK_OK;
+  }
+  if (ip.sqs == -2) {
+    if (idx != (size_t)-1 && s->ovl_live == (int)idx) return exchange_overlapped(s, ip, idx);
+    return exchange_cross(s, ip);
+  }
+  return QK_OK;
+}
+
 int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   if (s->nshards <= 1 || (int)s->peers.size() < s->nshards)
     return fail(QK_ESIM, "cross-rank swap needs the peer shards' state (qk_ipc_open)");
@@ -2825,7 +3052,9 @@ int exchange_cross(qk_sim* s, const InstrPlan& ip) {
   if (!dev_bar && !s->barrier) return fail(QK_ESIM, "cross-rank swap needs a barrier between the shards");
   auto meet = [&]() -> int {
     if (dev_bar) {
-      if (launch_peer_barrier(s->flags, rflags.data(), group.data(), (int)group.size(), s->shard, ++s->epoch,
+      std::vector<unsigned long long> ep;
+      for (int p : group) ep.push_back(++s->pair_epoch[p]);
+      if (launch_peer_barrier(s->flags, rflags.data(), group.data(), ep.data(), (int)group.size(), s->shard,
                               s->d_err, (CUstream_st*)s->stream))
         return fail(QK_ECUDA, "peer barrier launch failed");
       return QK_OK;
@@ -2982,6 +3211,11 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
     }
   }
   CUDA_TRY(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&s->comm, cudaStreamNonBlocking));
+  for (int k = 0; k < 8; ++k) {
+    CUDA_TRY(cudaEventCreateWithFlags(&s->ev_part[k], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&s->ev_x[k], cudaEventDisableTiming));
+  }
   CUDA_TRY(cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device));
   CUDA_TRY(cudaMalloc(&s->d_partial, 148 * 8 * sizeof(double) + 256));
   CUDA_TRY(cudaMalloc(&s->d_nrm, 4096 * sizeof(double)));
@@ -3000,6 +3234,7 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   s->peers1[s->shard] = s->bufs[1];
   s->peer_flags.assign(s->nshards, nullptr);
   s->peer_flags[s->shard] = s->flags;
+  s->pair_epoch.assign(s->nshards, 0);
   *out = s;
   return QK_OK;
 }
@@ -3058,6 +3293,8 @@ int run_prepare(qk_sim* s, size_t* first_exec) {
   if (rc) return rc;
   s->fresh_saved = 0;
   *first_exec = s->iplan.size();  // the instruction whose pass read the fresh state
+  s->skipped.assign(s->iplan.size(), 0);
+  s->ovl_live = -1;
   return ensure_events(s, 2 * s->iplan.size() + 2);
 }
 
@@ -3065,10 +3302,15 @@ int run_step(qk_sim* s, size_t i, size_t* first_exec) {
   CUDA_TRY(cudaSetDevice(s->device));
   CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
   const bool was_fresh = s->fresh;
-  int rc = run_instr(s, s->iplan[i]);
+  bool skipped = false;
+  const bool overlapped = s->iplan[i].type == QK_INS_CSQS && s->ovl_live == (int)i;
+  int rc = run_instr(s, s->iplan[i], &skipped, i);
   if (rc) return rc;
+  s->skipped[i] = skipped;
   if (was_fresh && !s->fresh && s->fresh_saved > 0) *first_exec = i;
-  CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
+  // (an overlapped exchange brackets itself on the comm stream)
+  if (!overlapped) CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
+  else s->stat_overlapped += 1;
   return QK_OK;
 }
 
@@ -3095,7 +3337,7 @@ int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
                     s->tma[s->pass_tma[ip.pass0 + ip.npass - 1]].xbits > 0;
     const int sc = xp ? 3 : c;
     s->stat_ms[sc] += ms;
-    if (fused_away(s, ip)) continue;
+    if (fused_away(s, ip) || s->skipped[i]) continue;
     s->stat_bytes[sc] += ip.bytes - (i == first_exec ? s->fresh_saved : 0.0);
     s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
   }
@@ -3291,6 +3533,8 @@ int qk_create_multi(int n, int r, int b, const int* devs, int ndev, qk_sim** out
       }
       cudaGetLastError();
     }
+  const bool distinct = per_dev.size() == (size_t)ndev;
+  for (qk_sim* m : g->members) m->overlap = distinct ? 1 : 0;
   for (int a = 0; a < ndev; ++a)
     for (int c = 0; c < ndev; ++c) {
       g->members[a]->peers[c] = g->members[c]->bufs[0];
@@ -3327,6 +3571,14 @@ int qk_destroy(qk_sim* s) {
   if (s->d_partial) cudaFree(s->d_partial);
   if (s->d_nrm) cudaFree(s->d_nrm);
   if (s->d_scratch) cudaFree(s->d_scratch);
+  if (s->comm) {
+    cudaStreamSynchronize(s->comm);
+    cudaStreamDestroy(s->comm);
+  }
+  for (int k = 0; k < 8; ++k) {
+    if (s->ev_part[k]) cudaEventDestroy(s->ev_part[k]);
+    if (s->ev_x[k]) cudaEventDestroy(s->ev_x[k]);
+  }
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return QK_OK;
@@ -3480,9 +3732,13 @@ int qk_kernel_stats(qk_sim* s, double* out, int reset) {
     out[9] = s->stat_ms[3];
     out[10] = s->stat_launch[3];
     out[11] = s->stat_bytes[3];
-    }
-  if (reset)
+    out[12] = s->stat_overlapped;
+    out[13] = out[14] = out[15] = 0;
+  }
+  if (reset) {
     for (int c = 0; c < 4; ++c) s->stat_ms[c] = s->stat_launch[c] = s->stat_bytes[c] = 0;
+    s->stat_overlapped = 0;
+  }
   return QK_OK;
 }
 
@@ -4036,6 +4292,13 @@ int qk_ipc_open(qk_sim* s, int peer, const void* handle128) {
     if (!b) s->peer_flags[peer] = (unsigned long long*)((char*)p + ((size_t)16 << s->nbits));
     s->ipc_mapped = true;
   }
+  return QK_OK;
+}
+
+int qk_set_overlap(qk_sim* s, int enable) {
+  if (!s) return fail(QK_EINVAL, "null handle");
+  QK_GROUP_ALL(qk_set_overlap(m, enable));
+  s->overlap = enable ? 1 : 0;
   return QK_OK;
 }
 

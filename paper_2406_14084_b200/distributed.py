@@ -21,6 +21,15 @@ from . import _lib
 from .circuit import replay_permutation
 
 
+def _device_uuid(dev: int) -> str:
+    try:
+        import torch
+        return str(torch.cuda.get_device_properties(dev).uuid)
+    except Exception:  # noqa: BLE001 — unknown: treat every shard as its own GPU
+        import os
+        return f"{os.getpid()}:{dev}"
+
+
 class ShardedSimulator:
     """Shard of a 2^R-rank state held by this process (count = 2^R / world)."""
 
@@ -49,6 +58,12 @@ class ShardedSimulator:
                 _lib.check(_lib.lib().qk_ipc_open(self.h.ptr, peer, raw))
         self._cb = _lib.BARRIER_FN(self._barrier)
         _lib.check(_lib.lib().qk_set_barrier(self.h.ptr, self._cb, None))
+        # pipeline the exchanges with the neighbour passes when every shard has
+        # its own GPU (NVLink transfer next to HBM passes; shards sharing one
+        # GPU would share its HBM)
+        uuids = [None] * self.world
+        dist.all_gather_object(uuids, _device_uuid(dev), group=group)
+        _lib.check(_lib.lib().qk_set_overlap(self.h.ptr, int(len(set(uuids)) == self.world)))
         self.perm = tuple(range(n))
 
     def close(self) -> None:

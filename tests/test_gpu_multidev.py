@@ -118,3 +118,39 @@ def test_group_33_qubits_two_members(gpu, name):
     sim.release()
     del res, sim
     gc.collect()
+
+
+@pytest.mark.parametrize("name", ["qft24_c10_r1"])
+def test_group_overlapped_exchange_matches_oracle(gpu, name):
+    """2^23 amplitudes per member (specialised lazy passes): the CSQS runs
+    overlapped with its neighbour passes (pre-pass part by part, exchange on
+    the comm stream per segment, post-pass part by part). Same result as the
+    CPU oracle and as the non-overlapped exchange (QK_NO_OVERLAP)."""
+    fam_n, c, r = name.split("_")
+    n, c, r = int(fam_n[3:]), int(c[1:]), int(r[1:])
+    text = open(os.path.join(ROOT, "bench_circuits", name + ".txt")).read()
+    want, perm, _ = orc.simulate_text(text, n, n - r, r=r)
+    outs = {}
+    for mode in ("overlap", "QK_NO_OVERLAP"):
+        # (members on one GPU pipeline only when forced: QK_OVERLAP)
+        os.environ["QK_OVERLAP" if mode == "overlap" else mode] = "1"
+        try:
+            sim = Simulator(LayoutParams(n=n, c=n - r, r=r), devices=[0, 0])
+            p2 = sim.load_text(text, c)
+            for _ in range(2):            # the second run reuses events, epochs and flags
+                sim.reset()
+                res = sim.run_loaded(p2)
+            st = sim.handle.stats()
+            outs[mode] = (res.physical_vector(), res.norm(), st[12], st[5])
+            sim.release()
+        finally:
+            os.environ.pop(mode, None)
+            os.environ.pop("QK_OVERLAP", None)
+    assert tuple(perm) == tuple(p2)
+    vec, nrm, n_ovl, n_x = outs["overlap"]
+    print(f"\n  {name}: {int(n_ovl)} of {int(n_x)} exchanges overlapped over 2 runs")
+    assert n_ovl >= 1
+    assert outs["QK_NO_OVERLAP"][2] == 0
+    assert np.max(np.abs(vec - want)) <= TOL
+    assert np.array_equal(vec, outs["QK_NO_OVERLAP"][0])
+    assert abs(nrm - np.linalg.norm(want)) <= 1e-12

@@ -27,13 +27,19 @@ def _port():
 
 
 CIRCUITS = [("example", 10, 4, 2, 8), ("random", 12, 5, 2, 6), ("random3", 13, 6, 3, 7),
-            ("random18", 18, 8, 1, 10), ("random19r2", 19, 8, 2, 10), ("random19c12", 19, 12, 1, 12)]
+            ("random18", 18, 8, 1, 10), ("random19r2", 19, 8, 2, 10), ("random19c12", 19, 12, 1, 12),
+            # reference optimizer output, 2^23 per shard: specialised lazy passes and
+            # the exchange overlapped with its neighbour passes
+            ("qft24_c10_r1", 24, 10, 1, 23)]
 
 
 def _circuit(name, n, c, r, seed=0):
     from conftest import EXAMPLE_OPTIMIZED
     if name == "example":
         return EXAMPLE_OPTIMIZED
+    if name.startswith("qft"):
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        return open(os.path.join(root, "bench_circuits", name + ".txt")).read()
     from paper_2406_14084_b200 import LayoutParams, OptimizedCircuit, serialize_optimized
     from test_gpu_parity import _random_stream
     rng = np.random.default_rng(900 + n)
@@ -55,7 +61,7 @@ def _worker(rank, world, port, results):
         for name, n, c, r, b in CIRCUITS:
             text = _circuit(name, n, c, r)
             sim = ShardedSimulator(n, r, b=b, device=0)
-            perm = sim.load_text(text, n - r)
+            perm = sim.load_text(text, c if name.startswith("qft") else n - r)
             sim.reset()
             sim.run()
             shard = np.concatenate([sim.h.read(k, 0, 1 << (n - r)) for k in range(sim.count)])
@@ -75,7 +81,8 @@ def test_two_processes_share_the_state(gpu, mode):
     from paper_2406_14084_b200 import LayoutParams, Simulator
     mgr = mp.Manager()
     results = mgr.dict()
-    env = {"lazy": {"QK_INPLACE": "1", "QK_JIT": "0"}, "relabel": {"QK_JIT": "0"}}.get(mode, {})
+    env = {"lazy": {"QK_INPLACE": "1", "QK_JIT": "0"}, "relabel": {"QK_JIT": "0"},
+           "default": {"QK_OVERLAP": "1"}}.get(mode, {})
     os.environ.update(env)
     try:
         mp.spawn(_worker, args=(2, _port(), results), nprocs=2, join=True)
