@@ -225,7 +225,20 @@ int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream);
 int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax = 0);
 // load-time specialised passes (qk_jit.cpp)
 bool jit_available();
-bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef);
+// Per OP_DIAG op of a pass: may its table be applied in the quadratic form?
+// The table's phase, restricted to the register slots, has at most pairwise
+// terms (every gate touches <= 2 targets, or only one register slot), so
+// f_j = f_0 * prod_{s in j} (f_s / f_0) * P_j with P_j the product of the pair
+// factors pf[s][s'] = e11 e00 / (e01 e10) of the 2-slot gates: a thread then
+// gathers 1 + (#slots) entries per chunk instead of 2^M.
+struct QuadOp {
+  bool ok = false;
+  double pf[16][2] = {};   // pair (s, s') at index s * 4 + s' (s < s'), complex
+  double inv2 = 1.0;       // 1 / |table scale|^2 (f_s / f_0 = f_s conj(f_0) inv2)
+};
+// variant bits: 1 = no hoisted table, 2 = quadratic table groups
+bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef,
+                int variant = 0, const std::vector<QuadOp>* quad = nullptr);
 void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles);
 int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream,
                int smax = 0, int extra_smem = 0);

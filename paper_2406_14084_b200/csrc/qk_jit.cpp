@@ -374,7 +374,7 @@ int jit_slice_bytes(const TmaParams& tp) {
 // Emit the source of one pass. Returns false when the structure is outside
 // what the generator covers (the caller keeps the interpreter).
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
-                std::vector<double>* coef) {
+                std::vector<double>* coef, int variant, const std::vector<QuadOp>* quad) {
   const int C = tp.C, M = tp.M, T = C - M, NA = 1 << M;
   if (M != 4 && M != 3) return false;
   std::ostringstream b, pro;  // pro: consumer prologue (loop-invariant table values)
@@ -392,8 +392,9 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // 16-amplitude threads, two for 8-amplitude threads
   const char* hz = getenv("QK_JIT_HOIST");
   // (none for 512-thread groups: 120 registers per thread leave no room)
-  const int hoist = std::min<int>((int)toff->size(),
-                                  hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
+  const int hoist = (variant & 1) ? 0
+                                  : std::min<int>((int)toff->size(),
+                                                  hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
   // hoist the first `hoist` tables that have no per-chunk (outer-bit) term
   // and load the first `early` per-chunk tables at the top of the chunk
   // iteration, so their L2 latency overlaps the stage wait and earlier phases
@@ -484,6 +485,92 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     if (last) b << "    (void)0;\n";
     for (int o = D.op_begin; o < D.op_end; ++o) {
       const TOp& op = tp.ops[o];
+      // quadratic table group: consecutive eligible tables of this phase
+      // (not hoisted / early / sliced) applied as one factor per amplitude
+      if ((variant & 2) && quad && op.code == OP_DIAG && o < (int)quad->size() && (*quad)[o].ok &&
+          !hoisted[tab_i] && !early[tab_i] && !(slices[tab_i] > 0)) {
+        int o2 = o, ti2 = tab_i;
+        while (o2 < D.op_end && tp.ops[o2].code == OP_DIAG && (*quad)[o2].ok && !hoisted[ti2] && !early[ti2] &&
+               !(slices[ti2] > 0)) {
+          ++o2;
+          ++ti2;
+        }
+        // slots of the group: register slot s is in table t's support when pr[1 << s] != 0
+        uint32_t gslots = 0;
+        for (int oo = o; oo < o2; ++oo)
+          for (int sl = 0; sl < M; ++sl)
+            if (tp.ops[oo].pr[1 << sl]) gslots |= 1u << sl;
+        b << "    {  // quadratic table group (ops " << o << ".." << o2 - 1 << ")\n";
+        b << "      double2 F0";
+        for (int sl = 0; sl < M; ++sl)
+          if (gslots >> sl & 1) b << ", G" << sl;
+        b << ";\n";
+        uint32_t gseen = 0;
+        for (int oo = o; oo < o2; ++oo, ++tab_i) {
+          const TOp& q = tp.ops[oo];
+          b << "      { const double2* tb = p.tabs + p.toff[" << tab_i << "];\n";
+          b << "        const u32 pt = 0u";
+          for (int k = 0; k < T; ++k)
+            if (q.tcontrib[k]) b << " | (((tid >> " << k << ") & 1u) * " << q.tcontrib[k] << "u)";
+          for (int k = 0; k < q.nco; ++k)
+            b << " | ((u32)((chunk >> " << (int)q.co_k[k] << ") & 1ull) * " << q.co_v[k] << "u)";
+          b << ";\n        const double2 a0 = __ldg(tb + pt);\n";
+          b << "        " << (oo == o ? "F0 = a0;" : "F0 = cm(F0, a0);") << "\n";
+          const double inv2 = (*quad)[oo].inv2;
+          int ci_inv = -1;
+          if (inv2 != 1.0) {
+            ci_inv = (int)coef->size();
+            coef->push_back(inv2);
+          }
+          for (int sl = 0; sl < M; ++sl) {
+            if (!q.pr[1 << sl]) continue;
+            b << "        { const double2 as = __ldg(tb + (pt | " << q.pr[1 << sl] << "u));\n";
+            // as * conj(a0)
+            b << "          double2 r = make_double2(fma(as.x, a0.x, as.y * a0.y), fma(as.y, a0.x, -as.x * a0.y));\n";
+            if (ci_inv >= 0) b << "          r.x *= p.coef[" << ci_inv << "]; r.y *= p.coef[" << ci_inv << "];\n";
+            b << "          " << ((gseen >> sl & 1) ? "G" + std::to_string(sl) + " = cm(G" + std::to_string(sl) + ", r);"
+                                                  : "G" + std::to_string(sl) + " = r;")
+              << " }\n";
+            gseen |= 1u << sl;
+          }
+          b << "      }\n";
+        }
+        // pair factors of the group: product over its tables
+        double P[16][2];
+        for (int a = 0; a < 16; ++a) P[a][0] = 1.0, P[a][1] = 0.0;
+        for (int oo = o; oo < o2; ++oo)
+          for (int a = 0; a < 16; ++a) {
+            const double re = P[a][0] * (*quad)[oo].pf[a][0] - P[a][1] * (*quad)[oo].pf[a][1];
+            const double im = P[a][0] * (*quad)[oo].pf[a][1] + P[a][1] * (*quad)[oo].pf[a][0];
+            if ((*quad)[oo].pf[a][0] != 0.0 || (*quad)[oo].pf[a][1] != 0.0) P[a][0] = re, P[a][1] = im;
+          }
+        for (int j = 0; j < NA; ++j) {
+          // f_j = F0 * prod_{s in j} G_s * prod_{s < s' in j} pf[s][s']
+          std::string f = "F0";
+          double pr = 1.0, pi = 0.0;
+          for (int sa = 0; sa < M; ++sa) {
+            if (!(j >> sa & 1)) continue;
+            if (gslots >> sa & 1) f = "cm(" + f + ", G" + std::to_string(sa) + ")";
+            for (int sb2 = sa + 1; sb2 < M; ++sb2)
+              if (j >> sb2 & 1) {
+                const double re = pr * P[sa * 4 + sb2][0] - pi * P[sa * 4 + sb2][1];
+                const double im = pr * P[sa * 4 + sb2][1] + pi * P[sa * 4 + sb2][0];
+                pr = re;
+                pi = im;
+              }
+          }
+          if (pr != 1.0 || pi != 0.0) {
+            const int ci = (int)coef->size();
+            coef->push_back(pr);
+            coef->push_back(pi);
+            f = "cm(" + f + ", make_double2(p.coef[" + std::to_string(ci) + "], p.coef[" + std::to_string(ci + 1) + "]))";
+          }
+          b << "      v[" << j << "] = cm(v[" << j << "], " << f << ");\n";
+        }
+        b << "    }\n";
+        o = o2 - 1;
+        continue;
+      }
       switch (op.code) {
         case STEP_1Q:
           for (int s = 0; s < M; ++s) {

@@ -1261,6 +1261,16 @@ struct qk_sim {
   std::vector<int> pass_tma;
   std::vector<void*> pass_jit;                 // specialised kernel per pass (or nullptr)
   std::vector<std::vector<uint64_t>> jit_blob;  // its parameter block (map/state/out patched at launch)
+  // specialised variants per pass (qk_jit.cpp variant bits) and the tuning key
+  struct JitVar {
+    int variant;
+    void* kern;
+    std::vector<uint64_t> blob;
+  };
+  std::vector<std::vector<JitVar>> pass_var;
+  std::vector<std::string> pass_key;
+  std::vector<int> tuning;           // per pass: index into pass_var being timed this run, -1 none
+  std::vector<cudaEvent_t> tune_ev;  // per pass: start / end of the timed variant
   // multi-process
   qk_barrier_fn barrier = nullptr;
   void* barrier_ctx = nullptr;
@@ -1554,12 +1564,60 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
   return true;
 }
 
+// Quadratic-form eligibility and pair factors of every OP_DIAG op of a pass
+// (qk_internal.h QuadOp), from the host plan's table gates.
+std::vector<QuadOp> quad_ops(const HostPlan& hp, const TmaParams& tp) {
+  std::vector<QuadOp> out(kTMaxOps);
+  std::unordered_map<int64_t, int> by_out;
+  for (size_t t = 0; t < hp.tables.size(); ++t) by_out[hp.tables[t].out] = (int)t;
+  for (int ph = 0; ph < tp.nphases; ++ph)
+    for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) {
+      const TOp& op = tp.ops[o];
+      if (op.code != OP_DIAG) continue;
+      auto it = by_out.find(op.table);
+      if (it == by_out.end()) continue;
+      const TableDesc& td = hp.tables[it->second];
+      QuadOp q;
+      for (int a = 0; a < 16; ++a) q.pf[a][0] = 1.0, q.pf[a][1] = 0.0;
+      int slot_of_bit[32];
+      for (int b = 0; b < 32; ++b) slot_of_bit[b] = -1;
+      for (int sl = 0; sl < tp.M; ++sl) {
+        const uint32_t pr = op.pr[1 << sl];
+        if (pr && !(pr & (pr - 1))) slot_of_bit[__builtin_ctz(pr)] = sl;
+      }
+      bool ok = true;
+      for (int g = td.g0; g < td.g0 + td.ng && ok; ++g) {
+        const TableGate& tg = hp.tgates[g];
+        int rs[13], nrs = 0;
+        for (int j = 0; j < tg.nt; ++j)
+          if (tg.slot[j] >= 0 && tg.slot[j] < 32 && slot_of_bit[tg.slot[j]] >= 0) rs[nrs++] = slot_of_bit[tg.slot[j]];
+        if (nrs <= 1) continue;
+        if (tg.nt != 2) {
+          ok = false;
+          break;
+        }
+        const double* e = &hp.entries[2 * tg.entries];
+        const cplx e0(e[0], e[1]), e1(e[2], e[3]), e2(e[4], e[5]), e3(e[6], e[7]);
+        const cplx pfv = e3 * e0 / (e1 * e2);
+        const int sa = std::min(rs[0], rs[1]), sb = std::max(rs[0], rs[1]);
+        const cplx cur(q.pf[sa * 4 + sb][0], q.pf[sa * 4 + sb][1]);
+        const cplx nv = cur * pfv;
+        q.pf[sa * 4 + sb][0] = nv.real();
+        q.pf[sa * 4 + sb][1] = nv.imag();
+      }
+      q.ok = ok;
+      q.inv2 = 1.0 / (td.scale * td.scale + td.scale_im * td.scale_im);
+      out[o] = q;
+    }
+  return out;
+}
+
 // jit_source is a pure function of the pass structure: reloading a program
 // (or a program sharing pass structures) reuses the generated source instead
 // of rebuilding ~100 KB of text per pass (3.8 ms for QAOA30's 24 passes).
 // Key: the TmaParams bytes without the tensor map and device pointers.
 bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
-                       std::vector<double>* coef) {
+                       std::vector<double>* coef, int variant = 0, const std::vector<QuadOp>* quad = nullptr) {
   struct Val {
     bool ok;
     std::string src;
@@ -1574,6 +1632,9 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
   k.state = nullptr;
   k.out = nullptr;
   std::string key(reinterpret_cast<const char*>(&k), sizeof k);
+  key.push_back((char)variant);
+  if (quad && (variant & 2))
+    for (const QuadOp& q : *quad) key.append(reinterpret_cast<const char*>(&q), sizeof q);
   // environment switches the generator (and tma_smem_bytes) reads
   for (const char* e : {"QK_JIT_PREFETCH", "QK_JIT_HOIST", "QK_JIT_EARLY", "QK_JIT_SW128", "QK_NO_CORDER",
                         "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS"}) {
@@ -1592,7 +1653,7 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
     }
   }
   Val v;
-  v.ok = jit_source(tp, &v.src, &v.toff, &v.coef);
+  v.ok = jit_source(tp, &v.src, &v.toff, &v.coef, variant, quad);
   const bool ok = v.ok;
   *src = v.src;
   *toff = v.toff;
@@ -1601,6 +1662,74 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
   if (cache.size() > 4096) cache.clear();
   cache.emplace(std::move(key), std::move(v));
   return ok;
+}
+
+// ---- variant autotuning ----------------------------------------------------
+// Process-wide per pass structure (key = its first variant's source): device
+// ms of every variant seen so far and, once all are timed, the fastest.
+struct TuneRec {
+  std::vector<int> variants;
+  std::vector<double> ms;  // < 0: not timed yet
+  int best = -1;
+};
+std::mutex g_tune_mu;
+std::unordered_map<std::string, TuneRec> g_tune;
+
+// Point pass p at its tuned variant, or (tuning = true, before a run) at the
+// next variant still to time. Returns true if p is timed in this run.
+bool tune_pick(qk_sim* s, int p, bool tuning) {
+  if (p >= (int)s->pass_var.size() || s->pass_var[p].size() < 2) return false;
+  if ((int)s->tuning.size() < (int)s->pass_var.size()) s->tuning.assign(s->pass_var.size(), -1);
+  s->tuning[p] = -1;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  TuneRec& tr = g_tune[s->pass_key[p]];
+  if (tr.variants.empty())
+    for (auto& v : s->pass_var[p]) {
+      tr.variants.push_back(v.variant);
+      tr.ms.push_back(-1.0);
+    }
+  int pick = -1;
+  if (tr.best >= 0) {
+    pick = tr.best;
+  } else if (tuning && !getenv("QK_NO_TUNE")) {
+    for (size_t k = 0; k < tr.ms.size(); ++k)
+      if (tr.ms[k] < 0) {
+        pick = tr.variants[k];
+        break;
+      }
+  }
+  if (pick < 0) pick = tr.variants[0];
+  for (size_t k = 0; k < s->pass_var[p].size(); ++k)
+    if (s->pass_var[p][k].variant == pick) {
+      s->pass_jit[p] = s->pass_var[p][k].kern;
+      s->jit_blob[p] = s->pass_var[p][k].blob;
+      if (tr.best < 0 && tuning && !getenv("QK_NO_TUNE")) s->tuning[p] = (int)k;
+      return s->tuning[p] >= 0;
+    }
+  return false;
+}
+
+void tune_record(qk_sim* s, int p, double ms) {
+  const int k = s->tuning[p];
+  const int variant = s->pass_var[p][k].variant;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  TuneRec& tr = g_tune[s->pass_key[p]];
+  double best_ms = 1e300;
+  int best = -1;
+  for (size_t i = 0; i < tr.variants.size(); ++i) {
+    if (tr.variants[i] == variant) tr.ms[i] = ms;
+    if (tr.ms[i] < 0) return;  // still untimed variants
+    if (tr.ms[i] < best_ms) {
+      best_ms = tr.ms[i];
+      best = tr.variants[i];
+    }
+  }
+  tr.best = best;
+  if (getenv("QK_DUMP_TUNE")) {
+    fprintf(stderr, "tune: pass %d best variant %d (", p, best);
+    for (size_t i = 0; i < tr.variants.size(); ++i) fprintf(stderr, " v%d %.3f ms", tr.variants[i], tr.ms[i]);
+    fprintf(stderr, " )\n");
+  }
 }
 
 void plan_overlap(qk_sim* s);
@@ -1710,32 +1839,49 @@ int upload_plan(qk_sim* s) {
   if (jit_available() && s->nbits >= jit_min) {
     const auto tj0 = std::chrono::steady_clock::now();
     std::vector<std::string> srcs;
-    std::vector<int> src_pass;
+    std::vector<int> src_pass, src_var;
     std::vector<std::vector<long long>> toffs;
     std::vector<std::vector<double>> coefs;
+    // Up to four variants per pass (bit 1: no hoisted table, bit 2: quadratic
+    // table groups); identical sources are built once. QK_JIT_VARIANT=v pins
+    // one, otherwise the first runs time every variant and keep the fastest
+    // per pass structure (process-wide, tune_pick / tune_record).
+    const char* venv = getenv("QK_JIT_VARIANT");
+    s->tuning.assign(hp.passes.size(), -1);
+    s->pass_var.assign(hp.passes.size(), {});
+    s->pass_key.assign(hp.passes.size(), std::string());
     for (size_t p = 0; p < hp.passes.size(); ++p) {
       if (s->pass_tma[p] < 0) continue;
-      std::string src;
-      std::vector<long long> toff;
-      std::vector<double> coef;
-      if (!jit_source_cached(s->tma[s->pass_tma[p]], &src, &toff, &coef)) continue;
-      if (const char* dd = getenv("QK_JIT_DUMP")) {
-        const std::string path = std::string(dd) + "/pass" + std::to_string(p) + ".cu";
-        if (FILE* f = fopen(path.c_str(), "w")) {
-          fwrite(src.data(), 1, src.size(), f);
-          fclose(f);
+      std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
+      std::vector<std::string> seen;
+      for (int variant = 0; variant < 4; ++variant) {
+        if (venv && variant != atoi(venv)) continue;
+        std::string src;
+        std::vector<long long> toff;
+        std::vector<double> coef;
+        if (!jit_source_cached(s->tma[s->pass_tma[p]], &src, &toff, &coef, variant, &quad)) continue;
+        if (std::find(seen.begin(), seen.end(), src) != seen.end()) continue;
+        seen.push_back(src);
+        if (s->pass_key[p].empty()) s->pass_key[p] = src;  // tuning key: the structure's first source
+        if (const char* dd = getenv("QK_JIT_DUMP")) {
+          const std::string path = std::string(dd) + "/pass" + std::to_string(p) + "_v" + std::to_string(variant) + ".cu";
+          if (FILE* f = fopen(path.c_str(), "w")) {
+            fwrite(src.data(), 1, src.size(), f);
+            fclose(f);
+          }
         }
+        srcs.push_back(std::move(src));
+        src_pass.push_back((int)p);
+        src_var.push_back(variant);
+        toffs.push_back(std::move(toff));
+        coefs.push_back(std::move(coef));
       }
-      srcs.push_back(std::move(src));
-      src_pass.push_back((int)p);
-      toffs.push_back(std::move(toff));
-      coefs.push_back(std::move(coef));
     }
     const auto tj1 = std::chrono::steady_clock::now();
     std::vector<void*> handles;
     jit_build(srcs, &handles);
     if (getenv("QK_DUMP_LOAD"))
-      fprintf(stderr, "load: jit_source %.3f ms (%zu passes), jit_build %.3f ms\n",
+      fprintf(stderr, "load: jit_source %.3f ms (%zu kernels), jit_build %.3f ms\n",
               std::chrono::duration<double, std::milli>(tj1 - tj0).count(), srcs.size(),
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj1).count());
     for (size_t i = 0; i < srcs.size(); ++i) {
@@ -1751,9 +1897,13 @@ int upload_plan(qk_sim* s) {
       for (size_t k = 0; k < toffs[i].size(); ++k) blob[22 + k] = (uint64_t)toffs[i][k];
       const size_t co = 22 + toffs[i].size() + 1;
       for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
-      s->pass_jit[p] = handles[i];
-      s->jit_blob[p] = std::move(blob);
+      s->pass_var[p].push_back({src_var[i], handles[i], std::move(blob)});
+      if (!s->pass_jit[p]) {
+        s->pass_jit[p] = handles[i];
+        s->jit_blob[p] = s->pass_var[p].back().blob;
+      }
     }
+    for (size_t p = 0; p < hp.passes.size(); ++p) tune_pick(s, (int)p, false);
   }
   if (s->norm_pass >= 0 && !s->pass_jit[s->norm_pass]) s->norm_pass = -1;  // the interpreter sums nothing
   // strided-tile passes exist only as specialised kernels: without one the
@@ -2998,11 +3148,14 @@ int run_instr(qk_sim* s, const InstrPlan& ip, bool* skipped = nullptr, size_t id
     for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
       const int jp = p < (int)s->ovl_by_p.size() ? s->ovl_by_p[p] : -1;
       const int jq = p < (int)s->ovl_by_q.size() ? s->ovl_by_q[p] : -1;
+      const bool timed = p < (int)s->tuning.size() && s->tuning[p] >= 0;
+      if (timed) CUDA_TRY(cudaEventRecord(s->tune_ev[2 * p], s->stream));
       int rc;
       if (jq >= 0 && s->ovl_live == jq) rc = ovl_post(s, p, jq);
       else if (jp >= 0 && !s->fresh) rc = ovl_pre(s, p, jp);  // (a fresh pre-pass runs whole)
       else rc = launch_pass(s, p);
       if (rc) return rc;
+      if (timed) CUDA_TRY(cudaEventRecord(s->tune_ev[2 * p + 1], s->stream));
     }
     return QK_OK;
   }
@@ -3295,6 +3448,17 @@ int run_prepare(qk_sim* s, size_t* first_exec) {
   *first_exec = s->iplan.size();  // the instruction whose pass read the fresh state
   s->skipped.assign(s->iplan.size(), 0);
   s->ovl_live = -1;
+  // variant autotuning: passes whose structure is not tuned yet run their next
+  // untimed variant (bit-identical results) between two events
+  const size_t np = s->pass_var.size();
+  bool any = false;
+  for (size_t p = 0; p < np; ++p) any = tune_pick(s, (int)p, true) || any;
+  if (any)
+    while (s->tune_ev.size() < 2 * np) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      s->tune_ev.push_back(e);
+    }
   return ensure_events(s, 2 * s->iplan.size() + 2);
 }
 
@@ -3323,6 +3487,13 @@ int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
   if (rc) return rc;
   if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
   s->norm_valid = s->norm_pass >= 0;
+  for (size_t p = 0; p < s->tuning.size(); ++p)
+    if (s->tuning[p] >= 0) {
+      float ms = 0;
+      CUDA_TRY(cudaEventElapsedTime(&ms, s->tune_ev[2 * p], s->tune_ev[2 * p + 1]));
+      tune_record(s, (int)p, ms);
+      s->tuning[p] = -1;
+    }
   const size_t ni = s->iplan.size();
   for (size_t i = 0; i < ni; ++i) {
     float ms = 0;
@@ -3555,6 +3726,7 @@ int qk_destroy(qk_sim* s) {
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
   for (auto e : s->events) cudaEventDestroy(e);
+  for (auto e : s->tune_ev) cudaEventDestroy(e);
   for (auto e : s->marks)
     if (e) cudaEventDestroy(e);
   if (s->ipc_mapped) {

@@ -60,12 +60,15 @@ def test_reference_full_size(gpu, name):
           f"norm {nrm!r} vs ref {float(g['norm'])!r}")
     assert err <= TOL, err
     assert abs(nrm - float(g["norm"])) <= 1e-12
-    # a second run on the same handle (continues from the end layout) must
-    # equal a fresh one
-    sim.reset()
-    res = sim.run_loaded(res.final_permutation)
-    again = sim.handle.gather(g["idx"].astype(np.uint64))
-    assert np.array_equal(again, got)
+    # later runs on the same handle (continuing from the end layout; the
+    # autotuner times the other kernel variants of each pass meanwhile) stay
+    # within the tolerance of the reference too
+    for _ in range(4):
+        sim.reset()
+        res = sim.run_loaded(res.final_permutation)
+        again = sim.handle.gather(g["idx"].astype(np.uint64))
+        assert np.max(np.abs(again - g["amps"])) <= TOL
+        assert np.max(np.abs(again - got)) <= 1e-13
     sim.release()
     gc.collect()
 
@@ -165,7 +168,7 @@ def test_kernel_level_entry_points_after_run(gpu):
     assert np.max(np.abs(np.asarray(sim.partitions[0].amps) - host.amps)) <= TOL
     sim.reset()
     again = sim.run_loaded(perm).physical_vector()   # the program survived
-    assert np.array_equal(again, first)
+    assert np.max(np.abs(again - first)) <= 1e-13    # (the autotuner may pick another variant)
     assert abs(sim.handle.sumsq() - 1.0) <= 1e-12
 
 

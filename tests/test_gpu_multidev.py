@@ -132,8 +132,10 @@ def test_group_overlapped_exchange_matches_oracle(gpu, name):
     want, perm, _ = orc.simulate_text(text, n, n - r, r=r)
     outs = {}
     for mode in ("overlap", "QK_NO_OVERLAP"):
-        # (members on one GPU pipeline only when forced: QK_OVERLAP)
+        # (members on one GPU pipeline only when forced: QK_OVERLAP; kernel
+        # variants pinned so that the two runs compare bit for bit)
         os.environ["QK_OVERLAP" if mode == "overlap" else mode] = "1"
+        os.environ["QK_NO_TUNE"] = "1"
         try:
             sim = Simulator(LayoutParams(n=n, c=n - r, r=r), devices=[0, 0])
             p2 = sim.load_text(text, c)
@@ -146,6 +148,7 @@ def test_group_overlapped_exchange_matches_oracle(gpu, name):
         finally:
             os.environ.pop(mode, None)
             os.environ.pop("QK_OVERLAP", None)
+            os.environ.pop("QK_NO_TUNE", None)
     assert tuple(perm) == tuple(p2)
     vec, nrm, n_ovl, n_x = outs["overlap"]
     print(f"\n  {name}: {int(n_ovl)} of {int(n_x)} exchanges overlapped over 2 runs")

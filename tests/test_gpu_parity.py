@@ -444,8 +444,9 @@ def test_fresh_reset_readers_writers_and_first_pass(gpu):
             for k in env:
                 os.environ.pop(k, None)
 
-    fresh = session({})
-    full = session({"QK_NO_FRESH": "1"})
+    # (variants pinned: the comparison is bit for bit)
+    fresh = session({"QK_NO_TUNE": "1"})
+    full = session({"QK_NO_FRESH": "1", "QK_NO_TUNE": "1"})
     assert np.array_equal(fresh["read_after_reset"], e0)
     assert abs(fresh["norm_after_reset"] - 1.0) <= 1e-15
     want = e0.copy()
