@@ -133,6 +133,20 @@ int qk_load_packed(qk_sim* sim, const int32_t* words, size_t nwords,
 int qk_load_gate_by_gate(qk_sim* sim, const int32_t* words, size_t nwords,
                          const double* params, size_t nparams);
 
+/* Cross-block pass schedule of a packed program (host only, no device): the
+ * schedule qk_load_* uses in the lazy layout (qk_runtime.cpp reblock). The
+ * program is rewritten on wires (wire w = start position w, followed through
+ * every SQS/CSQS) and cut into passes of at most `cap` wires; out_words holds
+ * one QK_INS_BLOCK record per pass (targets = wires, no swaps), p2w[q] the
+ * wire at final position q (so the reference's physical bit q is wire
+ * p2w[q]). *npass = 0 when the program cannot be rescheduled (a non-quadratic
+ * diagonal gate, a gate wider than cap - 3 wires, cap > n). Two-call protocol
+ * as qk_parse_text. This replaces no reference interface: it exposes the
+ * execution order of simulator.py:529-555's blocks for the parity tests. */
+int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params, size_t nparams,
+                      int n, int cap, int32_t* out_words, size_t* out_nwords, double* out_params,
+                      size_t* out_nparams, int32_t* p2w, int* npass);
+
 /* Program queries: number of instructions, and the final physical->logical
  * permutation replayed from the swaps (circuit.py:202-210); perm has n ints. */
 int qk_program_info(const qk_sim* sim, int* n_instr, int* n_blocks, int* n_sqs,

@@ -46,6 +46,8 @@ _SIGS = {
     "qk_parse_text": (c_int, [ctypes.c_char_p, c_size, c_int, c_int, c_int, P(c_int32), P(c_size),
                               P(c_dbl), P(c_size), P(c_int)]),
     "qk_load_packed": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
+    "qk_reblock_packed": (c_int, [P(c_int32), c_size, P(c_dbl), c_size, c_int, c_int, P(c_int32),
+                                  P(c_size), P(c_dbl), P(c_size), P(c_int32), P(c_int)]),
     "qk_load_gate_by_gate": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
     "qk_program_info": (c_int, [c_void, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int32)]),
     "qk_run": (c_int, [c_void, P(c_dbl)]),
@@ -197,6 +199,27 @@ def parse_text(text: str, n: int, local: int, c: int):
                          ctypes.byref(npar), ctypes.byref(line))
     check(rc, line.value)
     return words[:nw.value], params[:npar.value]
+
+
+def reblock_packed(words, params, n: int, cap: int):
+    """Cross-block pass schedule (qk_reblock_packed) -> (words, params, p2w, npass);
+    npass 0 when the program cannot be rescheduled."""
+    L = lib()
+    w = np.ascontiguousarray(words, dtype=np.int32)
+    p = np.ascontiguousarray(params, dtype=np.float64)
+    if p.size == 0:
+        p = np.zeros(1)
+    nw, npar, npass = c_size(0), c_size(0), c_int(0)
+    check(L.qk_reblock_packed(iptr(w), w.size, dptr(p), p.size, n, cap, None, ctypes.byref(nw), None,
+                              ctypes.byref(npar), None, ctypes.byref(npass)))
+    if npass.value == 0:
+        return None, None, None, 0
+    ow = np.zeros(max(1, nw.value), dtype=np.int32)
+    op = np.zeros(max(1, npar.value), dtype=np.float64)
+    p2w = np.zeros(n, dtype=np.int32)
+    check(L.qk_reblock_packed(iptr(w), w.size, dptr(p), p.size, n, cap, iptr(ow), ctypes.byref(nw),
+                              dptr(op), ctypes.byref(npar), iptr(p2w), ctypes.byref(npass)))
+    return ow[:nw.value], op[:npar.value], p2w, npass.value
 
 
 def csqs_plan(n: int, r: int, count: int, shard: int, local_set, rank_set):

@@ -38,7 +38,43 @@ enum OpCode : int32_t {
   OP_SWAP = 4,   // swap register slots r0, r1
   OP_DIAG = 5,   // multiply by tables[table + (pt | pr[j])]
   OP_SCALE = 6,  // multiply by the complex coef[0] + i coef[1]
+  OP_QUAD = 7,   // diagonal phase exp(i q(x)) with q quadratic in ALL address bits x (tile and chunk
+                 // bits); `table` = offset (complex entries) of its QuadLayout data in the table
+                 // pool. Specialised kernels only (qk_jit.cpp): the producer warp turns the chunk
+                 // bits into per-position factors, each thread multiplies a few of them.
 };
+
+// Data of one OP_QUAD op (doubles, at tabs + table), for a pass with C chunk
+// positions, M register slots, T = C - M thread bits and NO outer bits:
+//   thr[2^T][1 + M] complex   per thread: w = scale * exp(i sum of the pairs
+//                             among its set thread bits), v_s = exp(i sum over
+//                             its set thread bits of beta(bit, slot s))
+//   pj[2^M] complex           exp(i sum of the pairs among the slots of j)
+//   phi0                      constant angle
+//   at[C]                     linear angle of chunk position l
+//   ao[NO]                    linear angle of chunk-index bit k
+//   bto[C][NO]                pair angle (position l, chunk bit k)
+//   boo[NO][NO]               pair angle (chunk bit k, chunk bit k' < k), row k
+// Per chunk: b_l = exp(i (at[l] + sum_k bto[l][k] x_k)) and
+// b0 = exp(i (phi0 + sum_k x_k (ao[k] + sum_{k'<k} boo[k][k'] x_k'))); a
+// thread's amplitude j gets b0 w prod_{thread bits set} b_l prod_{s in j} (b_R(s) v_s) pj[j].
+struct QuadLayout {
+  int thr, pj, phi0, at, ao, bto, boo, total;  // offsets in doubles
+};
+inline QuadLayout quad_layout(int C, int M, int nouter) {
+  QuadLayout q;
+  const int T = C - M;
+  q.thr = 0;
+  q.pj = q.thr + (1 << T) * (1 + M) * 2;
+  q.phi0 = q.pj + (1 << M) * 2;
+  q.at = q.phi0 + 2;
+  q.ao = q.at + C;
+  q.bto = q.ao + nouter;
+  q.boo = q.bto + C * nouter;
+  q.total = q.boo + nouter * nouter;
+  q.total += q.total & 1;
+  return q;
+}
 
 struct OpDesc {
   int32_t code;
@@ -106,7 +142,7 @@ struct SqsDesc {
 // ---- persistent TMA gate-block pass (contiguous chunks, C in [9, 12], M = 4) ----
 constexpr int kTMaxPh = 12;
 constexpr int kTMaxOps = 64;
-constexpr int kTMaxCoef = 128;
+constexpr int kTMaxCoef = 256;
 
 // step of a TMA phase program. OP_H/OP_X/OP_MAT never appear as steps:
 // consecutive one-qubit gates on distinct register slots are fused into one

@@ -368,6 +368,10 @@ int jit_slice_bytes(const TmaParams& tp) {
   int b = 0;
   for (int e : slice_plan(tp, st)) b += e * 16;
   if (tp.norm) b += 16 * 32 * 8;  // per-warp partial sums of the fused norm
+  int nq = 0;                     // OP_QUAD factors: C + 1 per op per stage
+  for (int ph = 0; ph < tp.nphases; ++ph)
+    for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) nq += tp.ops[o].code == OP_QUAD;
+  b += nq * (tp.C + 1) * 16 * st;
   return b;
 }
 
@@ -386,6 +390,16 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       const TOp& op = tp.ops[o];
       if (op.code == OP_DIAG) toff->push_back(op.table);
     }
+  // OP_QUAD ops: their data offsets follow the tables in toff
+  std::vector<int> qops;
+  for (int ph = 0; ph < tp.nphases; ++ph)
+    for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o)
+      if (tp.ops[o].code == OP_QUAD) qops.push_back(o);
+  const int QT = (int)toff->size(), NQ = (int)qops.size();
+  for (int o : qops) toff->push_back(tp.ops[o].table);
+  const int NO = tp.nbits - C;
+  const QuadLayout QL = quad_layout(C, M, NO);
+  if (NQ && (NO > 32 || C + 1 > 32 || tp.xbits)) return false;
   int ng = 0, st = 0;
   if (tma_smem_bytes(C, M, &ng, &st, tp.smax) < 0) return false;
   // registers: 4 per complex entry, 2^M entries per table; one table for
@@ -435,6 +449,15 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   std::ostringstream ear;  // per-iteration early table loads
   for (size_t t = 0; t < hoisted.size(); ++t)
     if (hoisted[t]) pro << "  double2 tv" << t << "[" << NA << "];\n";
+  // OP_QUAD: a thread's chunk-invariant factors (w, v_s) stay in registers
+  const bool qhoist = NQ <= 2;
+  for (int q = 0; q < NQ && qhoist; ++q) {
+    pro << "  double2 qw" << q << ", qv" << q << "[" << M << "];\n";
+    pro << "  { const double2* qt = p.tabs + p.toff[" << QT + q << "] + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
+    pro << "    qw" << q << " = __ldg(qt);\n";
+    for (int sl = 0; sl < M; ++sl) pro << "    qv" << q << "[" << sl << "] = __ldg(qt + " << 1 + sl << ");\n";
+    pro << "  }\n";
+  }
   const int GT = 1 << T;
   const int consumers = GT * ng;
   const int rows_chunk = 1 << (C - 3);
@@ -653,6 +676,46 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
             if (((j >> op.r0) & 1) && !((j >> op.r1) & 1))
               b << "    xb(v[" << j << "], v[" << (j ^ (1 << op.r0) ^ (1 << op.r1)) << "]);\n";
           break;
+        case OP_QUAD: {
+          // b0 w prod_{thread bits set} b_l, then prod_{s in j} b_R(s) v_s and pj[j]
+          int q = 0;
+          while (qops[q] != o) ++q;
+          int R[4];
+          for (int sl = 0; sl < M; ++sl) R[sl] = __builtin_ctz(D.rloc[1 << sl]);
+          b << "    { const double2* fq = fac + ((u32)s * " << NQ << "u + " << q << "u) * " << C + 1 << "u;\n";
+          b << "      const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";
+          if (qhoist) {
+            b << "      double2 E = cm(fq[" << C << "], qw" << q << ");\n";
+          } else {
+            b << "      const double2* qt = qd + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
+            b << "      double2 E = cm(fq[" << C << "], __ldg(qt));\n";
+          }
+          for (int k = 0; k < T; ++k)
+            b << "      { const double2 f = fq[" << (int)D.tpos[k] << "]; const bool on = (tid >> " << k
+              << ") & 1u; E = cm(E, make_double2(on ? f.x : 1.0, on ? f.y : 0.0)); }\n";
+          for (int sl = 0; sl < M; ++sl) {
+            if (qhoist) b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], qv" << q << "[" << sl << "]);\n";
+            else b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], __ldg(qt + " << 1 + sl << "));\n";
+          }
+          // depth-first over the slots: a stack of M + 1 partial products
+          std::function<void(int, int, const std::string&)> visit = [&](int j, int bit, const std::string& f) {
+            if (bit < 0) {
+              if (__builtin_popcount((unsigned)j) >= 2)
+                b << "      v[" << j << "] = cm(v[" << j << "], cm(" << f << ", __ldg(qd + " << QL.pj / 2 + j << ")));\n";
+              else
+                b << "      v[" << j << "] = cm(v[" << j << "], " << f << ");\n";
+              return;
+            }
+            visit(j, bit - 1, f);
+            const std::string g = "F" + std::to_string(bit);
+            b << "      { const double2 " << g << " = cm(" << f << ", e" << bit << ");\n";
+            visit(j | (1 << bit), bit - 1, g);
+            b << "      }\n";
+          };
+          visit(0, M - 1, "E");
+          b << "    }\n";
+          break;
+        }
         case OP_SCALE: {
           const int ci = (int)coef->size();
           coef->push_back(tp.coef[op.coef]);
@@ -839,6 +902,12 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     else c << "(blockIdx.x + " << iv << " * G < p.nchunks)";
     return c.str();
   };
+  size_t fac_off = 0;
+  {
+    size_t planned = 0;
+    for (int e : slice_plan(tp, st)) planned += (size_t)e * 16;
+    fac_off = (size_t)st * (16u << C) + 16 * st + planned + (tp.norm ? 16 * 32 * 8 : 0);
+  }
   o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n"
     << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
     << "  unsigned char* base = smem_raw;\n"
@@ -852,15 +921,66 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "  const u64 G = gridDim.x;\n"
     << "  const u64 PER = (p.nchunks + G - 1) / G;\n"
     << "  (void)PER;\n"
-    << "  if (threadIdx.x < 32) {\n"
-    << "    if (threadIdx.x == 0) {\n"
-    << "      asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&p.map) : \"memory\");\n"
-    << "      for (u64 i = 0;; ++i) {\n"
-    << "        if (!" << chunk_ok("i") << ") break;\n"
-    << "        const u64 chunk = " << chunk_of("i") << ";\n"
-    << "        const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
-    << "        if (round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
-    << "        mbar_expect_tx(full + s, stage_bytes);\n"
+    << "  double2* fac = (double2*)(base + " << fac_off << "ull);\n"
+    << "  (void)fac;\n";
+  if (!NQ) {
+    o << "  if (threadIdx.x < 32) {\n"
+      << "    if (threadIdx.x == 0) {\n"
+      << "      asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&p.map) : \"memory\");\n"
+      << "      for (u64 i = 0;; ++i) {\n"
+      << "        if (!" << chunk_ok("i") << ") break;\n"
+      << "        const u64 chunk = " << chunk_of("i") << ";\n"
+      << "        const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
+      << "        if (round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n";
+  } else {
+    // OP_QUAD: the whole producer warp turns the chunk bits into the
+    // per-position factors of every quadratic op (stage slot s) before lane 0
+    // arms the stage, so the consumers' full-barrier wait also acquires them
+    o << "  if (threadIdx.x < 32) {\n"
+      << "    const u32 lane = threadIdx.x;\n"
+      << "    if (lane == 0) asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&p.map) : \"memory\");\n"
+      << "    for (u64 i = 0;; ++i) {\n"
+      << "      if (!" << chunk_ok("i") << ") break;\n"
+      << "      const u64 chunk = " << chunk_of("i") << ";\n"
+      << "      const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
+      << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
+      << "      __syncwarp();\n";
+    for (int q = 0; q < NQ; ++q) {
+      o << "      { const double* qd = (const double*)(p.tabs + p.toff[" << QT + q << "]);\n"
+        // boo[k][k'] is 0 for k' >= k: every lane sums a full unrolled row
+        << "        double t = 0.0;\n"
+        << "        if (lane < " << NO << "u) {\n"
+        << "          const double* row = qd + " << QL.boo << " + lane * " << NO << "u;\n"
+        << "          double t0 = __ldg(qd + " << QL.ao << " + lane), t1 = 0.0;\n"
+        << "#pragma unroll\n"
+        << "          for (int k = 0; k < " << NO << "; k += 2) {\n"
+        << "            t0 += ((chunk >> k) & 1ull) ? __ldg(row + k) : 0.0;\n"
+        << "            if (k + 1 < " << NO << ") t1 += ((chunk >> (k + 1)) & 1ull) ? __ldg(row + k + 1) : 0.0;\n"
+        << "          }\n"
+        << "          t = ((chunk >> lane) & 1ull) ? t0 + t1 : 0.0;\n"
+        << "        }\n"
+        << "        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);\n"
+        << "        double a = 0.0;\n"
+        << "        if (lane < " << C << "u) {\n"
+        << "          const double* row = qd + " << QL.bto << " + lane * " << NO << "u;\n"
+        << "          double a0 = __ldg(qd + " << QL.at << " + lane), a1 = 0.0;\n"
+        << "#pragma unroll\n"
+        << "          for (int k = 0; k < " << NO << "; k += 2) {\n"
+        << "            a0 += ((chunk >> k) & 1ull) ? __ldg(row + k) : 0.0;\n"
+        << "            if (k + 1 < " << NO << ") a1 += ((chunk >> (k + 1)) & 1ull) ? __ldg(row + k + 1) : 0.0;\n"
+        << "          }\n"
+        << "          a = a0 + a1;\n"
+        << "        } else if (lane == " << C << "u) {\n"
+        << "          a = __ldg(qd + " << QL.phi0 << ") + t;\n"
+        << "        }\n"
+        << "        if (lane <= " << C << "u) { double sn, cs; sincos(a, &sn, &cs); fac[((u32)s * " << NQ << "u + " << q
+        << "u) * " << C + 1 << "u + lane] = make_double2(cs, sn); }\n"
+        << "      }\n";
+    }
+    o << "      __syncwarp();\n"
+      << "      if (lane == 0) {\n";
+  }
+  o << "        mbar_expect_tx(full + s, stage_bytes);\n"
     << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n";
   const char* pfe = getenv("QK_JIT_PREFETCH");
   if (tp.lazy) {

@@ -72,6 +72,11 @@ struct InstrH {
   int type = 0;  // QK_INS_*
   std::vector<GateH> gates;
   std::vector<int> a, b;
+  // cross-block pass of the scheduler (reblock): targets are wires (start
+  // positions); the tile holds tile_w, and the store puts rows_next on the
+  // row bits 0.. and the next pass's wires on the lowest tile bits after them
+  int rb = 0;
+  std::vector<int> tile_w, rows_next;
 };
 
 // ---------------------------------------------------------------------------
@@ -374,6 +379,8 @@ struct HostPlan {
   std::vector<double> entries;  // complex pairs
   int64_t pool = 0;             // table pool size (complex entries)
   std::vector<SqsDesc> sqs;
+  // OP_QUAD data (qk_internal.h QuadLayout), copied into the pool at upload
+  std::vector<std::pair<int64_t, std::vector<double>>> qcopy;
   void clear() { *this = HostPlan(); }
 };
 
@@ -431,6 +438,57 @@ std::vector<int> order_tpos(const std::vector<int>& T) {
   return out;
 }
 
+// Phase of a diagonal gate as a quadratic form in its target bits:
+// e(x) = exp(i phi(x)), phi(x) = c + sum_j lin[j] x_j + sum_{j<j'} pair[j][j'] x_j x_j'
+// (x_j = the bit of target j; targets[0] is the MSB of the entry index,
+// circuit.py:426-463). RZ, RZZ and CP use their angle directly; D<k> entries
+// must be unit (|e| = 1 to 1e-13) and, for k >= 3, have no Moebius terms of
+// degree >= 3 (mod 2 pi). False otherwise: the gate then stays in a table.
+double wrap_angle(double x) {
+  const double tp = 6.283185307179586476925286766559;
+  return x - tp * std::nearbyint(x / tp);
+}
+
+bool quad_terms(const GateH& g, double* c, double lin[13], double pair[13][13]) {
+  const int nt = (int)g.t.size();
+  if (nt < 1 || nt > 13 || !is_diag(g.kind)) return false;
+  std::vector<double> ph((size_t)1 << nt, 0.0);
+  const double th = g.p.empty() ? 0.0 : g.p[0];
+  if (g.kind == QK_RZ && nt == 1) {
+    ph[0] = -0.5 * th;
+    ph[1] = 0.5 * th;
+  } else if (g.kind == QK_RZZ && nt == 2) {
+    ph[0] = ph[3] = -0.5 * th;
+    ph[1] = ph[2] = 0.5 * th;
+  } else if (g.kind == QK_CP && nt == 2) {
+    ph[3] = th;
+  } else {
+    const std::vector<cplx> e = diag_entries(g);
+    if (e.size() != ph.size()) return false;
+    for (size_t x = 0; x < e.size(); ++x) {
+      if (std::fabs(std::abs(e[x]) - 1.0) > 1e-13) return false;
+      ph[x] = std::arg(e[x]);
+    }
+  }
+  // Moebius transform: ph[m] becomes the coefficient of prod_{b in m} x_b
+  for (int b = 0; b < nt; ++b)
+    for (size_t x = 0; x < ph.size(); ++x)
+      if (x >> b & 1) ph[x] -= ph[x ^ ((size_t)1 << b)];
+  for (size_t m = 0; m < ph.size(); ++m)
+    if (popc(m) >= 3 && std::fabs(wrap_angle(ph[m])) > 1e-12) return false;
+  *c = ph[0];
+  for (int j = 0; j < nt; ++j) {
+    lin[j] = ph[(size_t)1 << (nt - 1 - j)];
+    for (int j2 = j + 1; j2 < nt; ++j2) pair[j][j2] = ph[((size_t)1 << (nt - 1 - j)) | ((size_t)1 << (nt - 1 - j2))];
+  }
+  return true;
+}
+
+bool quad_gate(const GateH& g) {
+  double c, lin[13], pair[13][13];
+  return quad_terms(g, &c, lin, pair);
+}
+
 struct Item {
   int type;  // 0 gate, 1 diag run
   const GateH* g;
@@ -441,7 +499,7 @@ struct Item {
 // vector of `nbits` address bits.
 int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const std::vector<int>& Q,
                  int nbits, uint64_t ncta_override, std::string& emsg, const std::vector<int>* dest = nullptr,
-                 int lanes_req = 5) {
+                 int lanes_req = 5, bool allow_quad = false) {
   // 0. U(th, ph, la) = P(ph) RY(th) P(la) with P(a) = diag(1, e^{ia}) exactly
   //    (circuit.py:420-423 Qiskit form). A run of U gates on distinct qubits
   //    becomes [all P(la)] [all RY] [all P(ph)]: the phase gates join two
@@ -500,6 +558,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
   // blocks folded into this pass): their value is fixed per chunk, so they
   // only add a per-chunk term to the table index (specialised kernels only)
   std::vector<uint64_t> run_outer;
+  // OP_QUAD runs (allow_quad, specialised kernels): every gate's phase is
+  // quadratic, so the run is one op whatever its width and outer bits
+  std::vector<char> run_quad;
   for (const GateH* g : gates) {
     uint32_t tm = 0;
     uint64_t om = 0;
@@ -515,19 +576,23 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
       tm |= 1u << loc[t];
     }
     if (is_diag(g->kind)) {
+      const bool gq = allow_quad && quad_gate(*g);
       const int width = last_run >= 0 ? popc(run_support[last_run] | tm) + popc(run_outer[last_run] | om) : 99;
-      if (last_run >= 0 && !(tm & blocked) && width <= 14 && popc(run_outer[last_run] | om) <= 8) {
+      const bool fits_table = width <= 14 && last_run >= 0 && popc(run_outer[last_run] | om) <= 8;
+      if (last_run >= 0 && !(tm & blocked) && ((gq && run_quad[last_run]) || fits_table)) {
         runs[last_run].push_back(g);
         run_support[last_run] |= tm;
         run_outer[last_run] |= om;
+        run_quad[last_run] = run_quad[last_run] && gq;
       } else {
-        if (popc(om) > 8) {
+        if (popc(om) > 8 && !gq) {
           emsg = "diagonal gate over too many bits outside the chunk";
           return QK_ESIM;
         }
         runs.push_back({g});
         run_support.push_back(tm);
         run_outer.push_back(om);
+        run_quad.push_back(gq);
         last_run = (int)runs.size() - 1;
         blocked = 0;
         items.push_back({1, nullptr, last_run});
@@ -870,14 +935,96 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     return QK_OK;
   };
   // 5. emit phases and ops
+  std::vector<int> O;
+  for (int p = 0; p < nbits; ++p)
+    if (std::find(Q.begin(), Q.end(), p) == Q.end()) O.push_back(p);
+  // OP_QUAD data (qk_internal.h QuadLayout) of run r, applied in a phase whose
+  // thread bits sit at chunk positions Tth and register slots at R
+  auto build_quad = [&](int r, const std::vector<int>& Tth, const std::vector<int>& R, int64_t* out) -> int {
+    const int nO = (int)O.size(), NB = C + nO, TT = (int)Tth.size();
+    int idx[64];
+    for (int& x : idx) x = -1;
+    for (int l = 0; l < C; ++l) idx[Q[l]] = l;
+    for (int k = 0; k < nO; ++k) idx[O[k]] = C + k;
+    std::vector<double> lin(NB, 0.0), pr((size_t)NB * NB, 0.0);
+    double ph0 = 0.0;
+    for (const GateH* g : runs[r]) {
+      double c, li[13], pa[13][13];
+      if (!quad_terms(*g, &c, li, pa)) {
+        emsg = "internal: non-quadratic gate in a quadratic run";
+        return QK_ESIM;
+      }
+      ph0 += c;
+      const int nt = (int)g->t.size();
+      for (int j = 0; j < nt; ++j) {
+        const int a = idx[g->t[j]];
+        if (a < 0) {
+          emsg = "internal: quadratic run target outside the address bits";
+          return QK_ESIM;
+        }
+        lin[a] += li[j];
+        for (int j2 = j + 1; j2 < nt; ++j2) {
+          const int b2 = idx[g->t[j2]];
+          if (b2 == a) lin[a] += pa[j][j2];  // x_a^2 = x_a
+          else pr[(size_t)std::min(a, b2) * NB + std::max(a, b2)] += pa[j][j2];
+        }
+      }
+    }
+    auto P2 = [&](int a, int b2) { return pr[(size_t)std::min(a, b2) * NB + std::max(a, b2)]; };
+    const QuadLayout L = quad_layout(C, M, nO);
+    std::vector<double> d(L.total, 0.0);
+    cplx sc(1.0, 0.0);
+    if (!scale_folded) {
+      sc = scale;
+      scale_folded = true;
+      run_scaled[r] = 1;
+    }
+    for (int tid = 0; tid < (1 << TT); ++tid) {
+      double aw = 0.0;
+      for (int k = 0; k < TT; ++k)
+        if (tid >> k & 1)
+          for (int k2 = k + 1; k2 < TT; ++k2)
+            if (tid >> k2 & 1) aw += P2(Tth[k], Tth[k2]);
+      const cplx w = sc * cexpi(wrap_angle(aw));
+      double* row = &d[L.thr + (size_t)tid * (1 + M) * 2];
+      row[0] = w.real();
+      row[1] = w.imag();
+      for (int sl = 0; sl < M; ++sl) {
+        double av = 0.0;
+        for (int k = 0; k < TT; ++k)
+          if (tid >> k & 1) av += P2(Tth[k], R[sl]);
+        const cplx v = cexpi(wrap_angle(av));
+        row[2 + 2 * sl] = v.real();
+        row[3 + 2 * sl] = v.imag();
+      }
+    }
+    for (int j = 0; j < (1 << M); ++j) {
+      double ap = 0.0;
+      for (int sa = 0; sa < M; ++sa)
+        if (j >> sa & 1)
+          for (int sb = sa + 1; sb < M; ++sb)
+            if (j >> sb & 1) ap += P2(R[sa], R[sb]);
+      const cplx v = cexpi(wrap_angle(ap));
+      d[L.pj + 2 * j] = v.real();
+      d[L.pj + 2 * j + 1] = v.imag();
+    }
+    d[L.phi0] = wrap_angle(ph0);
+    for (int l = 0; l < C; ++l) d[L.at + l] = wrap_angle(lin[l]);
+    for (int k = 0; k < nO; ++k) d[L.ao + k] = wrap_angle(lin[C + k]);
+    for (int l = 0; l < C; ++l)
+      for (int k = 0; k < nO; ++k) d[L.bto + l * nO + k] = wrap_angle(P2(l, C + k));
+    for (int k = 0; k < nO; ++k)
+      for (int k2 = 0; k2 < k; ++k2) d[L.boo + k * nO + k2] = wrap_angle(P2(C + k2, C + k));
+    *out = hp.pool;
+    hp.qcopy.emplace_back(hp.pool, std::move(d));
+    hp.pool += L.total / 2;
+    return QK_OK;
+  };
   PassDesc pd{};
   pd.C = C;
   pd.M = M;
   pd.phase0 = (int)hp.phases.size();
   pd.nphases = (int)phs.size();
-  std::vector<int> O;
-  for (int p = 0; p < nbits; ++p)
-    if (std::find(Q.begin(), Q.end(), p) == Q.end()) O.push_back(p);
   if ((int)O.size() > kMaxOuter) {
     emsg = "too many outer bits";
     return QK_ESIM;
@@ -922,7 +1069,15 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     for (int ii : pb.items) {
       const Item& it = items[ii];
       OpDesc op{};
-      if (it.type == 1) {
+      if (it.type == 1 && run_quad[it.run] && (run_outer[it.run] || popc(run_support[it.run]) > 14)) {
+        // one OP_QUAD for the whole run (tile and chunk bits)
+        std::vector<int> Tth(T.begin(), T.end());
+        int64_t off = 0;
+        int rc = build_quad(it.run, Tth, pb.R, &off);
+        if (rc) return rc;
+        op.code = OP_QUAD;
+        op.table = off;
+      } else if (it.type == 1) {
         const uint32_t S = run_support[it.run];
         if (run_table[it.run] < 0) {
           std::vector<int> order(T.begin(), T.end());
@@ -1538,7 +1693,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
             t.co_k[k] = op.co_k[k];
             t.co_v[k] = op.co_v[k];
           }
-          if (op.nco) tp.needs_jit = 1;
+          if (op.nco || op.code == OP_QUAD) tp.needs_jit = 1;
           if (op.code == OP_SCALE) {
             if (ncoef + 2 > kTMaxCoef) return false;
             tp.coef[ncoef] = hp.coef[op.coef];
@@ -1911,6 +2066,16 @@ int upload_plan(qk_sim* s) {
   for (size_t p = 0; p < hp.passes.size(); ++p)
     if (s->pass_tma[p] >= 0 && s->tma[s->pass_tma[p]].needs_jit && !(p < s->pass_jit.size() && s->pass_jit[p]))
       return fail(QK_ESIM, "folded diagonal block needs the specialised kernel (NVRTC)");
+  for (size_t p = 0; p < hp.passes.size(); ++p) {  // the generic kernels have no OP_QUAD
+    const PassDesc& pd = hp.passes[p];
+    bool quad = false;
+    for (int ph = 0; ph < pd.nphases; ++ph) {
+      const PhaseDesc& D = hp.phases[pd.phase0 + ph];
+      for (int o = D.op_begin; o < D.op_end; ++o) quad = quad || hp.ops[o].code == OP_QUAD;
+    }
+    if (quad && !(s->pass_tma[p] >= 0 && p < s->pass_jit.size() && s->pass_jit[p]))
+      return fail(QK_ESIM, "quadratic diagonal pass needs the specialised kernel (NVRTC)");
+  }
   for (size_t p = 0; p < hp.passes.size(); ++p)
     if (s->pass_tma[p] >= 0 && s->tma[s->pass_tma[p]].lazy && !(p < s->pass_jit.size() && s->pass_jit[p])) {
       const TmaParams& tq = s->tma[s->pass_tma[p]];
@@ -1959,6 +2124,9 @@ int upload_plan(qk_sim* s) {
                                  s->d_pool, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "table build launch failed: %s", cudaGetErrorString((cudaError_t)rc));
   }
+  for (auto& q : hp.qcopy)
+    CUDA_TRY(cudaMemcpyAsync(s->d_pool + 2 * q.first, q.second.data(), q.second.size() * sizeof(double),
+                             cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   return QK_OK;
 }
@@ -2042,7 +2210,245 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
   return oe - ob <= kTMaxOps && ncoef <= kTMaxCoef;
 }
 
-int compile_program(qk_sim* s) {
+// ---- cross-block pass scheduling (lazy layout, every swap in-handle) --------
+// The optimizer cut the circuit into blocks of <= c qubits with SQS between
+// them (optimizer.py); in the lazy layout a swap costs nothing, so the
+// only cost left is one HBM sweep per block. Here the program is rewritten on
+// "wires" (a wire = a start position, followed through every swap) and cut
+// again into passes over tiles of up to `cap` physical bits: a pass applies
+// every non-diagonal gate whose wires are all in its tile and whose
+// predecessors ran, and every diagonal gate whose predecessors ran (the
+// diagonal ones need no tile: OP_QUAD applies a quadratic phase over all
+// address bits). Dependencies: two gates sharing a wire are ordered unless
+// both are diagonal. The tile of a pass is chosen greedily (the wire that lets
+// the most gates run, ties to the earliest waiting gate), with the wires on
+// the row bits 0..rowbits-1 always in it; each pass's store permutation puts
+// wires of the next pass (a lookahead choice) on those row bits. QAOA30 c12
+// (51 blocks, 24 passes after folding) runs in 13 passes, QFT33 c10 in 4.
+// Results equal the block order's up to rounding: only commuting gates move.
+bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std::vector<InstrH>* out,
+             std::vector<int>* p2w_final) {
+  if (nb > 64 || cap > nb) return false;
+  std::vector<int> p2w(nb);
+  for (int q = 0; q < nb; ++q) p2w[q] = q;
+  struct WG {
+    const GateH* g;
+    uint64_t wm;
+    bool diag;
+    std::vector<int> w;  // wire of every target
+  };
+  std::vector<WG> G;
+  for (const InstrH& ins : prog) {
+    if (ins.type == QK_INS_BLOCK) {
+      for (const GateH& g : ins.gates) {
+        WG x{&g, 0, is_diag(g.kind), {}};
+        for (int t : g.t) {
+          if (t < 0 || t >= nb) return false;
+          x.wm |= 1ull << p2w[t];
+          x.w.push_back(p2w[t]);
+        }
+        if (x.diag && !quad_gate(g)) return false;
+        if (!x.diag && popc(x.wm) > cap - rowbits) return false;
+        G.push_back(x);
+      }
+    } else {
+      std::vector<int> sa = ins.a, sb = ins.b;
+      if (sa.size() != sb.size()) return false;
+      for (int q : sa)
+        if (q < 0 || q >= nb) return false;
+      for (int q : sb)
+        if (q < 0 || q >= nb) return false;
+      std::sort(sa.begin(), sa.end());
+      std::sort(sb.begin(), sb.end());
+      for (size_t k = 0; k < sa.size(); ++k) std::swap(p2w[sa[k]], p2w[sb[k]]);
+    }
+  }
+  *p2w_final = p2w;
+  // non-diagonal gates and their non-diagonal predecessors (through diagonal gates)
+  std::vector<int> nd;                       // gate index of every non-diagonal gate
+  std::vector<std::vector<uint64_t>> pre;    // predecessor bitsets over nd
+  std::vector<std::vector<int>> ddep(G.size());  // diagonal gate -> nd predecessors
+  {
+    std::vector<int> last(nb, -1);
+    std::vector<std::vector<int>> dd(nb);
+    for (size_t i = 0; i < G.size(); ++i) {
+      if (G[i].diag) {
+        std::vector<int> deps;
+        for (int w = 0; w < nb; ++w)
+          if ((G[i].wm >> w & 1) && last[w] >= 0) deps.push_back(last[w]);
+        for (int w = 0; w < nb; ++w)
+          if (G[i].wm >> w & 1) dd[w].insert(dd[w].end(), deps.begin(), deps.end());
+        ddep[i] = deps;
+      } else {
+        std::vector<int> p;
+        for (int w = 0; w < nb; ++w)
+          if (G[i].wm >> w & 1) {
+            if (last[w] >= 0) p.push_back(last[w]);
+            p.insert(p.end(), dd[w].begin(), dd[w].end());
+          }
+        const int k = (int)nd.size();
+        nd.push_back((int)i);
+        pre.emplace_back();
+        for (int x : p) {
+          if ((int)pre[k].size() <= x / 64) pre[k].resize(x / 64 + 1, 0);
+          pre[k][x / 64] |= 1ull << (x % 64);
+        }
+        for (int w = 0; w < nb; ++w)
+          if (G[i].wm >> w & 1) {
+            last[w] = k;
+            dd[w].clear();
+          }
+      }
+    }
+  }
+  const int N = (int)nd.size();
+  const size_t NW = (size_t)N / 64 + 1;
+  std::vector<uint64_t> done(NW, 0);
+  auto isdone = [&](const std::vector<uint64_t>& d, int k) { return (d[k / 64] >> (k % 64)) & 1; };
+  // the non-diagonal gates a tile S can run now (in program order)
+  auto closure = [&](uint64_t S, std::vector<uint64_t>& now, int* cnt) {
+    now = done;
+    int c = 0;
+    for (int k = 0; k < N; ++k) {
+      if (isdone(now, k) || (G[nd[k]].wm & ~S)) continue;
+      bool ok = true;
+      for (size_t w = 0; w < pre[k].size() && ok; ++w) ok = !(pre[k][w] & ~now[w]);
+      if (!ok) continue;
+      now[k / 64] |= 1ull << (k % 64);
+      ++c;
+    }
+    *cnt = c;
+  };
+  auto choose = [&](uint64_t forced) {
+    uint64_t S = forced;
+    std::vector<int> pend(nb, INT32_MAX);
+    for (int k = N - 1; k >= 0; --k)
+      if (!isdone(done, k))
+        for (int w = 0; w < nb; ++w)
+          if (G[nd[k]].wm >> w & 1) pend[w] = k;
+    std::vector<uint64_t> tmp;
+    while (popc(S) < cap) {
+      int best = -1, bc = -1;
+      for (int w = 0; w < nb; ++w) {
+        if ((S >> w & 1) || pend[w] == INT32_MAX) continue;
+        int c = 0;
+        closure(S | (1ull << w), tmp, &c);
+        if (c > bc || (c == bc && pend[w] < pend[best])) {
+          bc = c;
+          best = w;
+        }
+      }
+      if (best < 0) break;
+      S |= 1ull << best;
+    }
+    return S;
+  };
+  std::vector<int> wire_at(nb);  // physical bit -> wire (the layout the passes see)
+  for (int q = 0; q < nb; ++q) wire_at[q] = q;
+  std::vector<int> npass(N, -1);
+  std::vector<uint64_t> tiles;
+  std::vector<std::vector<int>> rows_after;
+  uint64_t forced = 0;
+  for (int r = 0; r < rowbits; ++r) forced |= 1ull << wire_at[r];
+  int left = N;
+  while (left > 0) {
+    const uint64_t S = choose(forced);
+    std::vector<uint64_t> now;
+    int c = 0;
+    closure(S, now, &c);
+    if (!c) return false;
+    for (int k = 0; k < N; ++k)
+      if (isdone(now, k) && !isdone(done, k)) npass[k] = (int)tiles.size();
+    done = now;
+    left -= c;
+    tiles.push_back(S);
+    // row bits after this pass: wires the next pass (lookahead) wants that the
+    // tile holds; rows whose wire the next pass wants keep it
+    std::vector<int> rows(rowbits);
+    for (int r = 0; r < rowbits; ++r) rows[r] = wire_at[r];
+    if (left > 0) {
+      const uint64_t S2 = choose(0);
+      std::vector<char> keep(rowbits, 0);
+      uint64_t placed = 0;
+      for (int r = 0; r < rowbits; ++r)
+        if (S2 >> rows[r] & 1) keep[r] = 1, placed |= 1ull << rows[r];
+      uint64_t cand = S & S2 & ~placed;
+      for (int r = 0; r < rowbits && cand; ++r) {
+        if (keep[r]) continue;
+        const int w = __builtin_ctzll(cand);
+        cand &= cand - 1;
+        rows[r] = w;
+      }
+    }
+    rows_after.push_back(rows);
+    // the layout after the pass: only the row assignment matters here
+    std::vector<int> pos(nb);
+    for (int q = 0; q < nb; ++q) pos[wire_at[q]] = q;
+    for (int r = 0; r < rowbits; ++r) {
+      const int w = rows[r], from = pos[w], displaced = wire_at[r];
+      wire_at[r] = w;
+      wire_at[from] = displaced;
+      pos[w] = r;
+      pos[displaced] = from;
+    }
+    forced = 0;
+    for (int r = 0; r < rowbits; ++r) forced |= 1ull << wire_at[r];
+  }
+  if (tiles.empty()) {  // only diagonal gates: one pass over the row bits
+    tiles.push_back(forced);
+    rows_after.push_back(std::vector<int>(wire_at.begin(), wire_at.begin() + rowbits));
+  }
+  // pass of every gate: non-diagonal from the schedule, diagonal = the latest
+  // pass among its predecessors (0 if none)
+  std::vector<int> gpass(G.size(), 0);
+  for (int k = 0; k < N; ++k) gpass[nd[k]] = npass[k];
+  for (size_t i = 0; i < G.size(); ++i)
+    if (G[i].diag)
+      for (int k : ddep[i]) gpass[i] = std::max(gpass[i], npass[k]);
+  out->assign(tiles.size(), InstrH());
+  for (size_t p = 0; p < tiles.size(); ++p) {
+    InstrH& b = (*out)[p];
+    b.type = QK_INS_BLOCK;
+    b.rb = 1;
+    for (int w = 0; w < nb; ++w)
+      if (tiles[p] >> w & 1) b.tile_w.push_back(w);
+    b.rows_next = rows_after[p];
+  }
+  // gates in program order, each diagonal one moved down to just before the
+  // first later non-diagonal gate of its pass that shares a wire (the end if
+  // none), so the kernels see few, large diagonal runs
+  std::vector<std::vector<int>> pg(tiles.size());
+  for (size_t i = 0; i < G.size(); ++i) pg[gpass[i]].push_back((int)i);
+  for (size_t p = 0; p < tiles.size(); ++p) {
+    const std::vector<int>& v = pg[p];
+    std::vector<int> tail;
+    std::vector<std::vector<int>> before(v.size());
+    for (size_t a = 0; a < v.size(); ++a) {
+      if (!G[v[a]].diag) continue;
+      size_t dl = v.size();
+      for (size_t c2 = a + 1; c2 < v.size(); ++c2)
+        if (!G[v[c2]].diag && (G[v[c2]].wm & G[v[a]].wm)) {
+          dl = c2;
+          break;
+        }
+      (dl == v.size() ? tail : before[dl]).push_back(v[a]);
+    }
+    std::vector<int> order;
+    for (size_t a = 0; a < v.size(); ++a) {
+      for (int i : before[a]) order.push_back(i);
+      if (!G[v[a]].diag) order.push_back(v[a]);
+    }
+    order.insert(order.end(), tail.begin(), tail.end());
+    for (int i : order) {
+      GateH g = *G[i].g;
+      g.t = G[i].w;
+      (*out)[p].gates.push_back(std::move(g));
+    }
+  }
+  return true;
+}
+
+int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
   const auto tc0 = std::chrono::steady_clock::now();
   struct PlanTimer {
     std::chrono::steady_clock::time_point t0;
@@ -2095,6 +2501,38 @@ int compile_program(qk_sim* s) {
   const bool lazy = lazy_ok && all_chunked && (!s->bufs[1] || relabel) &&
                     (Cg <= 10 || (Cg <= 12 && !getenv("QK_NO_LAZY12")));
   if (lazy) relabel = false;
+  // cross-block pass scheduling (reblock): lazy layout, every swap inside
+  // the handle, every diagonal gate quadratic; checked up front so the
+  // reference's errors (swap ranges, CSQS contract) still come from the loop
+  std::vector<InstrH> rprog;
+  std::vector<int> rb_p2w;
+  *reblocked = false;
+  if (try_reblock && lazy && !getenv("QK_NO_FOLD")) {
+    bool ok = true;
+    for (auto& ins : s->prog) {
+      if (ins.type == QK_INS_SQS) {
+        for (int q : ins.a) ok = ok && q >= 0 && q < s->L;
+        for (int q : ins.b) ok = ok && q >= 0 && q < s->L;
+      } else if (ins.type == QK_INS_CSQS) {
+        ok = ok && check_csqs(s, ins.a, ins.b) == QK_OK;
+        for (int q : ins.b) ok = ok && q - s->L < nb - s->L;
+      }
+    }
+    const char* cenv = getenv("QK_REBLOCK_CAP");
+    if (ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w)) {
+      // worth it only with fewer sweeps than the block order (one per block
+      // that is not diagonal-only; those fold into the pass before)
+      size_t sweeps = 0;
+      for (auto& ins : s->prog) {
+        if (ins.type != QK_INS_BLOCK || ins.gates.empty()) continue;
+        bool dg = true;
+        for (auto& g : ins.gates) dg = dg && is_diag(g.kind);
+        sweeps += !dg;
+      }
+      *reblocked = rprog.size() < std::max<size_t>(sweeps, 1) || getenv("QK_REBLOCK");
+    }
+  }
+  const std::vector<InstrH>& prog = *reblocked ? rprog : s->prog;
   auto emit_restore = [&]() {
     std::vector<std::pair<int, int>> rounds[2];
     restore_rounds(sigma, rounds);
@@ -2151,7 +2589,7 @@ int compile_program(qk_sim* s) {
   };
   std::vector<int> ident(nb);
   for (int q = 0; q < nb; ++q) ident[q] = q;
-  std::vector<char> fused(s->prog.size(), 0);
+  std::vector<char> fused(prog.size(), 0);
   auto diag_block = [&](const InstrH& b) {
     if (b.type != QK_INS_BLOCK || b.gates.empty()) return false;
     for (auto& g : b.gates) {
@@ -2164,15 +2602,15 @@ int compile_program(qk_sim* s) {
   const bool lazy_fold = lazy && !getenv("QK_NO_FOLD");
   const bool fold_eager = !s->gbg && !getenv("QK_NO_FOLD") && jit_available() && nb >= (jenv ? atoi(jenv) : 20);
   const bool merge_sqs = !relabel && !lazy && !getenv("QK_NO_SQS_MERGE");
-  std::vector<int> folded_into(s->prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
+  std::vector<int> folded_into(prog.size(), -1);  // lazy mode: diagonal block -> absorbing pass
   auto remap = [&](const InstrH& ins) {
     InstrH m = ins;
     for (auto& g : m.gates)
       for (int& t : g.t) t = sigma[t];
     return m;
   };
-  for (size_t ii = 0; ii < s->prog.size(); ++ii) {
-    auto& ins = s->prog[ii];
+  for (size_t ii = 0; ii < prog.size(); ++ii) {
+    auto& ins = prog[ii];
     InstrPlan ip;
     ip.type = ins.type;
     // eager mode: a run of swaps (diagonal blocks folded away in between) is
@@ -2192,12 +2630,20 @@ int compile_program(qk_sim* s) {
         // bring the block's qubits down first
         std::vector<char> inP(nb, 0);
         std::vector<int> P;
-        for (auto& g : ins.gates)
-          for (int t : g.t)
-            if (t >= 0 && t < nb && !inP[sigma[t]]) {
-              inP[sigma[t]] = 1;
-              P.push_back(sigma[t]);
+        if (ins.rb) {
+          for (int w : ins.tile_w)
+            if (!inP[sigma[w]]) {
+              inP[sigma[w]] = 1;
+              P.push_back(sigma[w]);
             }
+        } else {
+          for (auto& g : ins.gates)
+            for (int t : g.t)
+              if (t >= 0 && t < nb && !inP[sigma[t]]) {
+                inP[sigma[t]] = 1;
+                P.push_back(sigma[t]);
+              }
+        }
         int c3 = 0;
         for (int p = 0; p < nb; ++p) c3 += inP[p] || p < 3;
         std::vector<int> T3;
@@ -2207,7 +2653,7 @@ int compile_program(qk_sim* s) {
         for (size_t x = 0; x < T3.size() && x < 16; ++x) tb3[x] = (uint8_t)T3[x];
         TileDims td3{};
         const bool fits = T3.size() <= 13 && tile_dims(tb3, (int)T3.size(), nb, &td3, 3);
-        if (!fits && Cg > 10 && !getenv("QK_NO_FIXUP")) {
+        if (!fits && (Cg > 10 || ins.rb) && !getenv("QK_NO_FIXUP")) {
           std::sort(P.begin(), P.end());
           if (!emit_fixup(P, std::min(nb, std::max(12, (int)P.size()))))
             return fail(QK_ESIM, "internal: layout fix-up failed");
@@ -2219,9 +2665,11 @@ int compile_program(qk_sim* s) {
       for (auto& g : mapped.gates)
         for (int t : g.t) {
           if (t < 0 || t >= nb) return fail(QK_ESIM, "gate target %d beyond local range", t);
+          if (ins.rb) continue;  // the scheduler's tile: diagonal targets may stay outside
           inT[t] = 1;
           maxt = std::max(maxt, t);
         }
+      for (int w : ins.tile_w) inT[sigma[w]] = 1;
       // row bits: 0..2 (128-B rows); when that makes a 13-bit tile (one
       // 128-KiB stage) and 0..1 keeps it at 12, take 64-B rows and 3 stages,
       // unless the tile spans many 2-MiB pages (address bits >= 17): its 1024
@@ -2261,8 +2709,8 @@ int compile_program(qk_sim* s) {
         std::vector<int> sig2 = sigma;
         size_t jj = ii + 1;
         bool ok = true;
-        for (; jj < s->prog.size(); ++jj) {
-          const InstrH& nx = s->prog[jj];
+        for (; jj < prog.size(); ++jj) {
+          const InstrH& nx = prog[jj];
           if (nx.type == QK_INS_BLOCK) {
             if (!nx.gates.empty() && !(lazy_fold && diag_block(nx))) break;
             continue;
@@ -2279,9 +2727,33 @@ int compile_program(qk_sim* s) {
           std::sort(sb.begin(), sb.end());
           for (size_t k = 0; k < sa.size(); ++k) std::swap(sig2[sa[k]], sig2[sb[k]]);
         }
-        if (ok && jj < s->prog.size() && !getenv("QK_NO_LAZY_PERM")) {
+        if (ins.rb && !getenv("QK_NO_LAZY_PERM")) {
+          // the scheduler's rows: rows_next on bits 0.., then the next pass's
+          // tile wires, then the rest, each group in ascending bit order,
+          // onto the tile's bits in ascending order
+          std::vector<char> used(nb, 0), nxt(nb, 0);
+          if (jj < prog.size())
+            for (int w : prog[jj].tile_w) nxt[sigma[w]] = 1;
+          std::vector<int> srcs;
+          bool rows_ok = true;
+          for (int w : ins.rows_next) {
+            const int p0 = sigma[w];
+            rows_ok = rows_ok && inT[p0] && !used[p0];
+            if (!rows_ok) break;
+            used[p0] = 1;
+            srcs.push_back(p0);
+          }
+          if (rows_ok && (int)srcs.size() <= (inT[2] ? 3 : 2)) {
+            for (int x : T)
+              if (!used[x] && nxt[x]) used[x] = 1, srcs.push_back(x);
+            for (int x : T)
+              if (!used[x]) used[x] = 1, srcs.push_back(x);
+            dphys = ident;
+            for (size_t k = 0; k < T.size(); ++k) dphys[srcs[k]] = T[k];
+          }
+        } else if (ok && jj < prog.size() && !getenv("QK_NO_LAZY_PERM")) {
           std::vector<char> need(nb, 0);
-          for (auto& g : s->prog[jj].gates)
+          for (auto& g : prog[jj].gates)
             for (int t : g.t)
               if (t >= 0 && t < nb) need[sig2[t]] = 1;
           std::vector<int> want, low;
@@ -2367,8 +2839,8 @@ int compile_program(qk_sim* s) {
           for (int q = 0; q < nb; ++q) dinv[dphys[q]] = q;
           std::vector<int> sig3(nb);
           for (int q = 0; q < nb; ++q) sig3[q] = dphys[sigma[q]];
-          for (size_t j = ii + 1; j < s->prog.size(); ++j) {
-            const InstrH& nx = s->prog[j];
+          for (size_t j = ii + 1; j < prog.size(); ++j) {
+            const InstrH& nx = prog[j];
             if (nx.type == QK_INS_BLOCK) {
               if (nx.gates.empty()) continue;
               if (!diag_block(nx)) break;
@@ -2394,7 +2866,9 @@ int compile_program(qk_sim* s) {
         for (auto& g : mapped.gates) gs.push_back(&g);
         for (auto& g : folded) gs.push_back(&g);
         ip.pass0 = (int)s->hp.passes.size();
-        int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys, inT[2] ? 3 : 2);
+        int rc = compile_pass(s->hp, gs, T, nb, 0, emsg, &dphys, inT[2] ? 3 : 2, ins.rb != 0);
+        if (ins.rb && !rc && !tma_plan_ok(s->hp, ip.pass0, nb, 13))
+          return fail(QK_ESIM, "reblock: pass %d does not fit the specialised kernel", ip.pass0);
         if (!rc && !folded.empty() && !tma_plan_ok(s->hp, ip.pass0, nb, 13)) {
           // too many ops for one specialised pass: the folded blocks run on their own
           s->hp.passes.resize(ip.pass0);
@@ -2420,6 +2894,7 @@ int compile_program(qk_sim* s) {
         continue;
       }
       // contiguous chunk: the standard pass; a tile the TMA view cannot take: restore first
+      if (ins.rb) return fail(QK_ESIM, "reblock: tile of pass %zu does not fit the TMA view", ii);
       if (!contiguous && !emit_restore()) return fail(QK_ESIM, "internal: layout restore failed");
     }
     if (ins.type == QK_INS_BLOCK) {
@@ -2435,8 +2910,8 @@ int compile_program(qk_sim* s) {
         // so it needs no chunk of its own (targets mapped back through the
         // swaps before it; bits outside this chunk add a per-chunk table term).
         std::vector<GateH> folded;
-        for (size_t j = ii + 1; j < s->prog.size(); ++j) {
-          const InstrH& nx = s->prog[j];
+        for (size_t j = ii + 1; j < prog.size(); ++j) {
+          const InstrH& nx = prog[j];
           if (nx.type == QK_INS_BLOCK && fold && !nx.gates.empty()) {
             bool diag = true;
             for (auto& g : nx.gates) {
@@ -2453,7 +2928,7 @@ int compile_program(qk_sim* s) {
             continue;
           }
           if (!(nx.type == QK_INS_SQS && !nx.a.empty())) break;
-          std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
+          std::vector<int> a = prog[j].a, b = prog[j].b;
           bool ok = true;
           for (int q : a) ok = ok && q >= 0 && q < s->L;
           for (int q : b) ok = ok && q >= 0 && q < s->L;
@@ -2497,8 +2972,8 @@ int compile_program(qk_sim* s) {
           std::vector<int> P2(nb);
           for (int q = 0; q < nb; ++q) P2[q] = q;
           size_t j = ii + 1;
-          for (; j < s->prog.size() && s->prog[j].type == QK_INS_SQS && !s->prog[j].a.empty(); ++j) {
-            std::vector<int> a = s->prog[j].a, b = s->prog[j].b;
+          for (; j < prog.size() && prog[j].type == QK_INS_SQS && !prog[j].a.empty(); ++j) {
+            std::vector<int> a = prog[j].a, b = prog[j].b;
             bool ok = true;
             for (int q : a) ok = ok && q >= 0 && q < s->L;
             for (int q : b) ok = ok && q >= 0 && q < s->L;
@@ -2575,7 +3050,7 @@ int compile_program(qk_sim* s) {
             const int block_idx = (int)s->iplan.size() - 1;
             for (size_t j = ii + 1; j < best_j; ++j) {
               InstrPlan fp;
-              fp.type = s->prog[j].type;  // SQS, or a folded diagonal block (no pass)
+              fp.type = prog[j].type;  // SQS, or a folded diagonal block (no pass)
               fp.fused_by = block_idx;
               s->iplan.push_back(std::move(fp));
             }
@@ -2597,8 +3072,8 @@ int compile_program(qk_sim* s) {
         for (int q = 0; q < nb; ++q) P[q] = q;
         std::vector<GateH> folded;
         std::vector<size_t> folded_at;
-        for (size_t j = ii + 1; j < s->prog.size(); ++j) {
-          const InstrH& nx = s->prog[j];
+        for (size_t j = ii + 1; j < prog.size(); ++j) {
+          const InstrH& nx = prog[j];
           if (nx.type == QK_INS_BLOCK) {
             if (nx.gates.empty()) continue;
             if (!diag_block(nx)) break;
@@ -2737,6 +3212,11 @@ int compile_program(qk_sim* s) {
   // lazy and relabel modes: the handle keeps the end layout (readbacks map
   // through it, writers and the next run restore it); QK_RELABEL_RESTORE
   // restores it with a final permuted pass instead
+  if (*reblocked) {  // sigma is indexed by wire: final position q holds wire rb_p2w[q]
+    std::vector<int> ns(nb);
+    for (int q = 0; q < nb; ++q) ns[q] = sigma[rb_p2w[q]];
+    sigma = ns;
+  }
   s->oop_sqs = relabel;
   s->lay_final = ident;
   if (lazy || (relabel && !getenv("QK_RELABEL_RESTORE"))) {
@@ -2792,6 +3272,14 @@ int compile_program(qk_sim* s) {
     fprintf(stderr, "load: upload_plan %.3f ms\n",
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
   return urc;
+}
+
+int compile_program(qk_sim* s) {
+  bool rb = false;
+  const int rc = compile_program_impl(s, !getenv("QK_NO_REBLOCK"), &rb);
+  if (rc == QK_OK || !rb) return rc;
+  if (getenv("QK_DUMP_PLAN")) fprintf(stderr, "reblock: plan failed (%s), block order instead\n", g_err.c_str());
+  return compile_program_impl(s, false, &rb);
 }
 
 int ensure_events(qk_sim* s, size_t n) {
@@ -3390,6 +3878,39 @@ int create_common(int n, int r, int b, int device, int rank_lo, int count, qk_si
   s->pair_epoch.assign(s->nshards, 0);
   *out = s;
   return QK_OK;
+}
+
+// packed form of a program (qk_load_packed / qk_parse_text): per instruction
+// its type; a block then has its gate count and per gate kind, #targets,
+// targets, #params (params go to the double array); a swap has its size and
+// both sets. Gate ids follow after a -1 sentinel and their count.
+void pack_prog(const std::vector<InstrH>& prog, std::vector<int32_t>* wp, std::vector<double>* pp) {
+  std::vector<int32_t>& w = *wp;
+  std::vector<double>& p = *pp;
+  for (auto& ins : prog) {
+    w.push_back(ins.type);
+    if (ins.type == QK_INS_BLOCK) {
+      w.push_back((int32_t)ins.gates.size());
+      for (auto& g : ins.gates) {
+        w.push_back(g.kind);
+        w.push_back((int32_t)g.t.size());
+        for (int t : g.t) w.push_back(t);
+        w.push_back((int32_t)g.p.size());
+        p.insert(p.end(), g.p.begin(), g.p.end());
+      }
+    } else {
+      w.push_back((int32_t)ins.a.size());
+      w.insert(w.end(), ins.a.begin(), ins.a.end());
+      w.insert(w.end(), ins.b.begin(), ins.b.end());
+    }
+  }
+  std::vector<int32_t> ids;
+  for (auto& ins : prog)
+    if (ins.type == QK_INS_BLOCK)
+      for (auto& g : ins.gates) ids.push_back((int32_t)g.gid);
+  w.push_back(-1);
+  w.push_back((int32_t)ids.size());
+  w.insert(w.end(), ids.begin(), ids.end());
 }
 
 std::vector<InstrH> unpack(const int32_t* w, size_t nw, const double* p, size_t np, int* rc_out,
@@ -4154,6 +4675,36 @@ int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64
   return QK_OK;
 }
 
+int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params, size_t nparams, int n, int cap,
+                      int32_t* out_words, size_t* out_nwords, double* out_params, size_t* out_nparams,
+                      int32_t* p2w, int* npass) {
+  if (!words || !out_nwords || !out_nparams || !npass || n < 1 || n > 64) return fail(QK_EINVAL, "bad argument");
+  int rc = 0;
+  std::string emsg;
+  std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
+  if (rc) return fail(rc, "%s", emsg.c_str());
+  std::vector<InstrH> out;
+  std::vector<int> pw;
+  if (!reblock(prog, n, cap, 3, &out, &pw)) {
+    *npass = 0;
+    return QK_OK;
+  }
+  std::vector<int32_t> w;
+  std::vector<double> p;
+  pack_prog(out, &w, &p);
+  if (out_words) {
+    if (*out_nwords < w.size() || *out_nparams < p.size()) return fail(QK_EINVAL, "buffers too small");
+    memcpy(out_words, w.data(), w.size() * 4);
+    if (!p.empty()) memcpy(out_params, p.data(), p.size() * 8);
+    if (p2w)
+      for (int q = 0; q < n; ++q) p2w[q] = pw[q];
+  }
+  *out_nwords = w.size();
+  *out_nparams = p.size();
+  *npass = (int)out.size();
+  return QK_OK;
+}
+
 int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t* words, size_t* nwords,
                   double* params, size_t* nparams, int* err_line) {
   if (!nwords || !nparams || (!text && len)) return fail(QK_EINVAL, "null argument");
@@ -4168,33 +4719,7 @@ int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t
   }
   std::vector<int32_t> w;
   std::vector<double> p;
-  for (auto& ins : prog) {
-    w.push_back(ins.type);
-    if (ins.type == QK_INS_BLOCK) {
-      w.push_back((int32_t)ins.gates.size());
-      for (auto& g : ins.gates) {
-        w.push_back(g.kind);
-        w.push_back((int32_t)g.t.size());
-        for (int t : g.t) w.push_back(t);
-        w.push_back((int32_t)g.p.size());
-        p.insert(p.end(), g.p.begin(), g.p.end());
-        // gate id rides after the packed program: kept in a side channel below
-      }
-    } else {
-      w.push_back((int32_t)ins.a.size());
-      w.insert(w.end(), ins.a.begin(), ins.a.end());
-      w.insert(w.end(), ins.b.begin(), ins.b.end());
-    }
-  }
-  // gate ids (one per gate, in order) are appended after the program words,
-  // preceded by a sentinel record type -1 and their count
-  std::vector<int32_t> ids;
-  for (auto& ins : prog)
-    if (ins.type == QK_INS_BLOCK)
-      for (auto& g : ins.gates) ids.push_back((int32_t)g.gid);
-  w.push_back(-1);
-  w.push_back((int32_t)ids.size());
-  w.insert(w.end(), ids.begin(), ids.end());
+  pack_prog(prog, &w, &p);
   if (words) {
     if (*nwords < w.size() || *nparams < p.size()) return fail(QK_EINVAL, "buffers too small");
     memcpy(words, w.data(), w.size() * 4);
