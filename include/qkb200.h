@@ -147,6 +147,16 @@ int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params,
                       int n, int cap, int32_t* out_words, size_t* out_nwords, double* out_params,
                       size_t* out_nparams, int32_t* p2w, int* npass);
 
+/* Host-only planning (development and CPU tests; replaces no reference
+ * interface): parse `text` for an n-qubit single-rank state and run the
+ * planner exactly as qk_load_text would on a B200 (second_buffer: the state
+ * has room for the out-of-place buffer, n <= 32 on one B200), without any
+ * device. The plan summary goes to stderr; with dump_dir != NULL every pass's
+ * specialised kernel source is written there (pass<p>_v<variant>.cu) for
+ * offline NVRTC/nvcc builds. *npass = passes planned. */
+int qk_plan_dry(const char* text, size_t len, int n, int c, int second_buffer, const char* dump_dir,
+                int* npass);
+
 /* Program queries: number of instructions, and the final physical->logical
  * permutation replayed from the swaps (circuit.py:202-210); perm has n ints. */
 int qk_program_info(const qk_sim* sim, int* n_instr, int* n_blocks, int* n_sqs,

@@ -46,6 +46,7 @@ _SIGS = {
     "qk_parse_text": (c_int, [ctypes.c_char_p, c_size, c_int, c_int, c_int, P(c_int32), P(c_size),
                               P(c_dbl), P(c_size), P(c_int)]),
     "qk_load_packed": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
+    "qk_plan_dry": (c_int, [ctypes.c_char_p, c_size, c_int, c_int, c_int, ctypes.c_char_p, P(c_int)]),
     "qk_reblock_packed": (c_int, [P(c_int32), c_size, P(c_dbl), c_size, c_int, c_int, P(c_int32),
                                   P(c_size), P(c_dbl), P(c_size), P(c_int32), P(c_int)]),
     "qk_load_gate_by_gate": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
@@ -199,6 +200,15 @@ def parse_text(text: str, n: int, local: int, c: int):
                          ctypes.byref(npar), ctypes.byref(line))
     check(rc, line.value)
     return words[:nw.value], params[:npar.value]
+
+
+def plan_dry(text: str, n: int, c: int, second_buffer: bool = True, dump_dir: str | None = None) -> int:
+    """Host-only plan of a circuit (qk_plan_dry) -> number of passes."""
+    raw = text.encode()
+    npass = c_int(0)
+    check(lib().qk_plan_dry(raw, len(raw), n, c, int(second_buffer),
+                            dump_dir.encode() if dump_dir else None, ctypes.byref(npass)))
+    return npass.value
 
 
 def reblock_packed(words, params, n: int, cap: int):

@@ -1451,6 +1451,10 @@ struct qk_sim {
   int ovl_live = -1;
   int overlap = 0;  // pipeline exchanges with their neighbour passes (peers on other GPUs; qk_set_overlap)
   std::vector<unsigned long long> pair_epoch;  // device barrier meetings per peer shard
+  // host-only planning (qk_plan_dry): no device memory, tensor maps or kernel
+  // builds; upload_plan stops after writing the generated pass sources
+  bool dry = false;
+  std::string dry_dir;
 };
 
 constexpr size_t kFlagBytes = 4096;  // 64 shards x 8 B, padded
@@ -1491,6 +1495,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
   const int slot = __builtin_ctz((unsigned)box_rows) - 3;  // 8..256 -> 0..5
   if (slot < 0 || slot > 5 || !s->bufs[buf]) return nullptr;
+  if (s->dry) return &s->maps[buf][slot];
   if (!s->map_ok[buf][slot]) {
     auto fn = encode_fn();
     if (!fn || s->nbits < 3) return nullptr;
@@ -1550,9 +1555,12 @@ int ensure_full(qk_sim* s) {
 }
 
 // N-D strided view of `buf` for the tile of a lazy pass (qk_internal.h tile_dims)
+bool g_dry_maps = false;  // qk_plan_dry: tensor maps are not encoded (no driver needed)
+
 bool encode_lazy_map(const TmaParams& tp, double* buf, CUtensorMap* out) {
   TileDims td{};
   if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return false;
+  if (g_dry_maps) return true;
   auto fn = encode_fn();
   if (!fn || !buf) return false;
   cuuint64_t dims[5];
@@ -1889,7 +1897,10 @@ void tune_record(qk_sim* s, int p, double ms) {
 
 void plan_overlap(qk_sim* s);
 
+int upload_plan_dry(qk_sim* s);
+
 int upload_plan(qk_sim* s) {
+  if (s->dry) return upload_plan_dry(s);
   HostPlan& hp = s->hp;
   std::vector<char> buf;
   const size_t o_pass = push_section(buf, hp.passes);
@@ -2128,6 +2139,60 @@ int upload_plan(qk_sim* s) {
     CUDA_TRY(cudaMemcpyAsync(s->d_pool + 2 * q.first, q.second.data(), q.second.size() * sizeof(double),
                              cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return QK_OK;
+}
+
+// qk_plan_dry: the TMA parameters and specialised sources of every pass,
+// written to s->dry_dir (pass<p>_v<variant>.cu) with a one-line summary per
+// pass on stderr; nothing touches a device.
+int upload_plan_dry(qk_sim* s) {
+  HostPlan& hp = s->hp;
+  g_dry_maps = true;
+  s->tma.clear();
+  s->pass_tma.assign(hp.passes.size(), -1);
+  std::vector<const std::vector<int>*> pass_dest(hp.passes.size(), nullptr), pass_x(hp.passes.size(), nullptr),
+      pass_tile(hp.passes.size(), nullptr);
+  for (auto& ip : s->iplan) {
+    if (ip.type == QK_INS_BLOCK && ip.npass > 0 && !ip.dest.empty()) {
+      pass_dest[ip.pass0 + ip.npass - 1] = &ip.dest;
+      pass_x[ip.pass0 + ip.npass - 1] = &ip.xspec;
+    }
+    if (ip.type == QK_INS_BLOCK && ip.npass == 1 && !ip.tile.empty()) pass_tile[ip.pass0] = &ip.tile;
+  }
+  for (size_t p = 0; p < hp.passes.size(); ++p) {
+    TmaParams tp;
+    if (make_tma(s, hp.passes[p], tp, pass_dest[p], pass_x[p], pass_tile[p])) {
+      s->pass_tma[p] = (int)s->tma.size();
+      s->tma.push_back(tp);
+    }
+  }
+  g_dry_maps = false;
+  for (size_t p = 0; p < hp.passes.size(); ++p) {
+    const PassDesc& pd = hp.passes[p];
+    int cnt[8] = {0};
+    for (int ph = 0; ph < pd.nphases; ++ph) {
+      const PhaseDesc& D = hp.phases[pd.phase0 + ph];
+      for (int o = D.op_begin; o < D.op_end; ++o) cnt[hp.ops[o].code & 7]++;
+    }
+    fprintf(stderr, "dry pass %zu: C=%d phases=%d tma=%d H=%d MAT=%d CX=%d DIAG=%d QUAD=%d tile=", p, pd.C,
+            pd.nphases, s->pass_tma[p] >= 0, cnt[OP_H], cnt[OP_MAT], cnt[OP_CX], cnt[OP_DIAG], cnt[OP_QUAD]);
+    if (pass_tile[p])
+      for (int t : *pass_tile[p]) fprintf(stderr, "%d,", t);
+    fprintf(stderr, "\n");
+    if (s->pass_tma[p] < 0 || s->dry_dir.empty()) continue;
+    std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
+    for (int variant = 0; variant < 4; ++variant) {
+      std::string src;
+      std::vector<long long> toff;
+      std::vector<double> coef;
+      if (!jit_source_cached(s->tma[s->pass_tma[p]], &src, &toff, &coef, variant, &quad)) continue;
+      const std::string path = s->dry_dir + "/pass" + std::to_string(p) + "_v" + std::to_string(variant) + ".cu";
+      if (FILE* f = fopen(path.c_str(), "w")) {
+        fwrite(src.data(), 1, src.size(), f);
+        fclose(f);
+      }
+    }
+  }
   return QK_OK;
 }
 
@@ -2405,6 +2470,45 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   for (size_t i = 0; i < G.size(); ++i)
     if (G[i].diag)
       for (int k : ddep[i]) gpass[i] = std::max(gpass[i], npass[k]);
+  // Latest pass a diagonal gate may run in: that of its first non-diagonal
+  // successor on any of its wires (the last pass if none). A pass's tail —
+  // the diagonal gates no later non-diagonal gate of the pass touches —
+  // moves to the next pass when every gate of it would be tail there too:
+  // it then joins that pass's tail run instead of costing a run of its own
+  // (QAOA: the next layer's phases among a pass's own wires stop being a
+  // 12-bit table in front of the store).
+  {
+    const int P = (int)tiles.size();
+    std::vector<int> latest(G.size(), P - 1);
+    std::vector<int> next_nd(nb, -1);  // scanning backwards: next non-diagonal gate per wire
+    for (int i = (int)G.size() - 1; i >= 0; --i) {
+      if (G[i].diag) {
+        for (int w = 0; w < nb; ++w)
+          if ((G[i].wm >> w & 1) && next_nd[w] >= 0) latest[i] = std::min(latest[i], gpass[next_nd[w]]);
+      } else {
+        for (int w = 0; w < nb; ++w)
+          if (G[i].wm >> w & 1) next_nd[w] = i;
+      }
+    }
+    if (!getenv("QK_NO_TAIL_MOVE"))
+      for (int p = 0; p + 1 < P; ++p) {
+        std::vector<int> tail;
+        uint64_t later = 0;  // wires of non-diagonal gates of pass p after the scan point
+        bool all = true;
+        for (int i = (int)G.size() - 1; i >= 0; --i) {
+          if (gpass[i] != p) continue;
+          if (!G[i].diag) {
+            later |= G[i].wm;
+            continue;
+          }
+          if (G[i].wm & later) continue;  // a later gate of the pass needs it first
+          tail.push_back(i);
+          all = all && latest[i] > p + 1;
+        }
+        if (all)
+          for (int i : tail) gpass[i] = p + 1;
+      }
+  }
   out->assign(tiles.size(), InstrH());
   for (size_t p = 0; p < tiles.size(); ++p) {
     InstrH& b = (*out)[p];
@@ -4320,6 +4424,30 @@ int qk_load_text(qk_sim* s, const char* text, size_t len, int c, int* n_instr) {
   if (rc) return rc;
   if (n_instr) *n_instr = (int)s->prog.size();
   return QK_OK;
+}
+
+int qk_plan_dry(const char* text, size_t len, int n, int c, int second_buffer, const char* dump_dir, int* npass) {
+  if ((!text && len) || n < 1 || n > 48) return fail(QK_EINVAL, "bad argument");
+  qk_sim s;
+  s.dry = true;
+  s.n = n;
+  s.L = n;
+  s.nbits = n;
+  s.amps = (size_t)1 << n;
+  static double fake[2];
+  s.bufs[0] = &fake[0];  // never dereferenced: planning only tests them for presence
+  s.bufs[1] = second_buffer ? &fake[1] : nullptr;
+  s.state = s.bufs[0];
+  if (dump_dir) s.dry_dir = dump_dir;
+  Parser ps;
+  ps.n = n;
+  ps.local = n;
+  ps.c = c;
+  if (ps.run(text, len, &s.prog)) return fail(ps.code, "%s", ps.msg.c_str());
+  const int rc = compile_program(&s);
+  if (npass) *npass = (int)s.hp.passes.size();
+  s.bufs[0] = s.bufs[1] = s.state = nullptr;
+  return rc;
 }
 
 int qk_load_packed(qk_sim* s, const int32_t* words, size_t nwords, const double* params, size_t nparams) {

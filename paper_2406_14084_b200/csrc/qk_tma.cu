@@ -334,7 +334,10 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax) {
   // each stage belongs to exactly one consumer group (S % NG == 0), so a
   // group never waits on a stage more than one mbarrier phase ahead
   int S = (int)(kSmemBudget / stage);
-  S = (S / NG) * NG;
+  // Stages are taken in chunk order by whichever group owns the chunk, so a
+  // stage's barrier never runs more than one phase ahead of its waiter even
+  // when S is not a multiple of NG (QK_NG2: 2 groups of 256 on 3 stages)
+  if (!(NG == 2 && C == 12 && getenv("QK_NG2") && !getenv("QK_NG2_EVEN"))) S = (S / NG) * NG;
   if (S > 4 * NG) S = 4 * NG;
   if (const char* e = getenv("QK_SMAX")) smax = atoi(e);
   if (smax > 0) S = std::max(std::min(S, smax), NG);
