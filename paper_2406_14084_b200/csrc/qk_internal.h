@@ -42,6 +42,11 @@ enum OpCode : int32_t {
                  // bits); `table` = offset (complex entries) of its QuadLayout data in the table
                  // pool. Specialised kernels only (qk_jit.cpp): the producer warp turns the chunk
                  // bits into per-position factors, each thread multiplies a few of them.
+  OP_QLITE = 8,  // OP_QUAD of a run inside the tile (no chunk bits): every factor is chunk-invariant;
+                 // data = QuadLayout(C, M, 0) with thr[tid] = (E(tid), e_s(tid)) already holding
+                 // the linear angles and the pass scale; pr[0] = slots with e_s != 1, pr[1] = the
+                 // register amplitudes j whose pj[j] != 1, pr[2] = 1: constants only (pj[j]
+                 // holds the whole factor), 2: E == 1 (specialised kernels only)
 };
 
 // Data of one OP_QUAD op (doubles, at tabs + table), for a pass with C chunk

@@ -371,7 +371,7 @@ int jit_slice_bytes(const TmaParams& tp) {
   int nq = 0;                     // OP_QUAD factors: C + 1 per op per stage
   for (int ph = 0; ph < tp.nphases; ++ph)
     for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) nq += tp.ops[o].code == OP_QUAD;
-  b += nq * (tp.C + 1) * 16 * st;
+  b += nq * (tp.C + 1 + 32 + (1 << std::max(0, tp.C - tp.M - 5))) * 16 * st;
   return b;
 }
 
@@ -390,16 +390,24 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       const TOp& op = tp.ops[o];
       if (op.code == OP_DIAG) toff->push_back(op.table);
     }
-  // OP_QUAD ops: their data offsets follow the tables in toff
-  std::vector<int> qops;
+  // OP_QUAD / OP_QLITE ops: their data offsets follow the tables in toff;
+  // only OP_QUAD has per-chunk factors (fac slots, numbered by qfac)
+  std::vector<int> qops, qfac;
+  int NQ = 0;
   for (int ph = 0; ph < tp.nphases; ++ph)
     for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o)
-      if (tp.ops[o].code == OP_QUAD) qops.push_back(o);
-  const int QT = (int)toff->size(), NQ = (int)qops.size();
+      if (tp.ops[o].code == OP_QUAD || tp.ops[o].code == OP_QLITE) {
+        qops.push_back(o);
+        qfac.push_back(tp.ops[o].code == OP_QUAD ? NQ++ : -1);
+      }
+  const int QT = (int)toff->size();
   for (int o : qops) toff->push_back(tp.ops[o].table);
   const int NO = tp.nbits - C;
-  const QuadLayout QL = quad_layout(C, M, NO);
-  if (NQ && (NO > 32 || C + 1 > 32 || tp.xbits)) return false;
+  const QuadLayout QL = quad_layout(C, M, NO), QL0 = quad_layout(C, M, 0);
+  // per OP_QUAD and stage: b_l (C), b0, then the products of b over the lane
+  // thread bits (32 entries) and over the warp thread bits times b0
+  const int FS = C + 1 + 32 + (1 << std::max(0, C - M - 5));
+  if ((NQ || !qops.empty()) && (NO > 32 || C + 1 > 32 || tp.xbits)) return false;
   int ng = 0, st = 0;
   if (tma_smem_bytes(C, M, &ng, &st, tp.smax) < 0) return false;
   // registers: 4 per complex entry, 2^M entries per table; one table for
@@ -449,14 +457,27 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   std::ostringstream ear;  // per-iteration early table loads
   for (size_t t = 0; t < hoisted.size(); ++t)
     if (hoisted[t]) pro << "  double2 tv" << t << "[" << NA << "];\n";
-  // OP_QUAD: a thread's chunk-invariant factors (w, v_s) stay in registers
-  const bool qhoist = NQ <= 2;
-  for (int q = 0; q < NQ && qhoist; ++q) {
-    pro << "  double2 qw" << q << ", qv" << q << "[" << M << "];\n";
-    pro << "  { const double2* qt = p.tabs + p.toff[" << QT + q << "] + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
-    pro << "    qw" << q << " = __ldg(qt);\n";
-    for (int sl = 0; sl < M; ++sl) pro << "    qv" << q << "[" << sl << "] = __ldg(qt + " << 1 + sl << ");\n";
-    pro << "  }\n";
+  // OP_QUAD / OP_QLITE: a thread's chunk-invariant factors (w or E, and the
+  // active slots' v_s / e_s) stay in registers while they fit (~24 registers)
+  std::vector<char> qhoisted(qops.size(), 0);
+  {
+    // (measured spill-free: one OP_QUAD hoisted; with many OP_QLITE only ~8)
+    const char* qb = getenv("QK_QHOIST");
+    int budget = qb ? atoi(qb) : ((int)qops.size() > NQ ? 8 : 20);
+    for (size_t q = 0; q < qops.size(); ++q) {
+      const TOp& op = tp.ops[qops[q]];
+      const int act = op.code == OP_QUAD ? M : __builtin_popcount(op.pr[0] & ((1u << M) - 1));
+      const int regs = 4 * (1 + act);
+      if (regs > budget) continue;
+      budget -= regs;
+      qhoisted[q] = 1;
+      pro << "  double2 qw" << q << ", qv" << q << "[" << M << "];\n";
+      pro << "  { const double2* qt = p.tabs + p.toff[" << QT + q << "] + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
+      pro << "    qw" << q << " = __ldg(qt);\n";
+      for (int sl = 0; sl < M; ++sl)
+        if (op.code == OP_QUAD || (op.pr[0] >> sl & 1)) pro << "    qv" << q << "[" << sl << "] = __ldg(qt + " << 1 + sl << ");\n";
+      pro << "  }\n";
+    }
   }
   const int GT = 1 << T;
   const int consumers = GT * ng;
@@ -676,25 +697,82 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
             if (((j >> op.r0) & 1) && !((j >> op.r1) & 1))
               b << "    xb(v[" << j << "], v[" << (j ^ (1 << op.r0) ^ (1 << op.r1)) << "]);\n";
           break;
+        case OP_QLITE: {
+          // E(tid) prod_{active s in j} e_s(tid), times pj[j] where it is not 1
+          int q = 0;
+          while (qops[q] != o) ++q;
+          const uint32_t act = op.pr[0] & ((1u << M) - 1), pjm = op.pr[1];
+          b << "    { const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";
+          if (op.pr[2] == 1) {  // constants per register amplitude
+            for (int jj = 0; jj < NA; ++jj)
+              if (pjm >> jj & 1) b << "      v[" << jj << "] = cm(v[" << jj << "], __ldg(qd + " << QL0.pj / 2 + jj << "));\n";
+            b << "    }\n";
+            break;
+          }
+          const bool e_one = op.pr[2] == 2;
+          if (e_one) {
+            for (int sl = 0; sl < M; ++sl)
+              if (act >> sl & 1) {
+                if (qhoisted[q]) b << "      const double2 e" << sl << " = qv" << q << "[" << sl << "];\n";
+                else b << "      const double2 e" << sl << " = __ldg(qd + " << QL0.thr / 2 << " + tid * " << 1 + M << "u + " << 1 + sl << ");\n";
+              }
+          } else if (qhoisted[q]) {
+            b << "      const double2 E = qw" << q << ";\n";
+            for (int sl = 0; sl < M; ++sl)
+              if (act >> sl & 1) b << "      const double2 e" << sl << " = qv" << q << "[" << sl << "];\n";
+          } else {
+            b << "      const double2* qt = qd + " << QL0.thr / 2 << " + tid * " << 1 + M << "u;\n";
+            b << "      const double2 E = __ldg(qt);\n";
+            for (int sl = 0; sl < M; ++sl)
+              if (act >> sl & 1) b << "      const double2 e" << sl << " = __ldg(qt + " << 1 + sl << ");\n";
+          }
+          // partial products over the active slots, depth-first ("" = exactly 1)
+          std::function<void(int, int, const std::string&)> visit = [&](int j, int bit, const std::string& f) {
+            if (bit < 0) {
+              // every amplitude whose active bits are j (the inactive slots vary freely)
+              for (int jj = 0; jj < NA; ++jj) {
+                if ((uint32_t)(jj & (int)act) != (uint32_t)j) continue;
+                const std::string pjv = "__ldg(qd + " + std::to_string(QL0.pj / 2 + jj) + ")";
+                std::string m;
+                if (pjm >> jj & 1) m = f.empty() ? pjv : "cm(" + f + ", " + pjv + ")";
+                else m = f;
+                if (!m.empty()) b << "      v[" << jj << "] = cm(v[" << jj << "], " << m << ");\n";
+              }
+              return;
+            }
+            if (!(act >> bit & 1)) {
+              visit(j, bit - 1, f);
+              return;
+            }
+            visit(j, bit - 1, f);
+            const std::string g = "F" + std::to_string(bit);
+            b << "      { const double2 " << g << " = "
+              << (f.empty() ? "e" + std::to_string(bit) : "cm(" + f + ", e" + std::to_string(bit) + ")") << ";\n";
+            visit(j | (1 << bit), bit - 1, g);
+            b << "      }\n";
+          };
+          visit(0, M - 1, e_one ? "" : "E");
+          b << "    }\n";
+          break;
+        }
         case OP_QUAD: {
           // b0 w prod_{thread bits set} b_l, then prod_{s in j} b_R(s) v_s and pj[j]
           int q = 0;
           while (qops[q] != o) ++q;
+          const int qf = qfac[q];
           int R[4];
           for (int sl = 0; sl < M; ++sl) R[sl] = __builtin_ctz(D.rloc[1 << sl]);
-          b << "    { const double2* fq = fac + ((u32)s * " << NQ << "u + " << q << "u) * " << C + 1 << "u;\n";
+          b << "    { const double2* fq = fac + ((u32)s * " << NQ << "u + " << qf << "u) * " << FS << "u;\n";
           b << "      const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";
-          if (qhoist) {
-            b << "      double2 E = cm(fq[" << C << "], qw" << q << ");\n";
+          b << "      const double2 Bt = cm(fq[" << C + 1 << " + (tid & 31u)], fq[" << C + 33 << " + (tid >> 5)]);\n";
+          if (qhoisted[q]) {
+            b << "      double2 E = cm(Bt, qw" << q << ");\n";
           } else {
             b << "      const double2* qt = qd + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
-            b << "      double2 E = cm(fq[" << C << "], __ldg(qt));\n";
+            b << "      double2 E = cm(Bt, __ldg(qt));\n";
           }
-          for (int k = 0; k < T; ++k)
-            b << "      { const double2 f = fq[" << (int)D.tpos[k] << "]; const bool on = (tid >> " << k
-              << ") & 1u; E = cm(E, make_double2(on ? f.x : 1.0, on ? f.y : 0.0)); }\n";
           for (int sl = 0; sl < M; ++sl) {
-            if (qhoist) b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], qv" << q << "[" << sl << "]);\n";
+            if (qhoisted[q]) b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], qv" << q << "[" << sl << "]);\n";
             else b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], __ldg(qt + " << 1 + sl << "));\n";
           }
           // depth-first over the slots: a stack of M + 1 partial products
@@ -945,8 +1023,10 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "      const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
       << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
       << "      __syncwarp();\n";
-    for (int q = 0; q < NQ; ++q) {
-      o << "      { const double* qd = (const double*)(p.tabs + p.toff[" << QT + q << "]);\n"
+    for (size_t qi = 0; qi < qops.size(); ++qi) {
+      if (qfac[qi] < 0) continue;
+      const int q = qfac[qi];
+      o << "      { const double* qd = (const double*)(p.tabs + p.toff[" << QT + (int)qi << "]);\n"
         // boo[k][k'] is 0 for k' >= k: every lane sums a full unrolled row
         << "        double t = 0.0;\n"
         << "        if (lane < " << NO << "u) {\n"
@@ -973,8 +1053,24 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         << "        } else if (lane == " << C << "u) {\n"
         << "          a = __ldg(qd + " << QL.phi0 << ") + t;\n"
         << "        }\n"
-        << "        if (lane <= " << C << "u) { double sn, cs; sincos(a, &sn, &cs); fac[((u32)s * " << NQ << "u + " << q
-        << "u) * " << C + 1 << "u + lane] = make_double2(cs, sn); }\n"
+        << "        double2* fs = fac + ((u32)s * " << NQ << "u + " << q << "u) * " << FS << "u;\n"
+        << "        if (lane <= " << C << "u) { double sn, cs; sincos(a, &sn, &cs); fs[lane] = make_double2(cs, sn); }\n"
+        << "        __syncwarp();\n";
+      // products over the thread bits of the phase that applies the op
+      int oph = 0;
+      while (!(qops[qi] >= tp.ph[oph].op_begin && qops[qi] < tp.ph[oph].op_end)) ++oph;
+      const uint8_t* tpos = tp.ph[oph].tpos;
+      const int TB = C - M;
+      o << "        { double2 x = make_double2(1.0, 0.0);\n";
+      for (int k = 0; k < 5 && k < TB; ++k)
+        o << "          { const double2 f = fs[" << (int)tpos[k] << "]; const bool on = (lane >> " << k
+          << ") & 1u; x = cm(x, make_double2(on ? f.x : 1.0, on ? f.y : 0.0)); }\n";
+      o << "          fs[" << C + 1 << " + lane] = x; }\n";
+      o << "        if (lane < " << (1 << std::max(0, TB - 5)) << "u) { double2 y = fs[" << C << "];\n";
+      for (int k = 5; k < TB; ++k)
+        o << "          { const double2 f = fs[" << (int)tpos[k] << "]; const bool on = (lane >> " << k - 5
+          << ") & 1u; y = cm(y, make_double2(on ? f.x : 1.0, on ? f.y : 0.0)); }\n";
+      o << "          fs[" << C + 33 << " + lane] = y; }\n"
         << "      }\n";
     }
     o << "      __syncwarp();\n"

@@ -816,6 +816,92 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     return 0;
   };
   if (!sched.empty() && sched.size() + extra(sched) < phs.size() + extra(phs)) phs.swap(sched);
+  // Quadratic runs of one phase (allow_quad): the parts of each run that no
+  // later gate of the phase needs first — gates whose tile targets are thread
+  // bits or slots no later gate of the phase acts on — commute with the rest
+  // of the phase and gather in one run at its end. QFT's controlled-phase
+  // ladders then cost one op per phase plus the slot pairs that must stay
+  // between their H gates, instead of one op per H.
+  if (allow_quad && !getenv("QK_NO_PHASE_MERGE")) {
+    auto recompute = [&](int r) {
+      uint32_t tm = 0;
+      uint64_t om = 0;
+      bool q = true;
+      for (const GateH* g : runs[r]) {
+        q = q && quad_gate(*g);
+        for (int t : g->t) {
+          if (loc[t] >= 0) tm |= 1u << loc[t];
+          else om |= 1ull << t;
+        }
+      }
+      run_support[r] = tm;
+      run_outer[r] = om;
+      run_quad[r] = q;
+    };
+    for (auto& pb : phs) {
+      std::vector<size_t> qi;
+      for (size_t k = 0; k < pb.items.size(); ++k) {
+        const Item& it = items[pb.items[k]];
+        if (it.type == 1 && run_quad[it.run]) qi.push_back(k);
+      }
+      if (qi.size() < 2) continue;
+      // slots a later item of the phase acts on, per item position
+      std::vector<uint32_t> later(pb.items.size() + 1, 0);
+      for (size_t k = pb.items.size(); k-- > 0;) {
+        later[k] = later[k + 1];
+        for (int q : needs(items[pb.items[k]])) later[k] |= 1u << q;
+      }
+      std::vector<const GateH*> moved;
+      std::vector<std::vector<const GateH*>> stay(qi.size());
+      for (size_t a = 0; a < qi.size(); ++a) {
+        const int r = items[pb.items[qi[a]]].run;
+        for (const GateH* g : runs[r]) {
+          bool mov = true;
+          for (int t : g->t)
+            if (loc[t] >= 0 && (later[qi[a] + 1] >> loc[t] & 1)) mov = false;
+          (mov ? moved : stay[a]).push_back(g);
+        }
+      }
+      // cost of a run: per-thread factors (thread bits or chunk bits in it) or
+      // constants only (every target a slot of the phase)
+      uint32_t slots = 0;
+      for (int q : pb.R) slots |= 1u << q;
+      auto cost = [&](const std::vector<const GateH*>& v) {
+        if (v.empty()) return 0;
+        int c = 1;
+        for (const GateH* g : v)
+          for (int t : g->t) {
+            if (loc[t] < 0) return 6;
+            if (!(slots >> loc[t] & 1)) c = 3;
+          }
+        return c;
+      };
+      int before = 0, after = cost(moved);
+      for (size_t a = 0; a < qi.size(); ++a) {
+        before += cost(runs[items[pb.items[qi[a]]].run]);
+        after += cost(stay[a]);
+      }
+      if (moved.empty() || after >= before) continue;
+      std::vector<int> keep;
+      std::vector<char> drop(pb.items.size(), 0);
+      for (size_t a = 0; a < qi.size(); ++a) {
+        const int r = items[pb.items[qi[a]]].run;
+        runs[r] = stay[a];
+        if (stay[a].empty()) drop[qi[a]] = 1;
+        else recompute(r);
+      }
+      for (size_t k = 0; k < pb.items.size(); ++k)
+        if (!drop[k]) keep.push_back(pb.items[k]);
+      runs.push_back(moved);
+      run_support.push_back(0);
+      run_outer.push_back(0);
+      run_quad.push_back(true);
+      recompute((int)runs.size() - 1);
+      items.push_back({1, nullptr, (int)runs.size() - 1});
+      keep.push_back((int)items.size() - 1);
+      pb.items = keep;
+    }
+  }
   if (getenv("QK_DUMP_PHASES")) {
     fprintf(stderr, "pass C=%d dest=%d lanes:", C, dest ? 1 : 0);
     for (int q = 0; q < C; ++q)
@@ -1020,6 +1106,119 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     hp.pool += L.total / 2;
     return QK_OK;
   };
+  // OP_QLITE data of a run inside the tile: per thread E = scale * exp(i (phi0 +
+  // linear terms of its set thread bits + their pairs)) and e_s = exp(i (linear
+  // term of slot s + pairs with its set thread bits)); pj as for OP_QUAD.
+  // masks: slots whose e_s differs from 1 for some thread, j whose pj != 1.
+  auto build_qlite = [&](int r, const std::vector<int>& Tth, const std::vector<int>& R, int64_t* out,
+                         uint16_t* slot_mask, uint16_t* pj_mask, uint16_t* flags) -> int {
+    const int TT = (int)Tth.size();
+    std::vector<double> lin(C, 0.0), pr((size_t)C * C, 0.0);
+    double ph0 = 0.0;
+    for (const GateH* g : runs[r]) {
+      double c, li[13], pa[13][13];
+      if (!quad_terms(*g, &c, li, pa)) {
+        emsg = "internal: non-quadratic gate in a quadratic run";
+        return QK_ESIM;
+      }
+      ph0 += c;
+      const int nt = (int)g->t.size();
+      for (int j = 0; j < nt; ++j) {
+        const int a = loc[g->t[j]];
+        if (a < 0) {
+          emsg = "internal: tile quadratic run target outside the tile";
+          return QK_ESIM;
+        }
+        lin[a] += li[j];
+        for (int j2 = j + 1; j2 < nt; ++j2) {
+          const int b2 = loc[g->t[j2]];
+          if (b2 == a) lin[a] += pa[j][j2];
+          else pr[(size_t)std::min(a, b2) * C + std::max(a, b2)] += pa[j][j2];
+        }
+      }
+    }
+    auto P2 = [&](int a, int b2) { return pr[(size_t)std::min(a, b2) * C + std::max(a, b2)]; };
+    const QuadLayout L = quad_layout(C, M, 0);
+    std::vector<double> d(L.total, 0.0);
+    cplx sc(1.0, 0.0);
+    if (!scale_folded) {
+      sc = scale;
+      scale_folded = true;
+      run_scaled[r] = 1;
+    }
+    *slot_mask = 0;
+    *pj_mask = 0;
+    for (int tid = 0; tid < (1 << TT); ++tid) {
+      double ae = ph0;
+      for (int k = 0; k < TT; ++k)
+        if (tid >> k & 1) {
+          ae += lin[Tth[k]];
+          for (int k2 = k + 1; k2 < TT; ++k2)
+            if (tid >> k2 & 1) ae += P2(Tth[k], Tth[k2]);
+        }
+      const cplx e = sc * cexpi(wrap_angle(ae));
+      double* row = &d[L.thr + (size_t)tid * (1 + M) * 2];
+      row[0] = e.real();
+      row[1] = e.imag();
+      for (int sl = 0; sl < M; ++sl) {
+        double av = lin[R[sl]];
+        for (int k = 0; k < TT; ++k)
+          if (tid >> k & 1) av += P2(Tth[k], R[sl]);
+        av = wrap_angle(av);
+        if (av != 0.0) *slot_mask |= (uint16_t)(1u << sl);
+        const cplx v = cexpi(av);
+        row[2 + 2 * sl] = v.real();
+        row[3 + 2 * sl] = v.imag();
+      }
+    }
+    for (int j = 0; j < (1 << M); ++j) {
+      double ap = 0.0;
+      for (int sa = 0; sa < M; ++sa)
+        if (j >> sa & 1)
+          for (int sb = sa + 1; sb < M; ++sb)
+            if (j >> sb & 1) ap += P2(R[sa], R[sb]);
+      ap = wrap_angle(ap);
+      if (ap != 0.0) *pj_mask |= (uint16_t)(1u << j);
+      const cplx v = cexpi(ap);
+      d[L.pj + 2 * j] = v.real();
+      d[L.pj + 2 * j + 1] = v.imag();
+    }
+    // every thread's row the same (the run reads only slots): the 2^M
+    // products become constants in pj (flag 1); otherwise flag 2 when E is
+    // exactly 1 for every thread (no thread-only or global phase)
+    bool same = true, e_one = true;
+    const size_t rl = (size_t)(1 + M) * 2;
+    for (int tid = 0; tid < (1 << TT); ++tid) {
+      const double* row = &d[L.thr + (size_t)tid * rl];
+      same = same && std::equal(row, row + rl, &d[L.thr]);
+      e_one = e_one && row[0] == 1.0 && row[1] == 0.0;
+    }
+    *flags = 0;
+    if (same) {
+      *flags = 1;
+      *pj_mask = 0;
+      *slot_mask = 0;
+      for (int j = 0; j < (1 << M); ++j) {
+        cplx f(d[L.thr], d[L.thr + 1]);
+        for (int sl = 0; sl < M; ++sl)
+          if (j >> sl & 1) f *= cplx(d[L.thr + 2 + 2 * sl], d[L.thr + 3 + 2 * sl]);
+        f *= cplx(d[L.pj + 2 * j], d[L.pj + 2 * j + 1]);
+        d[L.pj + 2 * j] = f.real();
+        d[L.pj + 2 * j + 1] = f.imag();
+        if (f != cplx(1.0, 0.0)) *pj_mask |= (uint16_t)(1u << j);
+      }
+    } else if (e_one) {
+      *flags = 2;
+    }
+    *out = hp.pool;
+    hp.qcopy.emplace_back(hp.pool, std::move(d));
+    hp.pool += L.total / 2;
+    return QK_OK;
+  };
+  // tile-only quadratic runs of a quad-enabled pass become OP_QLITE (a few
+  // per-thread loads instead of 16 table gathers per run; QK_QLITE_TABLE1:
+  // the first keeps its table, which the specialised kernel may hoist)
+  bool tile_table_used = false;
   PassDesc pd{};
   pd.C = C;
   pd.M = M;
@@ -1077,7 +1276,20 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
         if (rc) return rc;
         op.code = OP_QUAD;
         op.table = off;
+      } else if (it.type == 1 && allow_quad && run_quad[it.run] && (tile_table_used || !getenv("QK_QLITE_TABLE1")) &&
+                 !getenv("QK_NO_QLITE")) {
+        std::vector<int> Tth(T.begin(), T.end());
+        int64_t off = 0;
+        uint16_t sm = 0, pm = 0, fl = 0;
+        int rc = build_qlite(it.run, Tth, pb.R, &off, &sm, &pm, &fl);
+        if (rc) return rc;
+        op.code = OP_QLITE;
+        op.table = off;
+        op.pr[0] = sm;
+        op.pr[1] = pm;
+        op.pr[2] = fl;
       } else if (it.type == 1) {
+        if (allow_quad && run_quad[it.run]) tile_table_used = true;
         const uint32_t S = run_support[it.run];
         if (run_table[it.run] < 0) {
           std::vector<int> order(T.begin(), T.end());
@@ -1701,7 +1913,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
             t.co_k[k] = op.co_k[k];
             t.co_v[k] = op.co_v[k];
           }
-          if (op.nco || op.code == OP_QUAD) tp.needs_jit = 1;
+          if (op.nco || op.code == OP_QUAD || op.code == OP_QLITE) tp.needs_jit = 1;
           if (op.code == OP_SCALE) {
             if (ncoef + 2 > kTMaxCoef) return false;
             tp.coef[ncoef] = hp.coef[op.coef];
@@ -2082,7 +2294,7 @@ int upload_plan(qk_sim* s) {
     bool quad = false;
     for (int ph = 0; ph < pd.nphases; ++ph) {
       const PhaseDesc& D = hp.phases[pd.phase0 + ph];
-      for (int o = D.op_begin; o < D.op_end; ++o) quad = quad || hp.ops[o].code == OP_QUAD;
+      for (int o = D.op_begin; o < D.op_end; ++o) quad = quad || hp.ops[o].code == OP_QUAD || hp.ops[o].code == OP_QLITE;
     }
     if (quad && !(s->pass_tma[p] >= 0 && p < s->pass_jit.size() && s->pass_jit[p]))
       return fail(QK_ESIM, "quadratic diagonal pass needs the specialised kernel (NVRTC)");
@@ -2169,13 +2381,14 @@ int upload_plan_dry(qk_sim* s) {
   g_dry_maps = false;
   for (size_t p = 0; p < hp.passes.size(); ++p) {
     const PassDesc& pd = hp.passes[p];
-    int cnt[8] = {0};
+    int cnt[16] = {0};
     for (int ph = 0; ph < pd.nphases; ++ph) {
       const PhaseDesc& D = hp.phases[pd.phase0 + ph];
-      for (int o = D.op_begin; o < D.op_end; ++o) cnt[hp.ops[o].code & 7]++;
+      for (int o = D.op_begin; o < D.op_end; ++o) cnt[hp.ops[o].code & 15]++;
     }
-    fprintf(stderr, "dry pass %zu: C=%d phases=%d tma=%d H=%d MAT=%d CX=%d DIAG=%d QUAD=%d tile=", p, pd.C,
-            pd.nphases, s->pass_tma[p] >= 0, cnt[OP_H], cnt[OP_MAT], cnt[OP_CX], cnt[OP_DIAG], cnt[OP_QUAD]);
+    fprintf(stderr, "dry pass %zu: C=%d phases=%d tma=%d H=%d MAT=%d CX=%d DIAG=%d QUAD=%d QLITE=%d tile=", p, pd.C,
+            pd.nphases, s->pass_tma[p] >= 0, cnt[OP_H], cnt[OP_MAT], cnt[OP_CX], cnt[OP_DIAG], cnt[OP_QUAD],
+            cnt[OP_QLITE]);
     if (pass_tile[p])
       for (int t : *pass_tile[p]) fprintf(stderr, "%d,", t);
     fprintf(stderr, "\n");
@@ -3348,7 +3561,7 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
       if (ip.type == QK_INS_BLOCK) {
         for (int p = ip.pass0; p < ip.pass0 + ip.npass; ++p) {
           const PassDesc& pd = s->hp.passes[p];
-          int cnt[8] = {0};
+          int cnt[16] = {0};
           for (int ph = 0; ph < pd.nphases; ++ph) {
             const PhaseDesc& D = s->hp.phases[pd.phase0 + ph];
             for (int o = D.op_begin; o < D.op_end; ++o) cnt[s->hp.ops[o].code]++;
