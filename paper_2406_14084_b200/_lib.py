@@ -15,7 +15,8 @@ import numpy as np
 from .errors import CudaError, ParseError, SimulationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqkb200.so")
+# QK_LIB_PATH: dev A/B runs against another build of the same library
+LIB_PATH = os.environ.get("QK_LIB_PATH") or os.path.join(_HERE, "libqkb200.so")
 
 QK_OK, QK_EINVAL, QK_EPARSE, QK_ESIM, QK_ENOMEM, QK_ECUDA = 0, -1, -2, -3, -4, -5
 INS_BLOCK, INS_SQS, INS_CSQS = 0, 1, 2

@@ -371,7 +371,7 @@ int jit_slice_bytes(const TmaParams& tp) {
   int nq = 0;                     // OP_QUAD factors: C + 1 per op per stage
   for (int ph = 0; ph < tp.nphases; ++ph)
     for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) nq += tp.ops[o].code == OP_QUAD;
-  b += nq * (tp.C + 1 + 32 + (1 << std::max(0, tp.C - tp.M - 5))) * 16 * st;
+  b += nq * (tp.C + 1 + 32 + (1 << std::max(0, tp.C - tp.M - 5))) * 16 * (st + 1);  // + the pending slot
   return b;
 }
 
@@ -518,6 +518,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     lf = indep3(ll[rl[0]], ll[rl[1]], ll[rl[2]]) ? ll : choose_layout(C, tp.ph[tp.nphases - 1].tpos, rl);
   }
   int tab_i = 0;
+  const int exp_skip = getenv("QK_EXP_SKIP") ? atoi(getenv("QK_EXP_SKIP")) : 0;
   for (int ph = 0; ph < tp.nphases; ++ph) {
     const TPhase& D = tp.ph[ph];
     const bool last = ph + 1 == tp.nphases;
@@ -529,6 +530,14 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     if (last) b << "    (void)0;\n";
     for (int o = D.op_begin; o < D.op_end; ++o) {
       const TOp& op = tp.ops[o];
+      // dev attribution only (wrong results): QK_EXP_SKIP bit 1 drops
+      // OP_QUAD/OP_QLITE, bit 2 one-qubit steps, bit 4 tables and scales
+      if (exp_skip && (((exp_skip & 1) && (op.code == OP_QUAD || op.code == OP_QLITE)) ||
+                       ((exp_skip & 2) && op.code == STEP_1Q) ||
+                       ((exp_skip & 4) && (op.code == OP_DIAG || op.code == OP_SCALE)))) {
+        if (op.code == OP_DIAG) ++tab_i;
+        continue;
+      }
       // quadratic table group: consecutive eligible tables of this phase
       // (not hoisted / early / sliced) applied as one factor per amplitude
       if ((variant & 2) && quad && op.code == OP_DIAG && o < (int)quad->size() && (*quad)[o].ok &&
@@ -862,7 +871,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     } else {
       b << "    fence_async_smem();\n    gbar(bar_id, " << GT << ");\n";
       b << "    if (tid == 0) mbar_arrive(empty + s);\n";
-      if (tp.permuted) {
+      if (tp.permuted && !(exp_skip & 8)) {  // (bit 8: contiguous store, timing only)
         b << "    u64 dst = 0ull";
         for (int k = 0; k < tp.nbits - C; ++k) b << " | (((chunk >> " << k << ") & 1ull) << " << (int)tp.dpos[C + k] << ")";
         b << ";\n";
@@ -986,7 +995,14 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     for (int e : slice_plan(tp, st)) planned += (size_t)e * 16;
     fac_off = (size_t)st * (16u << C) + 16 * st + planned + (tp.norm ? 16 * 32 * 8 : 0);
   }
-  o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n"
+  // (dev: QK_JIT_MAXNREG caps registers instead of the launch bounds; note
+  // that 17 warps allocate like 20, so 544 threads fit only up to 96)
+  const int maxreg = getenv("QK_JIT_MAXNREG") ? atoi(getenv("QK_JIT_MAXNREG")) : 0;
+  if (maxreg > 0)
+    o << "extern \"C\" __global__ void __maxnreg__(" << maxreg << ") qk_jit(const __grid_constant__ QkJitParams p) {\n";
+  else
+    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 + consumers << ", 1) qk_jit(const __grid_constant__ QkJitParams p) {\n";
+  o
     << "  extern __shared__ __align__(1024) unsigned char smem_raw[];\n"
     << "  unsigned char* base = smem_raw;\n"
     << "  const u32 stage_bytes = " << (16u << C) << "u;\n"
@@ -1012,8 +1028,10 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "        if (round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n";
   } else {
     // OP_QUAD: the whole producer warp turns the chunk bits into the
-    // per-position factors of every quadratic op (stage slot s) before lane 0
-    // arms the stage, so the consumers' full-barrier wait also acquires them
+    // per-position factors of every quadratic op in a pending slot while the
+    // stage is still in use (sincos and L2 reads off the refill path), copies
+    // them into the stage's slot once it is free, and lane 0 arms the stage:
+    // the consumers' full-barrier wait acquires both the tile and the factors
     o << "  if (threadIdx.x < 32) {\n"
       << "    const u32 lane = threadIdx.x;\n"
       << "    if (lane == 0) asm volatile(\"prefetch.tensormap [%0];\" ::\"l\"(&p.map) : \"memory\");\n"
@@ -1021,8 +1039,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "      if (!" << chunk_ok("i") << ") break;\n"
       << "      const u64 chunk = " << chunk_of("i") << ";\n"
       << "      const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
-      << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
-      << "      __syncwarp();\n";
+      << "      double2* const pend = fac + " << st * NQ * FS << "u;\n";
+  }
+  std::ostringstream fsrc;  // producer-side factors of the OP_QUAD ops
+  if (NQ) {
+    std::ostringstream& o = fsrc;
     for (size_t qi = 0; qi < qops.size(); ++qi) {
       if (qfac[qi] < 0) continue;
       const int q = qfac[qi];
@@ -1053,7 +1074,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         << "        } else if (lane == " << C << "u) {\n"
         << "          a = __ldg(qd + " << QL.phi0 << ") + t;\n"
         << "        }\n"
-        << "        double2* fs = fac + ((u32)s * " << NQ << "u + " << q << "u) * " << FS << "u;\n"
+        << "        double2* fs = pend + " << q * FS << "u;\n"
         << "        if (lane <= " << C << "u) { double sn, cs; sincos(a, &sn, &cs); fs[lane] = make_double2(cs, sn); }\n"
         << "        __syncwarp();\n";
       // products over the thread bits of the phase that applies the op
@@ -1073,9 +1094,13 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       o << "          fs[" << C + 33 << " + lane] = y; }\n"
         << "      }\n";
     }
-    o << "      __syncwarp();\n"
-      << "      if (lane == 0) {\n";
   }
+  if (NQ)
+    o << fsrc.str() << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
+      << "      __syncwarp();\n"
+      << "      for (u32 e = lane; e < " << NQ * FS << "u; e += 32u) fac[(u32)s * " << NQ * FS << "u + e] = pend[e];\n"
+      << "      __syncwarp();\n"
+      << "      if (lane == 0) {\n";
   o << "        mbar_expect_tx(full + s, stage_bytes);\n"
     << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n";
   const char* pfe = getenv("QK_JIT_PREFETCH");
@@ -1111,8 +1136,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       o << "          tma_prefetch(&p.map, 0, prow + " << t * tp.box_rows << ");\n";
     o << "        }\n";
   }
-  o << "      }\n    }\n    return;\n  }\n"
-    << "  const int ct = threadIdx.x - 32;\n"
+  if (NQ)
+    o << "      }\n    }\n    return;\n  }\n";
+  else
+    o << "      }\n    }\n    return;\n  }\n";
+  o << "  const int ct = threadIdx.x - 32;\n"
     << "  const int g = ct >> " << T << ";\n"
     << "  const u32 tid = ct & " << (GT - 1) << "u;\n"
     << pro.str()

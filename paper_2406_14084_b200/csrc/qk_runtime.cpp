@@ -2012,7 +2012,8 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
     for (const QuadOp& q : *quad) key.append(reinterpret_cast<const char*>(&q), sizeof q);
   // environment switches the generator (and tma_smem_bytes) reads
   for (const char* e : {"QK_JIT_PREFETCH", "QK_JIT_HOIST", "QK_JIT_EARLY", "QK_JIT_SW128", "QK_NO_CORDER",
-                        "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS"}) {
+                        "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS",
+                        "QK_EXP_SKIP", "QK_JIT_MAXNREG"}) {
     const char* v = getenv(e);
     key.push_back('|');
     if (v) key.append(v);
