@@ -24,6 +24,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <tuple>
 #include <set>
 #include <mutex>
 #include <sstream>
@@ -372,7 +373,35 @@ int jit_slice_bytes(const TmaParams& tp) {
   for (int ph = 0; ph < tp.nphases; ++ph)
     for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) nq += tp.ops[o].code == OP_QUAD;
   b += nq * (tp.C + 1 + 32 + (1 << std::max(0, tp.C - tp.M - 5))) * 16 * (st + 1);  // + the pending slot
+  if (jit_pairs(tp)) b += 8 * st;                                                     // pair barriers
   return b;
+}
+
+// Chunk bits the pass's diagonal tables read (per-chunk table terms).
+static uint64_t table_chunk_mask(const TmaParams& tp) {
+  uint64_t tmask = 0;
+  for (int ph = 0; ph < tp.nphases; ++ph)
+    for (int o2 = tp.ph[ph].op_begin; o2 < tp.ph[ph].op_end; ++o2)
+      if (tp.ops[o2].code == OP_DIAG)
+        for (int k = 0; k < tp.ops[o2].nco; ++k) tmask |= 1ull << tp.ops[o2].co_k[k];
+  return tmask;
+}
+
+// Cluster pairs for strided tiles with 128-B rows. Such a tile reads and
+// writes 128-B pieces, and HBM serves isolated 128-B accesses at ~5 TB/s
+// against ~6.1 TB/s for 256-B ones (tools/strided_bench.cu). When the
+// lowest non-tile bit is address bit 3, chunks 2u and 2u + 1 hold the two
+// halves of every 256-B segment: a 2-CTA cluster takes both, and its two
+// producers meet at a per-stage mbarrier before every TMA load, so the halves
+// reach the memory controller together.
+bool jit_pairs(const TmaParams& tp) {
+  if (!getenv("QK_PAIR") || !tp.lazy || tp.xbits || tp.rowbits != 3 || tp.nchunks < 2 || (tp.nchunks & 1)) return false;
+  int ng = 0, st = 0;
+  if (tma_smem_bytes(tp.C, tp.M, &ng, &st, tp.smax) < 0 || st < 2) return false;
+  if (table_chunk_mask(tp) && tp.C >= 12 && !getenv("QK_NO_CORDER")) return false;  // chunk order walk
+  uint32_t tb = 0;
+  for (int x = 0; x < tp.C; ++x) tb |= 1u << tp.tbit[x];
+  return (tb & 0xFu) == 0x7u;  // bits 0..2 in the tile, bit 3 the lowest chunk bit
 }
 
 // Emit the source of one pass. Returns false when the structure is outside
@@ -952,15 +981,12 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // contiguous range of a counter whose high bits are the chunk bits the
   // tables read, so a CTA keeps the same table slices (and their L1 lines)
   // over long stretches instead of switching slices every chunk.
-  uint64_t tmask = 0;
-  for (int ph = 0; ph < tp.nphases; ++ph)
-    for (int o2 = tp.ph[ph].op_begin; o2 < tp.ph[ph].op_end; ++o2)
-      if (tp.ops[o2].code == OP_DIAG)
-        for (int k = 0; k < tp.ops[o2].nco; ++k) tmask |= 1ull << tp.ops[o2].co_k[k];
+  const uint64_t tmask = table_chunk_mask(tp);
   const int nouter = tp.nbits - C;
   // (12-bit chunks only: QAOA30 0.166 -> 0.162 s, QAOA33r3 1.73 -> 1.64 s;
   // QFT30's 10-bit passes lose 4%, their CTAs then spread over more pages)
   const bool corder = tmask && C >= 12 && !getenv("QK_NO_CORDER");
+  const bool pair = jit_pairs(tp);
   if (corder) {
     std::vector<int> ord;
     for (int k = 0; k < nouter; ++k)
@@ -976,6 +1002,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // grid-stride order over their part of the chunks)
   auto chunk_of = [&](const char* iv) {
     std::ostringstream c;
+    if (pair) {  // pair u = cluster + i * clusters; the cluster rank is chunk bit 0
+      c << "(p.split ? qk_insert(2ull * (CID + " << iv << " * NCL) + RK, p.split) : (2ull * (CID + " << iv
+        << " * NCL) + RK))";
+      return c.str();
+    }
     c << "(p.split ? qk_insert(blockIdx.x + " << iv << " * G, p.split) : ";
     if (corder) c << "cmap(blockIdx.x * PER + " << iv << "))";
     else c << "(blockIdx.x + " << iv << " * G))";
@@ -983,6 +1014,10 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   };
   auto chunk_ok = [&](const char* iv) {
     std::ostringstream c;
+    if (pair) {
+      c << "(2ull * (CID + " << iv << " * NCL) < p.nchunks)";
+      return c.str();
+    }
     if (corder)
       c << "(p.split ? (blockIdx.x + " << iv << " * G < p.nchunks) : (" << iv << " < PER && blockIdx.x * PER + " << iv
         << " < p.nchunks))";
@@ -995,6 +1030,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     for (int e : slice_plan(tp, st)) planned += (size_t)e * 16;
     fac_off = (size_t)st * (16u << C) + 16 * st + planned + (tp.norm ? 16 * 32 * 8 : 0);
   }
+  const size_t pair_off = fac_off + (size_t)NQ * FS * 16 * (st + 1);
   // (dev: QK_JIT_MAXNREG caps registers instead of the launch bounds; note
   // that 17 warps allocate like 20, so 544 threads fit only up to 96)
   const int maxreg = getenv("QK_JIT_MAXNREG") ? atoi(getenv("QK_JIT_MAXNREG")) : 0;
@@ -1007,16 +1043,19 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     << "  unsigned char* base = smem_raw;\n"
     << "  const u32 stage_bytes = " << (16u << C) << "u;\n"
     << "  u64* full = (u64*)(base + " << (size_t)st * (16u << C) << "ull);\n"
-    << "  u64* empty = full + " << st << ";\n"
-    << "  if (threadIdx.x == 0) {\n"
-    << "    for (int s = 0; s < " << st << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n"
-    << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n"
-    << "  __syncthreads();\n"
+    << "  u64* empty = full + " << st << ";\n";
+  if (pair) o << "  u64* pairb = (u64*)(base + " << pair_off << "ull);\n";
+  o << "  if (threadIdx.x == 0) {\n"
+    << "    for (int s = 0; s < " << st << "; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }\n";
+  if (pair) o << "    for (int s = 0; s < " << st << "; ++s) mbar_init(pairb + s, 1);\n";
+  o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  }\n"
+    << (pair ? "  cluster_sync();\n" : "  __syncthreads();\n")
     << "  const u64 G = gridDim.x;\n"
     << "  const u64 PER = (p.nchunks + G - 1) / G;\n"
     << "  (void)PER;\n"
     << "  double2* fac = (double2*)(base + " << fac_off << "ull);\n"
     << "  (void)fac;\n";
+  if (pair) o << "  const u64 CID = cl_id(), NCL = cl_num();\n  const u32 RK = cl_rank();\n";
   if (!NQ) {
     o << "  if (threadIdx.x < 32) {\n"
       << "    if (threadIdx.x == 0) {\n"
@@ -1101,6 +1140,9 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "      for (u32 e = lane; e < " << NQ * FS << "u; e += 32u) fac[(u32)s * " << NQ * FS << "u + e] = pend[e];\n"
       << "      __syncwarp();\n"
       << "      if (lane == 0) {\n";
+  if (pair)
+    o << "        mbar_arrive_remote(mapa(su32(pairb + s), RK ^ 1u));\n"
+      << "        mbar_wait(pairb + s, round & 1u);\n";
   o << "        mbar_expect_tx(full + s, stage_bytes);\n"
     << "        unsigned char* dst = base + (size_t)s * stage_bytes;\n";
   const char* pfe = getenv("QK_JIT_PREFETCH");
@@ -1341,7 +1383,7 @@ void jit_build(const std::vector<std::string>& srcs, std::vector<void*>* handles
 
 // Launch a JIT kernel: params blob = QkJitParams laid out by jit_params().
 int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, int num_sms, CUstream_st* stream,
-               int smax, int extra_smem) {
+               int smax, int extra_smem, int cluster) {
   int ng = 0, st = 0;
   const int smem0 = tma_smem_bytes(C, M, &ng, &st, smax);
   if (smem0 < 0) return -1;
@@ -1361,6 +1403,41 @@ int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, i
     }
   }
   void* args[] = {const_cast<void*>(params)};
+  if (cluster > 1) {
+    // as many co-resident clusters as the device holds (one CTA per SM)
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = reinterpret_cast<cudaStream_t>(stream);
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static std::mutex mu;
+    static std::map<std::tuple<void*, int, int>, int> fit;
+    int dev = 0, ncl = 0;
+    cudaGetDevice(&dev);
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = fit.find({kern, dev, smem});
+      if (it == fit.end()) {
+        cfg.gridDim = dim3((unsigned)(num_sms / cluster * cluster));
+        if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)kern, &cfg) != cudaSuccess || ncl < 1) {
+          cudaGetLastError();
+          ncl = num_sms / cluster / 2;
+        }
+        fit[{kern, dev, smem}] = ncl;
+      } else {
+        ncl = it->second;
+      }
+    }
+    const uint64_t want = (nchunks + cluster - 1) / cluster;
+    cfg.gridDim = dim3((unsigned)(cluster * (want < (uint64_t)ncl ? want : (uint64_t)ncl)));
+    return (int)cudaLaunchKernelExC(&cfg, (const void*)kern, args);
+  }
   cudaError_t e = cudaLaunchKernel((const void*)kern, dim3((unsigned)grid), dim3(threads), args, smem,
                                    reinterpret_cast<cudaStream_t>(stream));
   return (int)e;

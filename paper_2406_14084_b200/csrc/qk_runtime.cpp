@@ -1580,7 +1580,14 @@ struct qk_sim {
   int norm_pass = -1, nrm_parts = 0;
   bool norm_valid = false;
   bool fresh = false;
+  // Zero support: during a run from a reset state every amplitude at a
+  // physical address >= 2^zbits is exactly zero (64: unknown). A TMA pass then
+  // loads through a view bounded at 2^zbits, so the TMA unit zero-fills the
+  // rest without HBM reads, and the bound grows to the pass's highest tile bit
+  // (its gates and in-tile permutation touch no other bit).
+  int zbits = 64;
   double fresh_saved = 0;  // read bytes skipped this way (kept out of the stats)
+  std::vector<double> saved_i;  // per instruction of the last run: read bytes skipped
   double* state = nullptr;      // == bufs[cur]
   double* bufs[2] = {nullptr, nullptr};  // bufs[1]: out-of-place target of fused passes
   int cur = 0;
@@ -1724,10 +1731,11 @@ const CUtensorMap* state_map(qk_sim* s, int buf, int box_rows) {
   return &s->maps[buf][slot];
 }
 
-// A pass's load view of bufs[0] with only addresses < 2^kFreshBits in bounds
-// (every other box is zero-filled by the TMA unit without touching HBM): on a
-// fresh |0...0> those are the only amplitudes qk_reset wrote.
-bool fresh_map(qk_sim* s, const TmaParams& tp, CUtensorMap* out) {
+// A pass's load view of `buf` with only addresses < 2^zb in bounds (every
+// other box is zero-filled by the TMA unit without touching HBM): on a fresh
+// |0...0> (zb = kFreshBits) those are the only amplitudes qk_reset wrote, and
+// later in a run from reset they are the only ones that can be nonzero.
+bool fresh_map(qk_sim* s, const TmaParams& tp, int zb, double* buf, CUtensorMap* out) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[5], strides[4];
@@ -1738,7 +1746,7 @@ bool fresh_map(qk_sim* s, const TmaParams& tp, CUtensorMap* out) {
     if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return false;
     rank = td.rank;
     for (int j = 0; j < rank; ++j) {
-      const int keep = std::max(0, std::min(td.len[j], kFreshBits - td.lo[j]));
+      const int keep = std::max(0, std::min(td.len[j], zb - td.lo[j]));
       dims[j] = j == 0 ? (cuuint64_t)(2 << td.len[0]) : (cuuint64_t)1 << keep;
       if (j) strides[j - 1] = (cuuint64_t)16 << td.lo[j];
       box[j] = (cuuint32_t)td.box[j];
@@ -1746,12 +1754,12 @@ bool fresh_map(qk_sim* s, const TmaParams& tp, CUtensorMap* out) {
   } else {
     rank = 2;
     dims[0] = 16;
-    dims[1] = (cuuint64_t)1 << (kFreshBits - 3);
+    dims[1] = (cuuint64_t)1 << (zb - 3);
     strides[0] = 128;
     box[0] = 16;
     box[1] = (cuuint32_t)tp.box_rows;
   }
-  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, s->bufs[0], dims, strides, box, es,
+  return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, buf, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE,
             (tp.lazy && tp.rowbits == 2) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -1760,6 +1768,7 @@ bool fresh_map(qk_sim* s, const TmaParams& tp, CUtensorMap* out) {
 // Write the whole |0...0> state of a fresh handle (before anything but the
 // first TMA pass reads or writes it).
 int ensure_full(qk_sim* s) {
+  s->zbits = 64;  // the caller reads or writes the state outside a pass
   if (!s->fresh) return QK_OK;
   s->fresh = false;
   int rc = launch_fill_zero_one(s->bufs[0], s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
@@ -3616,8 +3625,10 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
   // a fresh state is read only by a TMA pass (it writes every chunk) through a
   // view whose in-bounds part is the written prefix
   CUtensorMap fmap;
-  const bool from_fresh = !split && s->fresh && tma_pass && s->cur == 0 && !getenv("QK_NO_FRESH") &&
-                          fresh_map(s, s->tma[s->pass_tma[p]], &fmap);
+  const int zb = s->zbits;
+  const bool from_fresh = !split && zb < s->nbits && (s->fresh ? s->cur == 0 : true) && tma_pass &&
+                          !getenv("QK_NO_FRESH") &&
+                          fresh_map(s, s->tma[s->pass_tma[p]], zb, s->bufs[s->cur], &fmap);
   if (split && !(tma_pass && p < (int)s->pass_jit.size() && s->pass_jit[p]))
     return fail(QK_ESIM, "internal: split launch of a pass without a specialised kernel");
   if (!from_fresh) {
@@ -3631,7 +3642,7 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
     if (from_fresh) {
       if (!tp.lazy) tp.map = fmap;
       s->fresh = false;
-      s->fresh_saved += 16.0 * (double)(s->amps - (1ull << tp.C));
+      s->fresh_saved += 16.0 * (double)(s->amps - (1ull << zb));
     } else if (!tp.lazy) {
       const CUtensorMap* map = state_map(s, s->cur, tp.box_rows);
       if (!map) return fail(QK_ECUDA, "tensor map unavailable");
@@ -3657,7 +3668,7 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
                     : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, nch, s->num_sms, (CUstream_st*)s->stream,
-                                 tp.smax, jit_slice_bytes(tp));
+                                 tp.smax, jit_slice_bytes(tp), jit_pairs(tp) ? 2 : 1);
       if (split) {
         blob[19] = tp.nchunks;
         blob[21] = 0;
@@ -3675,8 +3686,19 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       s->cur ^= 1;
       s->state = s->bufs[s->cur];
     }
+    // zero support: the pass's gates and in-tile permutation touch only its
+    // tile bits (a permuted store of the relabeled mode may move any bit)
+    if (split || flip || tp.xbits || s->zbits >= s->nbits || getenv("QK_NO_ZBOUND")) {
+      s->zbits = 64;
+    } else {
+      int hi = tp.lazy ? 0 : tp.C - 1;
+      if (tp.lazy)
+        for (int x = 0; x < tp.C; ++x) hi = std::max(hi, (int)tp.tbit[x]);
+      s->zbits = std::max(s->zbits, hi + 1);
+    }
     return QK_OK;
   }
+  s->zbits = 64;
   PassDesc h = s->hp.passes[p];
   if (count_override) h.ncta = count_override;
   int rc = launch_block_pass(s->state, &h, s->d_pass + p, s->d_phase, s->d_ops, s->d_coef, s->d_pool, first,
@@ -3947,7 +3969,7 @@ int run_instr(qk_sim* s, const InstrPlan& ip, bool* skipped = nullptr, size_t id
     return QK_OK;
   }
   if (ip.type != QK_INS_BLOCK) {
-    int rc = ensure_full(s);
+    int rc = ensure_full(s);  // (drops the zero support: the swap moves data)
     if (rc) return rc;
   }
   if (ip.type == QK_INS_BLOCK) {
@@ -4286,6 +4308,7 @@ int run_prepare(qk_sim* s, size_t* first_exec) {
   s->fresh_saved = 0;
   *first_exec = s->iplan.size();  // the instruction whose pass read the fresh state
   s->skipped.assign(s->iplan.size(), 0);
+  s->saved_i.assign(s->iplan.size(), 0.0);
   s->ovl_live = -1;
   // variant autotuning: passes whose structure is not tuned yet run their next
   // untimed variant (bit-identical results) between two events
@@ -4305,11 +4328,13 @@ int run_step(qk_sim* s, size_t i, size_t* first_exec) {
   CUDA_TRY(cudaSetDevice(s->device));
   CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
   const bool was_fresh = s->fresh;
+  const double saved0 = s->fresh_saved;
   bool skipped = false;
   const bool overlapped = s->iplan[i].type == QK_INS_CSQS && s->ovl_live == (int)i;
   int rc = run_instr(s, s->iplan[i], &skipped, i);
   if (rc) return rc;
   s->skipped[i] = skipped;
+  s->saved_i[i] = s->fresh_saved - saved0;
   if (was_fresh && !s->fresh && s->fresh_saved > 0) *first_exec = i;
   // (an overlapped exchange brackets itself on the comm stream)
   if (!overlapped) CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
@@ -4325,6 +4350,7 @@ int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
   int rc = check_peer_error(s);
   if (rc) return rc;
   if (s->lay_final.size() == s->lay.size()) s->lay = s->lay_final;
+  s->zbits = 64;  // a later run or writer starts from an unknown state
   s->norm_valid = s->norm_pass >= 0;
   for (size_t p = 0; p < s->tuning.size(); ++p)
     if (s->tuning[p] >= 0) {
@@ -4348,7 +4374,7 @@ int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
     const int sc = xp ? 3 : c;
     s->stat_ms[sc] += ms;
     if (fused_away(s, ip) || s->skipped[i]) continue;
-    s->stat_bytes[sc] += ip.bytes - (i == first_exec ? s->fresh_saved : 0.0);
+    s->stat_bytes[sc] += ip.bytes - s->saved_i[i];
     s->stat_launch[sc] += c == QK_INS_BLOCK ? ip.npass : (ip.sqs != -1 ? 1 : 0);
   }
   return QK_OK;
@@ -4605,6 +4631,7 @@ int qk_reset(qk_sim* s) {
   for (int q = 0; q < s->nbits; ++q) s->lay[q] = q;  // |0...0> is the same in every layout
   // only the first chunk is written; the rest is filled on demand (ensure_full)
   s->fresh = s->amps >= (2ull << kFreshBits) && !getenv("QK_NO_FRESH");
+  s->zbits = s->fresh ? kFreshBits : 64;
   int rc = launch_fill_zero_one(s->state, s->fresh ? (1ull << kFreshBits) : s->amps, s->rank_lo == 0,
                                 (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
