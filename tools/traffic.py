@@ -1,53 +1,41 @@
 """Per-launch DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) of the
-block, cluster-exchange and SQS passes from the qaoa26 `ncu --set full`
-captures of tools/evidence.sh, scaled to one qaoa30 launch -> profiles/traffic.json.
+gate-block passes of one tuned QAOA30 run, from the `ncu --set full` capture of
+tools/r02v.sh (raw page, gzipped csv) -> profiles/traffic.json. Measured on the
+headline configuration itself, no scaling.
 
-    python tools/traffic.py gpurun_out/<tag> profiles/<tag>_ncu_full_qaoa26.txt
+    python tools/traffic.py gpurun_out/r02v/full_qaoa30/raw.csv.gz r02v
 """
 import csv
+import gzip
 import io
 import json
 import os
-import subprocess
 import sys
 
 UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def launches(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
+def main(path, tag):
+    rows = list(csv.reader(io.StringIO(gzip.open(path, "rt").read())))
     hdr, units = rows[0], rows[1]
-    out = []
+    per = []
     for r in rows[2:]:
         d = dict(zip(hdr, r))
 
         def val(k):
             return float(d[k].replace(",", "")) * UNITS.get(units[hdr.index(k)], 1)
 
-        out.append((d["Kernel Name"], val("dram__bytes_read.sum") + val("dram__bytes_write.sum")))
-    return out
-
-
-def main(run_dir, summary):
-    blk = launches(os.path.join(run_dir, "full_qaoa26.ncu-rep"))
-    sqs = launches(os.path.join(run_dir, "full_sqs_qaoa26.ncu-rep"))
-    jit = [b for k, b in blk if k.startswith("qk_jit") and not k.startswith("qk_jitx")]
-    jx = [b for k, b in blk if k.startswith("qk_jitx")]
-    sq = [b for _, b in sqs]
-    alg = 32 * 2 ** 26
-    t = {"_how": f"dram__bytes_read.sum + dram__bytes_write.sum per launch from {summary} (qaoa26: "
-                 "2^26 amplitudes, 1 GiB state >> L2), divided by the launch's algorithmic bytes "
-                 "(32 B x 2^26) and scaled to one qaoa30 launch (32 B x 2^30 = 34.36 GB). Dirty L2 "
-                 "lines still resident at kernel end drain after it, hence write < read. Every "
-                 "captured launch read a full state (none was the first pass after qk_reset).",
-         "qaoa26": {"k_block_tma": sum(jit) / len(jit), "k_sqs": sum(sq) / len(sq),
-                    "k_block_x": sum(jx) / max(1, len(jx)), "algorithmic_bytes": alg,
-                    "launches": {"qk_jit": len(jit), "qk_jitx": len(jx), "k_sqs": len(sq)}}}
-    t["qaoa30"] = {k: t["qaoa26"][k] * 16 for k in ("k_block_tma", "k_sqs", "k_block_x", "algorithmic_bytes")}
-    with open("profiles/traffic.json", "w") as fh:
-        json.dump(t, fh, indent=1)
-    print(json.dumps(t["qaoa30"]))
+        per.append({"kernel": d["Kernel Name"], "ms": float(d["gpu__time_duration.sum"].replace(",", "")),
+                    "dram_read": val("dram__bytes_read.sum"), "dram_write": val("dram__bytes_write.sum")})
+    avg = sum(p["dram_read"] + p["dram_write"] for p in per) / len(per)
+    out = {"_how": f"ncu --set full of the {len(per)} gate-block passes of one tuned qaoa30 run "
+                   f"(tools/r02v.sh, capture {tag}); k_block_tma = mean dram__bytes_read.sum + "
+                   "dram__bytes_write.sum per launch. The first passes after qk_reset read only "
+                   "the zero-support prefix (bounded TMA view), so their traffic is mostly writes.",
+           "qaoa30": {"k_block_tma": avg, "launches": per}}
+    json.dump(out, open(os.path.join(ROOT, "profiles", "traffic.json"), "w"), indent=1)
+    print(f"{len(per)} launches, mean {avg / 1e9:.2f} GB per launch")
 
 
 if __name__ == "__main__":
