@@ -1078,7 +1078,8 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "      if (!" << chunk_ok("i") << ") break;\n"
       << "      const u64 chunk = " << chunk_of("i") << ";\n"
       << "      const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
-      << "      double2* const pend = fac + " << st * NQ * FS << "u;\n";
+      << (variant & 4 ? "      double2* const pend = fac + (u32)s * " + std::to_string(NQ * FS) + "u;\n"
+                      : "      double2* const pend = fac + " + std::to_string(st * NQ * FS) + "u;\n");
   }
   std::ostringstream fsrc;  // producer-side factors of the OP_QUAD ops
   if (NQ) {
@@ -1134,7 +1135,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         << "      }\n";
     }
   }
-  if (NQ)
+  if (NQ && (variant & 4))  // variant bit 4: factors straight into the stage's slot after the wait
+    o << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
+      << "      __syncwarp();\n" << fsrc.str() << "      __syncwarp();\n"
+      << "      if (lane == 0) {\n";
+  else if (NQ)
     o << fsrc.str() << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
       << "      __syncwarp();\n"
       << "      for (u32 e = lane; e < " << NQ * FS << "u; e += 32u) fac[(u32)s * " << NQ * FS << "u + e] = pend[e];\n"

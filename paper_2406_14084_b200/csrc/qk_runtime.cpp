@@ -2230,8 +2230,9 @@ int upload_plan(qk_sim* s) {
     std::vector<int> src_pass, src_var;
     std::vector<std::vector<long long>> toffs;
     std::vector<std::vector<double>> coefs;
-    // Up to four variants per pass (bit 1: no hoisted table, bit 2: quadratic
-    // table groups); identical sources are built once. QK_JIT_VARIANT=v pins
+    // Up to eight variants per pass (bit 1: no hoisted table, bit 2: quadratic
+    // table groups, bit 4: OP_QUAD factors computed after the stage wait
+    // instead of ahead in a pending slot); identical sources are built once. QK_JIT_VARIANT=v pins
     // one, otherwise the first runs time every variant and keep the fastest
     // per pass structure (process-wide, tune_pick / tune_record).
     const char* venv = getenv("QK_JIT_VARIANT");
@@ -2242,7 +2243,7 @@ int upload_plan(qk_sim* s) {
       if (s->pass_tma[p] < 0) continue;
       std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
       std::vector<std::string> seen;
-      for (int variant = 0; variant < 4; ++variant) {
+      for (int variant = 0; variant < 8; ++variant) {
         if (venv && variant != atoi(venv)) continue;
         std::string src;
         std::vector<long long> toff;
@@ -2404,7 +2405,7 @@ int upload_plan_dry(qk_sim* s) {
     fprintf(stderr, "\n");
     if (s->pass_tma[p] < 0 || s->dry_dir.empty()) continue;
     std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
-    for (int variant = 0; variant < 4; ++variant) {
+    for (int variant = 0; variant < 8; ++variant) {
       std::string src;
       std::vector<long long> toff;
       std::vector<double> coef;
