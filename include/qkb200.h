@@ -146,6 +146,13 @@ int qk_load_gate_by_gate(qk_sim* sim, const int32_t* words, size_t nwords,
 int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params, size_t nparams,
                       int n, int cap, int32_t* out_words, size_t* out_nwords, double* out_params,
                       size_t* out_nparams, int32_t* p2w, int* npass);
+/* The same schedule for one shard of a multi-GPU job (simulator.py:179-235):
+ * positions >= nlocal are rank bits held by other shards. A CSQS pairing
+ * local bits with them is a barrier of the schedule; it comes out as a
+ * QK_INS_CSQS record whose a / b are the outgoing / incoming wires. */
+int qk_reblock_shard(const int32_t* words, size_t nwords, const double* params, size_t nparams,
+                     int n, int nlocal, int cap, int32_t* out_words, size_t* out_nwords,
+                     double* out_params, size_t* out_nparams, int32_t* p2w, int* npass);
 
 /* Host-only planning (development and CPU tests; replaces no reference
  * interface): parse `text` for an n-qubit single-rank state and run the

@@ -50,6 +50,8 @@ _SIGS = {
     "qk_plan_dry": (c_int, [ctypes.c_char_p, c_size, c_int, c_int, c_int, ctypes.c_char_p, P(c_int)]),
     "qk_reblock_packed": (c_int, [P(c_int32), c_size, P(c_dbl), c_size, c_int, c_int, P(c_int32),
                                   P(c_size), P(c_dbl), P(c_size), P(c_int32), P(c_int)]),
+    "qk_reblock_shard": (c_int, [P(c_int32), c_size, P(c_dbl), c_size, c_int, c_int, c_int, P(c_int32),
+                                 P(c_size), P(c_dbl), P(c_size), P(c_int32), P(c_int)]),
     "qk_load_gate_by_gate": (c_int, [c_void, P(c_int32), c_size, P(c_dbl), c_size]),
     "qk_program_info": (c_int, [c_void, P(c_int), P(c_int), P(c_int), P(c_int), P(c_int32)]),
     "qk_run": (c_int, [c_void, P(c_dbl)]),
@@ -212,24 +214,29 @@ def plan_dry(text: str, n: int, c: int, second_buffer: bool = True, dump_dir: st
     return npass.value
 
 
-def reblock_packed(words, params, n: int, cap: int):
-    """Cross-block pass schedule (qk_reblock_packed) -> (words, params, p2w, npass);
-    npass 0 when the program cannot be rescheduled."""
+def reblock_packed(words, params, n: int, cap: int, nlocal: int | None = None):
+    """Cross-block pass schedule (qk_reblock_packed, or qk_reblock_shard for a
+    shard of `nlocal` local bits) -> (words, params, p2w, npass); npass 0 when
+    the program cannot be rescheduled."""
     L = lib()
     w = np.ascontiguousarray(words, dtype=np.int32)
     p = np.ascontiguousarray(params, dtype=np.float64)
     if p.size == 0:
         p = np.zeros(1)
+
+    def call(ow, nw, op, npar, p2w, npass):
+        if nlocal is None:
+            return L.qk_reblock_packed(iptr(w), w.size, dptr(p), p.size, n, cap, ow, nw, op, npar, p2w, npass)
+        return L.qk_reblock_shard(iptr(w), w.size, dptr(p), p.size, n, nlocal, cap, ow, nw, op, npar, p2w, npass)
+
     nw, npar, npass = c_size(0), c_size(0), c_int(0)
-    check(L.qk_reblock_packed(iptr(w), w.size, dptr(p), p.size, n, cap, None, ctypes.byref(nw), None,
-                              ctypes.byref(npar), None, ctypes.byref(npass)))
+    check(call(None, ctypes.byref(nw), None, ctypes.byref(npar), None, ctypes.byref(npass)))
     if npass.value == 0:
         return None, None, None, 0
     ow = np.zeros(max(1, nw.value), dtype=np.int32)
     op = np.zeros(max(1, npar.value), dtype=np.float64)
     p2w = np.zeros(n, dtype=np.int32)
-    check(L.qk_reblock_packed(iptr(w), w.size, dptr(p), p.size, n, cap, iptr(ow), ctypes.byref(nw),
-                              dptr(op), ctypes.byref(npar), iptr(p2w), ctypes.byref(npass)))
+    check(call(iptr(ow), ctypes.byref(nw), dptr(op), ctypes.byref(npar), iptr(p2w), ctypes.byref(npass)))
     return ow[:nw.value], op[:npar.value], p2w, npass.value
 
 

@@ -77,6 +77,8 @@ struct InstrH {
   // row bits 0.. and the next pass's wires on the lowest tile bits after them
   int rb = 0;
   std::vector<int> tile_w, rows_next;
+  // reblocked cross-shard CSQS: the wire at every position just before it
+  std::vector<int> xw;
 };
 
 // ---------------------------------------------------------------------------
@@ -2515,11 +2517,25 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
 // wires of the next pass (a lookahead choice) on those row bits. QAOA30 c12
 // (51 blocks, 24 passes after folding) runs in 13 passes, QFT33 c10 in 4.
 // Results equal the block order's up to rounding: only commuting gates move.
+//
+// Shards (ntot > nb): positions >= nb are rank bits held by other shards. A
+// CSQS that pairs local bits with such rank bits moves wires in and out of
+// the shard, so it is a barrier: the gates before it are cut into passes
+// (segment by segment), the CSQS is emitted with the wire of every position
+// just before it (`xw`), and the next segment's passes see the wires it
+// brought in. A CSQS whose rank bits are all held here is a relabel.
 bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std::vector<InstrH>* out,
-             std::vector<int>* p2w_final) {
-  if (nb > 64 || cap > nb) return false;
-  std::vector<int> p2w(nb);
-  for (int q = 0; q < nb; ++q) p2w[q] = q;
+             std::vector<int>* p2w_final, int ntot = -1) {
+  if (ntot < nb) ntot = nb;
+  if (ntot > 64 || cap > nb) return false;
+  std::vector<int> p2w(ntot);
+  for (int q = 0; q < ntot; ++q) p2w[q] = q;
+  struct Bar {
+    size_t gate0;            // first gate after the barrier
+    const InstrH* ins;
+    std::vector<int> xw;     // position -> wire just before it
+  };
+  std::vector<Bar> bars;
   struct WG {
     const GateH* g;
     uint64_t wm;
@@ -2543,34 +2559,45 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     } else {
       std::vector<int> sa = ins.a, sb = ins.b;
       if (sa.size() != sb.size()) return false;
+      bool outside = false;
       for (int q : sa)
         if (q < 0 || q >= nb) return false;
-      for (int q : sb)
-        if (q < 0 || q >= nb) return false;
+      for (int q : sb) {
+        if (q < 0 || q >= ntot) return false;
+        outside = outside || q >= nb;
+      }
+      if (outside && ins.type != QK_INS_CSQS) return false;
+      if (outside) bars.push_back({G.size(), &ins, p2w});
       std::sort(sa.begin(), sa.end());
       std::sort(sb.begin(), sb.end());
       for (size_t k = 0; k < sa.size(); ++k) std::swap(p2w[sa[k]], p2w[sb[k]]);
     }
   }
   *p2w_final = p2w;
+  const int NS = (int)bars.size() + 1;  // segments
+  auto seg_of_gate = [&](size_t i) {
+    int sg = 0;
+    while (sg < (int)bars.size() && bars[sg].gate0 <= i) ++sg;
+    return sg;
+  };
   // non-diagonal gates and their non-diagonal predecessors (through diagonal gates)
   std::vector<int> nd;                       // gate index of every non-diagonal gate
   std::vector<std::vector<uint64_t>> pre;    // predecessor bitsets over nd
   std::vector<std::vector<int>> ddep(G.size());  // diagonal gate -> nd predecessors
   {
-    std::vector<int> last(nb, -1);
-    std::vector<std::vector<int>> dd(nb);
+    std::vector<int> last(ntot, -1);
+    std::vector<std::vector<int>> dd(ntot);
     for (size_t i = 0; i < G.size(); ++i) {
       if (G[i].diag) {
         std::vector<int> deps;
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if ((G[i].wm >> w & 1) && last[w] >= 0) deps.push_back(last[w]);
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if (G[i].wm >> w & 1) dd[w].insert(dd[w].end(), deps.begin(), deps.end());
         ddep[i] = deps;
       } else {
         std::vector<int> p;
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if (G[i].wm >> w & 1) {
             if (last[w] >= 0) p.push_back(last[w]);
             p.insert(p.end(), dd[w].begin(), dd[w].end());
@@ -2582,7 +2609,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
           if ((int)pre[k].size() <= x / 64) pre[k].resize(x / 64 + 1, 0);
           pre[k][x / 64] |= 1ull << (x % 64);
         }
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if (G[i].wm >> w & 1) {
             last[w] = k;
             dd[w].clear();
@@ -2591,6 +2618,9 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     }
   }
   const int N = (int)nd.size();
+  std::vector<int> nseg(N);
+  for (int k = 0; k < N; ++k) nseg[k] = seg_of_gate((size_t)nd[k]);
+  int cur_seg = 0;
   const size_t NW = (size_t)N / 64 + 1;
   std::vector<uint64_t> done(NW, 0);
   auto isdone = [&](const std::vector<uint64_t>& d, int k) { return (d[k / 64] >> (k % 64)) & 1; };
@@ -2599,7 +2629,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     now = done;
     int c = 0;
     for (int k = 0; k < N; ++k) {
-      if (isdone(now, k) || (G[nd[k]].wm & ~S)) continue;
+      if (nseg[k] != cur_seg || isdone(now, k) || (G[nd[k]].wm & ~S)) continue;
       bool ok = true;
       for (size_t w = 0; w < pre[k].size() && ok; ++w) ok = !(pre[k][w] & ~now[w]);
       if (!ok) continue;
@@ -2608,17 +2638,20 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     }
     *cnt = c;
   };
+  std::vector<int> wire_at(nb);  // physical bit -> wire (the layout the passes see)
+  for (int q = 0; q < nb; ++q) wire_at[q] = q;
   auto choose = [&](uint64_t forced) {
     uint64_t S = forced;
-    std::vector<int> pend(nb, INT32_MAX);
+    std::vector<int> pend(ntot, INT32_MAX);
     for (int k = N - 1; k >= 0; --k)
-      if (!isdone(done, k))
-        for (int w = 0; w < nb; ++w)
+      if (nseg[k] == cur_seg && !isdone(done, k))
+        for (int w = 0; w < ntot; ++w)
           if (G[nd[k]].wm >> w & 1) pend[w] = k;
     std::vector<uint64_t> tmp;
     while (popc(S) < cap) {
       int best = -1, bc = -1;
-      for (int w = 0; w < nb; ++w) {
+      for (int x = 0; x < nb; ++x) {
+        const int w = wire_at[x];
         if ((S >> w & 1) || pend[w] == INT32_MAX) continue;
         int c = 0;
         closure(S | (1ull << w), tmp, &c);
@@ -2632,14 +2665,23 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     }
     return S;
   };
-  std::vector<int> wire_at(nb);  // physical bit -> wire (the layout the passes see)
-  for (int q = 0; q < nb; ++q) wire_at[q] = q;
   std::vector<int> npass(N, -1);
   std::vector<uint64_t> tiles;
   std::vector<std::vector<int>> rows_after;
   uint64_t forced = 0;
   for (int r = 0; r < rowbits; ++r) forced |= 1ull << wire_at[r];
-  int left = N;
+  std::vector<int> seg_first(NS, 0), seg_last(NS, -1);
+  std::vector<char> seg_diag(NS, 0);
+  for (size_t i = 0; i < G.size(); ++i)
+    if (G[i].diag) seg_diag[seg_of_gate(i)] = 1;
+  for (cur_seg = 0; cur_seg < NS; ++cur_seg) {
+  seg_first[cur_seg] = (int)tiles.size();
+  int left = 0;
+  for (int k = 0; k < N; ++k) left += nseg[k] == cur_seg;
+  if (!left && seg_diag[cur_seg] && (NS > 1 || N == 0)) {  // diagonal gates only: one pass over the row bits
+    tiles.push_back(forced);
+    rows_after.push_back(std::vector<int>(wire_at.begin(), wire_at.begin() + rowbits));
+  }
   while (left > 0) {
     const uint64_t S = choose(forced);
     std::vector<uint64_t> now;
@@ -2671,7 +2713,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     }
     rows_after.push_back(rows);
     // the layout after the pass: only the row assignment matters here
-    std::vector<int> pos(nb);
+    std::vector<int> pos(ntot, -1);
     for (int q = 0; q < nb; ++q) pos[wire_at[q]] = q;
     for (int r = 0; r < rowbits; ++r) {
       const int w = rows[r], from = pos[w], displaced = wire_at[r];
@@ -2683,17 +2725,48 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     forced = 0;
     for (int r = 0; r < rowbits; ++r) forced |= 1ull << wire_at[r];
   }
+  seg_last[cur_seg] = (int)tiles.size() - 1;
+  if (cur_seg < (int)bars.size()) {
+    // the barrier's wire moves: a held pair swaps the two bits' wires, an
+    // outside pair brings the rank position's wire onto the local bit
+    const Bar& br = bars[cur_seg];
+    std::vector<int> sa = br.ins->a, sb = br.ins->b;
+    std::sort(sa.begin(), sa.end());
+    std::sort(sb.begin(), sb.end());
+    std::vector<int> pos(ntot, -1);
+    for (int x = 0; x < nb; ++x) pos[wire_at[x]] = x;
+    for (size_t k = 0; k < sa.size(); ++k) {
+      const int wa = br.xw[sa[k]], wb = br.xw[sb[k]];
+      const int xa = pos[wa];
+      if (xa < 0) return false;
+      if (sb[k] < nb) {
+        const int xb = pos[wb];
+        if (xb < 0) return false;
+        wire_at[xa] = wb;
+        wire_at[xb] = wa;
+      } else {
+        wire_at[xa] = wb;
+      }
+    }
+    forced = 0;
+    for (int r = 0; r < rowbits; ++r) forced |= 1ull << wire_at[r];
+  }
+  }
   if (tiles.empty()) {  // only diagonal gates: one pass over the row bits
     tiles.push_back(forced);
     rows_after.push_back(std::vector<int>(wire_at.begin(), wire_at.begin() + rowbits));
+    seg_last[0] = 0;
   }
   // pass of every gate: non-diagonal from the schedule, diagonal = the latest
   // pass among its predecessors (0 if none)
   std::vector<int> gpass(G.size(), 0);
   for (int k = 0; k < N; ++k) gpass[nd[k]] = npass[k];
   for (size_t i = 0; i < G.size(); ++i)
-    if (G[i].diag)
+    if (G[i].diag) {
       for (int k : ddep[i]) gpass[i] = std::max(gpass[i], npass[k]);
+      gpass[i] = std::max(gpass[i], seg_first[seg_of_gate(i)]);
+      if (seg_last[seg_of_gate(i)] < gpass[i]) return false;
+    }
   // Latest pass a diagonal gate may run in: that of its first non-diagonal
   // successor on any of its wires (the last pass if none). A pass's tail —
   // the diagonal gates no later non-diagonal gate of the pass touches —
@@ -2704,13 +2777,14 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   {
     const int P = (int)tiles.size();
     std::vector<int> latest(G.size(), P - 1);
-    std::vector<int> next_nd(nb, -1);  // scanning backwards: next non-diagonal gate per wire
+    for (size_t i = 0; i < G.size(); ++i) latest[i] = std::min(latest[i], seg_last[seg_of_gate(i)]);
+    std::vector<int> next_nd(ntot, -1);  // scanning backwards: next non-diagonal gate per wire
     for (int i = (int)G.size() - 1; i >= 0; --i) {
       if (G[i].diag) {
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if ((G[i].wm >> w & 1) && next_nd[w] >= 0) latest[i] = std::min(latest[i], gpass[next_nd[w]]);
       } else {
-        for (int w = 0; w < nb; ++w)
+        for (int w = 0; w < ntot; ++w)
           if (G[i].wm >> w & 1) next_nd[w] = i;
       }
     }
@@ -2733,12 +2807,12 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
           for (int i : tail) gpass[i] = p + 1;
       }
   }
-  out->assign(tiles.size(), InstrH());
+  std::vector<InstrH> passes(tiles.size());
   for (size_t p = 0; p < tiles.size(); ++p) {
-    InstrH& b = (*out)[p];
+    InstrH& b = passes[p];
     b.type = QK_INS_BLOCK;
     b.rb = 1;
-    for (int w = 0; w < nb; ++w)
+    for (int w = 0; w < ntot; ++w)
       if (tiles[p] >> w & 1) b.tile_w.push_back(w);
     b.rows_next = rows_after[p];
   }
@@ -2770,9 +2844,27 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     for (int i : order) {
       GateH g = *G[i].g;
       g.t = G[i].w;
-      (*out)[p].gates.push_back(std::move(g));
+      passes[p].gates.push_back(std::move(g));
     }
   }
+  // passes in order, each barrier after the last pass of its segment
+  out->clear();
+  size_t bi = 0;
+  auto flush_bars = [&](int upto) {
+    while (bi < bars.size() && seg_last[bi] <= upto) {
+      InstrH c = *bars[bi].ins;
+      c.rb = 1;
+      c.xw = bars[bi].xw;
+      out->push_back(std::move(c));
+      ++bi;
+    }
+  };
+  flush_bars(-1);
+  for (size_t p = 0; p < passes.size(); ++p) {
+    out->push_back(std::move(passes[p]));
+    flush_bars((int)p);
+  }
+  flush_bars(INT32_MAX);
   return true;
 }
 
@@ -2843,22 +2935,29 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
         for (int q : ins.b) ok = ok && q >= 0 && q < s->L;
       } else if (ins.type == QK_INS_CSQS) {
         ok = ok && check_csqs(s, ins.a, ins.b) == QK_OK;
-        for (int q : ins.b) ok = ok && q - s->L < nb - s->L;
+        // rank bits held by other shards: a barrier of the schedule (QK_NO_XREBLOCK: block order)
+        for (int q : ins.b) ok = ok && (q < nb || !getenv("QK_NO_XREBLOCK"));
       }
     }
     const char* cenv = getenv("QK_REBLOCK_CAP");
-    if (ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w)) {
+    if (ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n)) {
       // worth it only with fewer sweeps than the block order (one per block
       // that is not diagonal-only; those fold into the pass before)
-      size_t sweeps = 0;
+      size_t sweeps = 0, passes = 0;
       for (auto& ins : s->prog) {
         if (ins.type != QK_INS_BLOCK || ins.gates.empty()) continue;
         bool dg = true;
         for (auto& g : ins.gates) dg = dg && is_diag(g.kind);
         sweeps += !dg;
       }
-      *reblocked = rprog.size() < std::max<size_t>(sweeps, 1) || getenv("QK_REBLOCK");
+      for (auto& ins : rprog) passes += ins.type == QK_INS_BLOCK;
+      *reblocked = passes < std::max<size_t>(sweeps, 1) || getenv("QK_REBLOCK");
     }
+  }
+  // reblocked: sigma is indexed by wire; wires of other shards' rank bits sit outside (-1)
+  if (*reblocked && s->n > nb) {
+    sigma.resize(s->n);
+    for (int w = nb; w < s->n; ++w) sigma[w] = -1;
   }
   const std::vector<InstrH>& prog = *reblocked ? rprog : s->prog;
   auto emit_restore = [&]() {
@@ -3165,13 +3264,17 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
         if (lazy_fold) {
           std::vector<int> dinv(nb);
           for (int q = 0; q < nb; ++q) dinv[dphys[q]] = q;
-          std::vector<int> sig3(nb);
-          for (int q = 0; q < nb; ++q) sig3[q] = dphys[sigma[q]];
+          std::vector<int> sig3(sigma.size(), -1);
+          for (size_t q = 0; q < sigma.size(); ++q) sig3[q] = sigma[q] >= 0 ? dphys[sigma[q]] : -1;
           for (size_t j = ii + 1; j < prog.size(); ++j) {
             const InstrH& nx = prog[j];
             if (nx.type == QK_INS_BLOCK) {
               if (nx.gates.empty()) continue;
               if (!diag_block(nx)) break;
+              bool local = true;
+              for (auto& g : nx.gates)
+                for (int t : g.t) local = local && t >= 0 && t < (int)sig3.size() && sig3[t] >= 0;
+              if (!local) break;
               for (auto& g : nx.gates) {
                 GateH m = g;
                 for (int& t : m.t) t = dinv[sig3[t]];
@@ -3216,7 +3319,8 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
         ip.bytes = 32.0 * std::ldexp(1.0, nb) * ip.npass;
         ip.tile = T;
         ip.dest = dphys;
-        for (int& v : sigma) v = dphys[v];
+        for (int& v : sigma)
+          if (v >= 0) v = dphys[v];
         for (size_t j : folded_at) folded_into[j] = (int)s->iplan.size();
         s->iplan.push_back(std::move(ip));
         continue;
@@ -3477,6 +3581,37 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
       if (rc) return rc;
       // rank bits held inside this handle become plain address bits
       const int held_rank_bits = nb - s->L;
+      if (ins.rb) {
+        // a barrier of the cross-block schedule: exchange on the layout as it
+        // is (position q holds wire xw[q] at physical bit sigma[xw[q]]), then
+        // the wires move: held pairs swap bits, incoming wires take the bits
+        // of the outgoing ones
+        std::vector<int> xl(nb);
+        for (int q = 0; q < nb; ++q) {
+          xl[q] = sigma[ins.xw[q]];
+          if (xl[q] < 0) return fail(QK_ESIM, "internal: reblocked exchange on a non-local wire");
+        }
+        ip.a = ins.a;
+        ip.b = ins.b;
+        ip.csqs_s = (int)ins.a.size();
+        ip.sqs = -2;
+        ip.xlay = xl;
+        int so = 0;
+        for (int q : ins.b) so += q - s->L >= held_rank_bits;
+        ip.bytes = 16.0 * std::ldexp(1.0, s->L) * s->count * (1.0 - std::ldexp(1.0, -so));
+        std::vector<int> sa = ins.a, sb = ins.b;
+        std::sort(sa.begin(), sa.end());
+        std::sort(sb.begin(), sb.end());
+        std::vector<int> ns = sigma;
+        for (size_t k = 0; k < sa.size(); ++k) {
+          const int wa = ins.xw[sa[k]], wb = ins.xw[sb[k]];
+          ns[wb] = sigma[wa];
+          ns[wa] = sb[k] < nb ? sigma[wb] : -1;
+        }
+        sigma = ns;
+        s->iplan.push_back(std::move(ip));
+        continue;
+      }
       bool local_only = true;
       for (int q : ins.b)
         if (q - s->L >= held_rank_bits) local_only = false;
@@ -5045,20 +5180,32 @@ int qk_read_logical_range(qk_sim* s, const int32_t* perm, uint64_t start, uint64
   return QK_OK;
 }
 
-int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params, size_t nparams, int n, int cap,
-                      int32_t* out_words, size_t* out_nwords, double* out_params, size_t* out_nparams,
-                      int32_t* p2w, int* npass) {
-  if (!words || !out_nwords || !out_nparams || !npass || n < 1 || n > 64) return fail(QK_EINVAL, "bad argument");
+static int reblock_packed_impl(const int32_t* words, size_t nwords, const double* params, size_t nparams, int n,
+                               int nlocal, int cap, int32_t* out_words, size_t* out_nwords, double* out_params,
+                               size_t* out_nparams, int32_t* p2w, int* npass) {
+  if (!words || !out_nwords || !out_nparams || !npass || n < 1 || n > 64 || nlocal < 1 || nlocal > n)
+    return fail(QK_EINVAL, "bad argument");
   int rc = 0;
   std::string emsg;
   std::vector<InstrH> prog = unpack(words, nwords, params, nparams, &rc, emsg);
   if (rc) return fail(rc, "%s", emsg.c_str());
   std::vector<InstrH> out;
   std::vector<int> pw;
-  if (!reblock(prog, n, cap, 3, &out, &pw)) {
+  if (!reblock(prog, nlocal, cap, 3, &out, &pw, n)) {
     *npass = 0;
     return QK_OK;
   }
+  // a barrier (cross-shard CSQS) goes out as its outgoing and incoming wires
+  for (auto& ins : out)
+    if (ins.type == QK_INS_CSQS && !ins.xw.empty()) {
+      std::vector<int> sa = ins.a, sb = ins.b;
+      std::sort(sa.begin(), sa.end());
+      std::sort(sb.begin(), sb.end());
+      for (size_t k = 0; k < sa.size(); ++k) {
+        ins.a[k] = ins.xw[sa[k]];
+        ins.b[k] = ins.xw[sb[k]];
+      }
+    }
   std::vector<int32_t> w;
   std::vector<double> p;
   pack_prog(out, &w, &p);
@@ -5071,8 +5218,24 @@ int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params,
   }
   *out_nwords = w.size();
   *out_nparams = p.size();
-  *npass = (int)out.size();
+  int np = 0;
+  for (auto& ins : out) np += ins.type == QK_INS_BLOCK;
+  *npass = np;
   return QK_OK;
+}
+
+int qk_reblock_packed(const int32_t* words, size_t nwords, const double* params, size_t nparams, int n, int cap,
+                      int32_t* out_words, size_t* out_nwords, double* out_params, size_t* out_nparams,
+                      int32_t* p2w, int* npass) {
+  return reblock_packed_impl(words, nwords, params, nparams, n, n, cap, out_words, out_nwords, out_params,
+                             out_nparams, p2w, npass);
+}
+
+int qk_reblock_shard(const int32_t* words, size_t nwords, const double* params, size_t nparams, int n, int nlocal,
+                     int cap, int32_t* out_words, size_t* out_nwords, double* out_params, size_t* out_nparams,
+                     int32_t* p2w, int* npass) {
+  return reblock_packed_impl(words, nwords, params, nparams, n, nlocal, cap, out_words, out_nwords, out_params,
+                             out_nparams, p2w, npass);
 }
 
 int qk_parse_text(const char* text, size_t len, int n, int local, int c, int32_t* words, size_t* nwords,
