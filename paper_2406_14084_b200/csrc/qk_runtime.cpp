@@ -2710,6 +2710,24 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
         cand &= cand - 1;
         rows[r] = w;
       }
+    } else if (cur_seg < (int)bars.size()) {
+      // the segment's last pass: wires that leave at the barrier come off the
+      // row bits (an exchange over bits 0..2 moves 16-B pieces)
+      uint64_t leave = 0, onrow = 0;
+      for (size_t k = 0; k < bars[cur_seg].ins->b.size(); ++k) {
+        std::vector<int> sa = bars[cur_seg].ins->a, sb = bars[cur_seg].ins->b;
+        std::sort(sa.begin(), sa.end());
+        std::sort(sb.begin(), sb.end());
+        if (sb[k] >= nb) leave |= 1ull << bars[cur_seg].xw[sa[k]];
+      }
+      for (int r = 0; r < rowbits; ++r) onrow |= 1ull << rows[r];
+      uint64_t cand = S & ~leave & ~onrow;
+      for (int r = 0; r < rowbits && cand; ++r) {
+        if (!(leave >> rows[r] & 1)) continue;
+        const int w = __builtin_ctzll(cand);
+        cand &= cand - 1;
+        rows[r] = w;
+      }
     }
     rows_after.push_back(rows);
     // the layout after the pass: only the row assignment matters here
@@ -3158,9 +3176,19 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
           // the scheduler's rows: rows_next on bits 0.., then the next pass's
           // tile wires, then the rest, each group in ascending bit order,
           // onto the tile's bits in ascending order
-          std::vector<char> used(nb, 0), nxt(nb, 0);
+          std::vector<char> used(nb, 0), nxt(nb, 0), leave(nb, 0);
           if (jj < prog.size())
             for (int w : prog[jj].tile_w) nxt[sigma[w]] = 1;
+          if (jj < prog.size() && prog[jj].type == QK_INS_CSQS && prog[jj].rb) {
+            // a barrier next: the wires it sends away go to the highest tile
+            // bits, so the exchange moves long contiguous runs
+            const InstrH& bx = prog[jj];
+            std::vector<int> sa = bx.a, sb = bx.b;
+            std::sort(sa.begin(), sa.end());
+            std::sort(sb.begin(), sb.end());
+            for (size_t k = 0; k < sa.size(); ++k)
+              if (sb[k] >= nb && sigma[bx.xw[sa[k]]] >= 0) leave[sigma[bx.xw[sa[k]]]] = 1;
+          }
           std::vector<int> srcs;
           bool rows_ok = true;
           for (int w : ins.rows_next) {
@@ -3173,6 +3201,8 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
           if (rows_ok && (int)srcs.size() <= (inT[2] ? 3 : 2)) {
             for (int x : T)
               if (!used[x] && nxt[x]) used[x] = 1, srcs.push_back(x);
+            for (int x : T)
+              if (!used[x] && !leave[x]) used[x] = 1, srcs.push_back(x);
             for (int x : T)
               if (!used[x]) used[x] = 1, srcs.push_back(x);
             dphys = ident;
@@ -3609,6 +3639,11 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
           ns[wa] = sb[k] < nb ? sigma[wb] : -1;
         }
         sigma = ns;
+        if (getenv("QK_DUMP_PLAN")) {
+          fprintf(stderr, "reblocked csqs: exchanged local positions at physical bits");
+          for (int q : ins.a) fprintf(stderr, " %d", xl[q]);
+          fprintf(stderr, "\n");
+        }
         s->iplan.push_back(std::move(ip));
         continue;
       }
@@ -4807,10 +4842,15 @@ int qk_plan_dry(const char* text, size_t len, int n, int c, int second_buffer, c
   if ((!text && len) || n < 1 || n > 48) return fail(QK_EINVAL, "bad argument");
   qk_sim s;
   s.dry = true;
+  // (dev: QK_DRY_R=r plans one shard of a 2^r-GPU job, one rank partition each)
+  const int dr = getenv("QK_DRY_R") ? atoi(getenv("QK_DRY_R")) : 0;
+  if (dr < 0 || dr >= n) return fail(QK_EINVAL, "bad QK_DRY_R");
   s.n = n;
-  s.L = n;
-  s.nbits = n;
-  s.amps = (size_t)1 << n;
+  s.r = dr;
+  s.L = n - dr;
+  s.nbits = n - dr;
+  s.amps = (size_t)1 << (n - dr);
+  s.b = n - dr;
   static double fake[2];
   s.bufs[0] = &fake[0];  // never dereferenced: planning only tests them for presence
   s.bufs[1] = second_buffer ? &fake[1] : nullptr;
@@ -4818,7 +4858,7 @@ int qk_plan_dry(const char* text, size_t len, int n, int c, int second_buffer, c
   if (dump_dir) s.dry_dir = dump_dir;
   Parser ps;
   ps.n = n;
-  ps.local = n;
+  ps.local = n - dr;
   ps.c = c;
   if (ps.run(text, len, &s.prog)) return fail(ps.code, "%s", ps.msg.c_str());
   const int rc = compile_program(&s);
