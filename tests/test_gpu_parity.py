@@ -493,13 +493,32 @@ def test_wide_chunk_lazy_layout_at_33_qubits(gpu):
 
 
 @pytest.mark.gpu
-def test_fused_norm_matches_full_sum_and_invalidates(gpu):
+@pytest.mark.parametrize("mode", ["default", "eager", "block_order", "no_zbound"])
+def test_fused_norm_matches_full_sum_and_invalidates(gpu, mode):
     """The run's last pass sums |amp|^2 of what it stores; qk_sumsq then only
     adds the per-group partials. It must equal the full-state sum, and any
-    later writer must fall back to the full sum."""
+    later writer must fall back to the full sum. Every store path: the lazy
+    layout with the cross-block schedule (default), the relabeled/eager modes
+    (QK_NO_LAZY12), the optimizer's block order (QK_NO_REBLOCK), full reads
+    after the first pass (QK_NO_ZBOUND), and a 2^30-amplitude state."""
     import os
     from conftest import ROOT
-    for name, n, c in (("qaoa24_c12_r0.txt", 24, 12), ("qft20_c10_r0.txt", 20, 10)):
+    env = {"eager": {"QK_NO_LAZY12": "1"}, "block_order": {"QK_NO_REBLOCK": "1"},
+           "no_zbound": {"QK_NO_ZBOUND": "1"}}.get(mode, {})
+    cases = [("qaoa24_c12_r0.txt", 24, 12), ("qft20_c10_r0.txt", 20, 10)]
+    if mode in ("default", "eager"):
+        cases.append(("qaoa30_c12_r0.txt", 30, 12))
+    os.environ.update(env)
+    try:
+        _fused_norm_cases(cases, ROOT)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+
+
+def _fused_norm_cases(cases, ROOT):
+    import os
+    for name, n, c in cases:
         text = open(os.path.join(ROOT, "bench_circuits", name)).read()
         sim = Simulator(LayoutParams(n=n, c=n))
         perm = sim.load_text(text, c)
@@ -520,4 +539,4 @@ def test_fused_norm_matches_full_sum_and_invalidates(gpu):
         finally:
             os.environ.pop("QK_NO_FUSED_NORM")
         assert after == want and after > 20.0
-        sim.close()
+        sim.release()
