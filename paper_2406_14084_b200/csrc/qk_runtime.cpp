@@ -2618,6 +2618,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     }
   }
   const int N = (int)nd.size();
+  int first_open = 0;  // every gate before it is done (closure scans start here)
   std::vector<int> nseg(N);
   for (int k = 0; k < N; ++k) nseg[k] = seg_of_gate((size_t)nd[k]);
   int cur_seg = 0;
@@ -2625,14 +2626,22 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   std::vector<uint64_t> done(NW, 0);
   auto isdone = [&](const std::vector<uint64_t>& d, int k) { return (d[k / 64] >> (k % 64)) & 1; };
   // the non-diagonal gates a tile S can run now (in program order)
+  // (a wire is blocked once a gate on it cannot run: every later gate on it
+  // depends on that one, so the scan stops when all tile wires are blocked)
   auto closure = [&](uint64_t S, std::vector<uint64_t>& now, int* cnt) {
     now = done;
     int c = 0;
-    for (int k = 0; k < N; ++k) {
-      if (nseg[k] != cur_seg || isdone(now, k) || (G[nd[k]].wm & ~S)) continue;
-      bool ok = true;
+    uint64_t blocked = 0;
+    for (int k = first_open; k < N; ++k) {
+      if (nseg[k] != cur_seg || isdone(now, k)) continue;
+      const uint64_t wm = G[nd[k]].wm;
+      bool ok = !(wm & ~S) && !(wm & blocked);
       for (size_t w = 0; w < pre[k].size() && ok; ++w) ok = !(pre[k][w] & ~now[w]);
-      if (!ok) continue;
+      if (!ok) {
+        blocked |= wm;
+        if ((blocked & S) == S) break;
+        continue;
+      }
       now[k / 64] |= 1ull << (k % 64);
       ++c;
     }
@@ -2691,6 +2700,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
     for (int k = 0; k < N; ++k)
       if (isdone(now, k) && !isdone(done, k)) npass[k] = (int)tiles.size();
     done = now;
+    while (first_open < N && isdone(done, first_open)) ++first_open;
     left -= c;
     tiles.push_back(S);
     // row bits after this pass: wires the next pass (lookahead) wants that the
@@ -2958,7 +2968,12 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
       }
     }
     const char* cenv = getenv("QK_REBLOCK_CAP");
-    if (ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n)) {
+    const auto trb = std::chrono::steady_clock::now();
+    const bool rbok = ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n);
+    if (getenv("QK_DUMP_LOAD"))
+      fprintf(stderr, "load: reblock %.3f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trb).count());
+    if (rbok) {
       // worth it only with fewer sweeps than the block order (one per block
       // that is not diagonal-only; those fold into the pass before)
       size_t sweeps = 0, passes = 0;
