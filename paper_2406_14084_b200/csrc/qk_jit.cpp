@@ -319,6 +319,42 @@ std::string lazy_loads(const TmaParams& tp, const char* cv, const char* dst, boo
 
 }  // namespace
 
+// TMA stores of one strided tile from the stage image (same boxes and
+// coordinates as lazy_loads, so an in-place pass writes back what it read).
+std::string lazy_stores(const TmaParams& tp, const char* cv, const char* src, const char* ind) {
+  TileDims td;
+  if (!tile_dims(tp.tbit, tp.C, tp.nbits, &td, tp.rowbits)) return "";
+  std::vector<int> oidx(tp.nbits, -1), tidx(tp.nbits, -1);
+  for (int k = 0; k < tp.C; ++k) tidx[tp.tbit[k]] = k;
+  int no = 0;
+  for (int p = 0; p < tp.nbits; ++p)
+    if (tidx[p] < 0) oidx[p] = no++;
+  std::ostringstream o;
+  for (int it = 0; it < (1 << td.nit); ++it) {
+    o << ind << "asm volatile(\"cp.async.bulk.tensor." << td.rank << "d.global.shared::cta.bulk_group [%0, {";
+    for (int jd = 0; jd < td.rank; ++jd) o << (jd ? ", " : "") << "%" << 1 + jd;
+    o << "}], [%" << 1 + td.rank << "];\" :: \"l\"(&p.map)";
+    for (int jd = 0; jd < td.rank; ++jd) {
+      if (jd == 0) {
+        o << ", \"r\"(0)";
+        continue;
+      }
+      o << ", \"r\"((int)(0ull";
+      uint64_t konst = 0;
+      for (int p = td.lo[jd]; p < td.lo[jd] + td.len[jd]; ++p) {
+        if (oidx[p] >= 0)
+          o << " | (((" << cv << " >> " << oidx[p] << ") & 1ull) << " << p - td.lo[jd] << ")";
+        else if (td.box[jd] == 1 && tidx[p] >= td.inbox && ((it >> (tidx[p] - td.inbox)) & 1))
+          konst |= 1ull << (p - td.lo[jd]);
+      }
+      o << " | " << konst << "ull))";
+    }
+    o << ", \"r\"(su32(" << src << " + " << ((size_t)it << td.inbox) * 16 << ")) : \"memory\");\n";
+  }
+  o << ind << "asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n";
+  return o.str();
+}
+
 // Shared-memory slices of per-chunk diagonal tables (12-bit passes with the
 // table-aware chunk order). A table's chunk bits (co_v) are its top index
 // bits, so the entries one chunk reads are one contiguous slice of
@@ -546,6 +582,26 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
     const Layout& ll = layouts[tp.nphases - 1];
     lf = indep3(ll[rl[0]], ll[rl[1]], ll[rl[2]]) ? ll : choose_layout(C, tp.ph[tp.nphases - 1].tpos, rl);
   }
+  // Variant bit 8: TMA-store epilogue (lazy in-place passes). The last phase
+  // writes its amplitudes into the stage at their destination tile positions
+  // (the TMA image layout); the producer stores the image with the same boxes
+  // it loaded and waits for the TMA unit to have read it before it refills the
+  // stage. The consumers issue no global stores.
+  std::vector<int> Dm(C, -1);  // tile position -> destination tile position
+  bool tstore = (variant & 8) && tp.lazy && !tp.xbits && tp.permuted && !getenv("QK_NO_TSTORE");
+  if (tstore)
+    for (int x = 0; x < C && tstore; ++x) {
+      for (int k = 0; k < C; ++k)
+        if (tp.tbit[k] == tp.dpos[x]) Dm[x] = k;
+      tstore = Dm[x] >= 0;
+    }
+  if ((variant & 8) && !tstore) return false;
+  auto dmap = [&](uint32_t pos) {
+    uint32_t d = 0;
+    for (int x = 0; x < C; ++x)
+      if (pos >> x & 1) d |= 1u << Dm[x];
+    return d;
+  };
   int tab_i = 0;
   const int exp_skip = getenv("QK_EXP_SKIP") ? atoi(getenv("QK_EXP_SKIP")) : 0;
   for (int ph = 0; ph < tp.nphases; ++ph) {
@@ -897,6 +953,18 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       emit_lay_base(b, "lw", wrl, D.tpos, T);
       for (int j = 0; j < NA; ++j) b << "    sm[lw ^ " << lay(wrl, D.rloc[j]) << "u] = v[" << j << "];\n";
       b << "    gbar(bar_id, " << GT << ");\n";
+    } else if (tstore) {
+      // every thread's reads of the stage are done before any final write
+      b << "    gbar(bar_id, " << GT << ");\n";
+      b << "    { const u32 ls = 0u";
+      for (int k = 0; k < T; ++k) b << " ^ (((tid >> " << k << ") & 1u) * " << lay(layouts[0], dmap(1u << D.tpos[k])) << "u)";
+      b << ";\n";
+      for (int j = 0; j < NA; ++j) b << "      sm[ls ^ " << lay(layouts[0], dmap(D.rloc[j])) << "u] = v[" << j << "];\n";
+      b << "    }\n";
+      b << "    fence_async_smem();\n    gbar(bar_id, " << GT << ");\n";
+      b << "    if (tid == 0) mbar_arrive(empty + s);\n";
+      if (tp.norm)
+        for (int j = 0; j < NA; ++j) b << "    nacc = fma(v[" << j << "].x, v[" << j << "].x, fma(v[" << j << "].y, v[" << j << "].y, nacc));\n";
     } else {
       b << "    fence_async_smem();\n    gbar(bar_id, " << GT << ");\n";
       b << "    if (tid == 0) mbar_arrive(empty + s);\n";
@@ -1065,6 +1133,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       << "        const u64 chunk = " << chunk_of("i") << ";\n"
       << "        const int s = (int)(i % " << st << "); const u32 round = (u32)(i / " << st << ");\n"
       << "        if (round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n";
+    if (tstore)
+      o << "        if (round > 0) {\n          const u64 pchunk = " << chunk_of(("(i - " + std::to_string(st) + "ull)").c_str())
+        << ";\n          unsigned char* srcb = base + (size_t)s * stage_bytes;\n"
+        << lazy_stores(tp, "pchunk", "srcb", "          ")
+        << "          asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n        }\n";
   } else {
     // OP_QUAD: the whole producer warp turns the chunk bits into the
     // per-position factors of every quadratic op in a pending slot while the
@@ -1135,12 +1208,21 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
         << "      }\n";
     }
   }
+  std::string tstore_src;
+  if (tstore && NQ)
+    tstore_src = "      if (lane == 0 && round > 0) {\n        const u64 pchunk = " +
+                 chunk_of(("(i - " + std::to_string(st) + "ull)").c_str()) +
+                 ";\n        unsigned char* srcb = base + (size_t)s * stage_bytes;\n" +
+                 lazy_stores(tp, "pchunk", "srcb", "        ") +
+                 "        asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n      }\n";
   if (NQ && (variant & 4))  // variant bit 4: factors straight into the stage's slot after the wait
     o << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
+      << tstore_src
       << "      __syncwarp();\n" << fsrc.str() << "      __syncwarp();\n"
       << "      if (lane == 0) {\n";
   else if (NQ)
     o << fsrc.str() << "      if (lane == 0 && round > 0) mbar_wait(empty + s, (round - 1) & 1u);\n"
+      << tstore_src
       << "      __syncwarp();\n"
       << "      for (u32 e = lane; e < " << NQ * FS << "u; e += 32u) fac[(u32)s * " << NQ * FS << "u + e] = pend[e];\n"
       << "      __syncwarp();\n"
@@ -1183,10 +1265,21 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       o << "          tma_prefetch(&p.map, 0, prow + " << t * tp.box_rows << ");\n";
     o << "        }\n";
   }
+  // TMA-store epilogue: after the last refill the final uses of the stages
+  // still hold results; store them and wait for the writes
+  std::string drain;
+  if (tstore)
+    drain = std::string("    { u64 I = 0;\n      while (") + chunk_ok("I") + ") ++I;\n" +
+            "      for (u64 j = I > " + std::to_string(st) + "ull ? I - " + std::to_string(st) + "ull : 0ull; j < I; ++j) {\n" +
+            "        const int s = (int)(j % " + std::to_string(st) + "); const u32 round = (u32)(j / " + std::to_string(st) + ");\n" +
+            "        mbar_wait(empty + s, round & 1u);\n" +
+            "        const u64 pchunk = " + chunk_of("j") + ";\n" +
+            "        unsigned char* srcb = base + (size_t)s * stage_bytes;\n" + lazy_stores(tp, "pchunk", "srcb", "        ") +
+            "      }\n      asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n    }\n";
   if (NQ)
-    o << "      }\n    }\n    return;\n  }\n";
+    o << "      }\n    }\n" << (drain.empty() ? "" : "    if (lane == 0)\n" + drain) << "    return;\n  }\n";
   else
-    o << "      }\n    }\n    return;\n  }\n";
+    o << "      }\n" << drain << "    }\n    return;\n  }\n";
   o << "  const int ct = threadIdx.x - 32;\n"
     << "  const int g = ct >> " << T << ";\n"
     << "  const u32 tid = ct & " << (GT - 1) << "u;\n"

@@ -2232,9 +2232,10 @@ int upload_plan(qk_sim* s) {
     std::vector<int> src_pass, src_var;
     std::vector<std::vector<long long>> toffs;
     std::vector<std::vector<double>> coefs;
-    // Up to eight variants per pass (bit 1: no hoisted table, bit 2: quadratic
+    // Up to sixteen variants per pass (bit 1: no hoisted table, bit 2: quadratic
     // table groups, bit 4: OP_QUAD factors computed after the stage wait
-    // instead of ahead in a pending slot); identical sources are built once. QK_JIT_VARIANT=v pins
+    // instead of ahead in a pending slot, bit 8: TMA-store epilogue for lazy
+    // passes); identical sources are built once. QK_JIT_VARIANT=v pins
     // one, otherwise the first runs time every variant and keep the fastest
     // per pass structure (process-wide, tune_pick / tune_record).
     const char* venv = getenv("QK_JIT_VARIANT");
@@ -2245,7 +2246,7 @@ int upload_plan(qk_sim* s) {
       if (s->pass_tma[p] < 0) continue;
       std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
       std::vector<std::string> seen;
-      for (int variant = 0; variant < 8; ++variant) {
+      for (int variant = 0; variant < 16; ++variant) {
         if (venv && variant != atoi(venv)) continue;
         std::string src;
         std::vector<long long> toff;
@@ -2407,7 +2408,7 @@ int upload_plan_dry(qk_sim* s) {
     fprintf(stderr, "\n");
     if (s->pass_tma[p] < 0 || s->dry_dir.empty()) continue;
     std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
-    for (int variant = 0; variant < 8; ++variant) {
+    for (int variant = 0; variant < 16; ++variant) {
       std::string src;
       std::vector<long long> toff;
       std::vector<double> coef;
@@ -3842,7 +3843,26 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
     tp.out = flip ? s->bufs[s->cur ^ 1] : s->bufs[s->cur];
     int rc;
     if (p < (int)s->pass_jit.size() && s->pass_jit[p]) {
-      std::vector<uint64_t>& blob = s->jit_blob[p];
+      void* kern = s->pass_jit[p];
+      std::vector<uint64_t>* bl = &s->jit_blob[p];
+      if (from_fresh && p < (int)s->pass_var.size()) {
+        // a TMA-store variant (bit 8) writes through the load view: with a
+        // bounded view it would drop the stores beyond the bound, so the
+        // pass runs its register-store twin
+        int cur = -1;
+        for (auto& v : s->pass_var[p])
+          if (v.kern == kern) cur = v.variant;
+        if (cur >= 0 && (cur & 8)) {
+          kern = nullptr;
+          for (auto& v : s->pass_var[p])
+            if (v.variant == (cur ^ 8)) {
+              kern = v.kern;
+              bl = &v.blob;
+            }
+          if (!kern) return fail(QK_ESIM, "internal: no register-store twin for a bounded pass");
+        }
+      }
+      std::vector<uint64_t>& blob = *bl;
       memcpy(blob.data(), lazy_map, 128);
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
@@ -3851,9 +3871,9 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
         blob[19] = nch;
         blob[21] = split;
       }
-      rc = tp.xbits ? jit_launch_x(s->pass_jit[p], blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
+      rc = tp.xbits ? jit_launch_x(kern, blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
-                    : jit_launch(s->pass_jit[p], blob.data(), tp.C, tp.M, nch, s->num_sms, (CUstream_st*)s->stream,
+                    : jit_launch(kern, blob.data(), tp.C, tp.M, nch, s->num_sms, (CUstream_st*)s->stream,
                                  tp.smax, jit_slice_bytes(tp), jit_pairs(tp) ? 2 : 1);
       if (split) {
         blob[19] = tp.nchunks;
