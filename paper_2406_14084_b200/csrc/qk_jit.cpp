@@ -89,6 +89,7 @@ struct QkJitParams {
   u64 split;  // sub-launch over part of the chunks (qk_insert); 0 = every chunk
   long long toff[QK_NTAB + 1];
   double coef[QK_NCOEF + 1];
+  QkMap smap;  // unbounded view of the state (TMA-store epilogue; map may be a bounded load view)
 };
 __device__ __forceinline__ u32 su32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* b, u32 n) {
@@ -333,7 +334,7 @@ std::string lazy_stores(const TmaParams& tp, const char* cv, const char* src, co
   for (int it = 0; it < (1 << td.nit); ++it) {
     o << ind << "asm volatile(\"cp.async.bulk.tensor." << td.rank << "d.global.shared::cta.bulk_group [%0, {";
     for (int jd = 0; jd < td.rank; ++jd) o << (jd ? ", " : "") << "%" << 1 + jd;
-    o << "}], [%" << 1 + td.rank << "];\" :: \"l\"(&p.map)";
+    o << "}], [%" << 1 + td.rank << "];\" :: \"l\"(&p.smap)";
     for (int jd = 0; jd < td.rank; ++jd) {
       if (jd == 0) {
         o << ", \"r\"(0)";

@@ -2279,8 +2279,10 @@ int upload_plan(qk_sim* s) {
     for (size_t i = 0; i < srcs.size(); ++i) {
       if (!handles[i]) continue;
       const int p = src_pass[i];
-      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | split | toff[ntab+1] | coef[ncoef+1]
-      std::vector<uint64_t> blob(16 + 6 + toffs[i].size() + 1 + coefs[i].size() + 1 + 8, 0);
+      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | split | toff[ntab+1] |
+      // coef[ncoef+1] | smap[16 words] (64-B aligned: the last 16 words of the blob)
+      const size_t smap_off = (16 + 6 + toffs[i].size() + 1 + coefs[i].size() + 1 + 7) & ~(size_t)7;
+      std::vector<uint64_t> blob(smap_off + 16, 0);
       blob[16] = (uint64_t)(uintptr_t)s->d_pool;
       const TmaParams& tq = s->tma[s->pass_tma[p]];
       blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
@@ -3845,10 +3847,8 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
     if (p < (int)s->pass_jit.size() && s->pass_jit[p]) {
       void* kern = s->pass_jit[p];
       std::vector<uint64_t>* bl = &s->jit_blob[p];
-      if (from_fresh && p < (int)s->pass_var.size()) {
-        // a TMA-store variant (bit 8) writes through the load view: with a
-        // bounded view it would drop the stores beyond the bound, so the
-        // pass runs its register-store twin
+      if (from_fresh && p < (int)s->pass_var.size() && getenv("QK_TSTORE_TWIN")) {
+        // (dev) run a TMA-store variant's register-store twin on bounded passes
         int cur = -1;
         for (auto& v : s->pass_var[p])
           if (v.kern == kern) cur = v.variant;
@@ -3864,6 +3864,11 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       }
       std::vector<uint64_t>& blob = *bl;
       memcpy(blob.data(), lazy_map, 128);
+      {  // the unbounded view, for the TMA-store epilogue
+        const CUtensorMap* full =
+            tp.lazy ? (s->cur ? &s->lazy_map1[s->pass_tma[p]] : &tp.map) : &tp.map;
+        memcpy(blob.data() + blob.size() - 16, full, 128);
+      }
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
       const uint64_t nch = split ? tp.nchunks >> (split & 3) : tp.nchunks;
