@@ -87,7 +87,7 @@ def analytic_factors(fam: str, n: int):
 
 
 METRIC = "circuit sim time (s), achieved HBM GB/s vs 8 TB/s, at 1/2/4/8 B200"
-AUTOTUNE_RUNS = 16  # untimed setup runs: one per kernel variant (qk_runtime.cpp tune_pick)
+AUTOTUNE_RUNS = 32  # untimed setup runs: every kernel variant timed twice (qk_runtime.cpp tune_pick)
 REASONS = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
 
 

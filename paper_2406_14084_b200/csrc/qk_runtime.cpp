@@ -2056,9 +2056,16 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
 // ms of every variant seen so far and, once all are timed, the fastest.
 struct TuneRec {
   std::vector<int> variants;
-  std::vector<double> ms;  // < 0: not timed yet
+  std::vector<double> ms;  // fastest timing so far (< 0: not timed yet)
+  std::vector<int> cnt;    // timings so far
   int best = -1;
 };
+// every variant is timed this many times (its fastest counts), so one noisy
+// run does not decide (QK_TUNE_ROUNDS)
+int tune_rounds() {
+  static const int r = getenv("QK_TUNE_ROUNDS") ? std::max(1, atoi(getenv("QK_TUNE_ROUNDS"))) : 2;
+  return r;
+}
 std::mutex g_tune_mu;
 std::unordered_map<std::string, TuneRec> g_tune;
 
@@ -2074,15 +2081,17 @@ bool tune_pick(qk_sim* s, int p, bool tuning) {
     for (auto& v : s->pass_var[p]) {
       tr.variants.push_back(v.variant);
       tr.ms.push_back(-1.0);
+      tr.cnt.push_back(0);
     }
   int pick = -1;
   if (tr.best >= 0) {
     pick = tr.best;
   } else if (tuning && !getenv("QK_NO_TUNE")) {
-    for (size_t k = 0; k < tr.ms.size(); ++k)
-      if (tr.ms[k] < 0) {
+    int least = INT32_MAX;
+    for (size_t k = 0; k < tr.cnt.size(); ++k)
+      if (tr.cnt[k] < least) {
+        least = tr.cnt[k];
         pick = tr.variants[k];
-        break;
       }
   }
   if (pick < 0) pick = tr.variants[0];
@@ -2103,9 +2112,13 @@ void tune_record(qk_sim* s, int p, double ms) {
   TuneRec& tr = g_tune[s->pass_key[p]];
   double best_ms = 1e300;
   int best = -1;
+  for (size_t i = 0; i < tr.variants.size(); ++i)
+    if (tr.variants[i] == variant) {
+      tr.ms[i] = tr.cnt[i] ? std::min(tr.ms[i], ms) : ms;
+      ++tr.cnt[i];
+    }
   for (size_t i = 0; i < tr.variants.size(); ++i) {
-    if (tr.variants[i] == variant) tr.ms[i] = ms;
-    if (tr.ms[i] < 0) return;  // still untimed variants
+    if (tr.cnt[i] < tune_rounds()) return;  // still variants to time
     if (tr.ms[i] < best_ms) {
       best_ms = tr.ms[i];
       best = tr.variants[i];

@@ -13,7 +13,7 @@ sim = Simulator(LayoutParams(n=n, c=n - r, r=r))
 os.environ["QK_DUMP_PLAN"] = "1"
 perm = sim.load_text(text, c)
 del os.environ["QK_DUMP_PLAN"]
-for _ in range(17):  # the first runs time every kernel variant (autotune, 16 variants)
+for _ in range(33):  # the first runs time every kernel variant twice (autotune, 16 variants)
     sim.handle.reset()
     sim.run_loaded(perm)
 os.environ["QK_DUMP_TIMES"] = "1"
