@@ -285,7 +285,8 @@ int jit_launch(void* kern, const void* params, int C, int M, uint64_t nchunks, i
                int smax = 0, int extra_smem = 0, int cluster = 1);
 // shared-memory bytes of the table slices a specialised pass stages (qk_jit.cpp slice_plan)
 int jit_slice_bytes(const TmaParams& tp);
-bool jit_pairs(const TmaParams& tp);  // 2-CTA cluster pairs for 128-B-row strided tiles
+bool jit_pairs(const TmaParams& tp);
+bool jit_corder(const TmaParams& tp);  // the specialised kernel walks the table-aware chunk order  // 2-CTA cluster pairs for 128-B-row strided tiles
 // cluster-exchange pass: 2^xbits CTAs per cluster, nsuper supertiles
 int jit_launch_x(void* kern, const void* params, int C, int M, int xbits, uint64_t nsuper, CUstream_st* stream);
 int launch_build_tables(const TableDesc* d_tables, int ntables, const TableGate* d_gates,

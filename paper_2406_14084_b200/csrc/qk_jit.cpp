@@ -414,6 +414,12 @@ int jit_slice_bytes(const TmaParams& tp) {
   return b;
 }
 
+static uint64_t table_chunk_mask(const TmaParams& tp);
+// the specialised kernel walks the table-aware chunk order (cmap)
+bool jit_corder(const TmaParams& tp) {
+  return table_chunk_mask(tp) && tp.C >= 12 && !getenv("QK_NO_CORDER");
+}
+
 // Chunk bits the pass's diagonal tables read (per-chunk table terms).
 static uint64_t table_chunk_mask(const TmaParams& tp) {
   uint64_t tmask = 0;

@@ -1588,6 +1588,11 @@ struct qk_sim {
   // rest without HBM reads, and the bound grows to the pass's highest tile bit
   // (its gates and in-tile permutation touch no other bit).
   int zbits = 64;
+  // memory of the current buffer at amplitudes >= 2^zmem was never written in
+  // this run (logically zero; 64: all written). A pass that reads through a
+  // bounded view skips the chunks above its next bound (they are zero and no
+  // later pass reads them); any reader outside the passes fills them first.
+  int zmem = 64, zmem_next = 64;
   double fresh_saved = 0;  // read bytes skipped this way (kept out of the stats)
   std::vector<double> saved_i;  // per instruction of the last run: read bytes skipped
   double* state = nullptr;      // == bufs[cur]
@@ -1771,8 +1776,16 @@ bool fresh_map(qk_sim* s, const TmaParams& tp, int zb, double* buf, CUtensorMap*
 // first TMA pass reads or writes it).
 int ensure_full(qk_sim* s) {
   s->zbits = 64;  // the caller reads or writes the state outside a pass
-  if (!s->fresh) return QK_OK;
+  if (!s->fresh) {
+    if (s->zmem < s->nbits) {  // the part the skipping passes never wrote
+      const size_t lo = (size_t)1 << s->zmem;
+      s->zmem = 64;
+      CUDA_TRY(cudaMemsetAsync(s->bufs[s->cur] + 2 * lo, 0, (s->amps - lo) * 16, s->stream));
+    }
+    return QK_OK;
+  }
   s->fresh = false;
+  s->zmem = 64;
   int rc = launch_fill_zero_one(s->bufs[0], s->amps, s->rank_lo == 0, (CUstream_st*)s->stream);
   return rc ? fail(QK_ECUDA, "state fill failed") : QK_OK;
 }
@@ -3876,6 +3889,27 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
         }
       }
       std::vector<uint64_t>& blob = *bl;
+      // zero support: chunks with an outer bit at or above the next bound
+      // hold zeros and no later pass reads them: a prefix of the chunk index
+      // range (outer bits ascend), so the pass runs only the chunks below it
+      uint64_t nlive = 0;
+      if (from_fresh && !split && !tp.norm && !tp.xbits && !flip && !getenv("QK_NO_ZSKIP") && !jit_corder(tp) &&
+          !jit_pairs(tp)) {
+        int hi = tp.lazy ? 0 : tp.C - 1;
+        std::vector<char> in_tile(s->nbits, 0);
+        if (tp.lazy)
+          for (int x = 0; x < tp.C; ++x) hi = std::max(hi, (int)tp.tbit[x]), in_tile[tp.tbit[x]] = 1;
+        else
+          for (int x = 0; x < tp.C; ++x) in_tile[x] = 1;
+        const int zb2 = std::max(zb, hi + 1);
+        if (zb2 < s->nbits) {
+          int nlo = 0;
+          for (int b = 0; b < zb2; ++b) nlo += !in_tile[b];
+          nlive = 1ull << nlo;
+          s->zmem_next = zb2;
+          s->fresh_saved += 16.0 * (double)(s->amps - (1ull << zb2));  // stores skipped
+        }
+      }
       memcpy(blob.data(), lazy_map, 128);
       {  // the unbounded view, for the TMA-store epilogue
         const CUtensorMap* full =
@@ -3884,16 +3918,17 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
       }
       blob[17] = (uint64_t)(uintptr_t)tp.state;
       blob[18] = (uint64_t)(uintptr_t)tp.out;
-      const uint64_t nch = split ? tp.nchunks >> (split & 3) : tp.nchunks;
+      const uint64_t nch = split ? tp.nchunks >> (split & 3) : nlive ? nlive : tp.nchunks;
       if (split) {
         blob[19] = nch;
         blob[21] = split;
       }
+      if (nlive) blob[19] = nch;
       rc = tp.xbits ? jit_launch_x(kern, blob.data(), tp.C, tp.M, tp.xbits, tp.nchunks >> tp.xbits,
                                    (CUstream_st*)s->stream)
                     : jit_launch(kern, blob.data(), tp.C, tp.M, nch, s->num_sms, (CUstream_st*)s->stream,
                                  tp.smax, jit_slice_bytes(tp), jit_pairs(tp) ? 2 : 1);
-      if (split) {
+      if (split || nlive) {
         blob[19] = tp.nchunks;
         blob[21] = 0;
       }
@@ -3912,6 +3947,8 @@ int launch_pass(qk_sim* s, int p, uint64_t first = 0, uint64_t count_override = 
     }
     // zero support: the pass's gates and in-tile permutation touch only its
     // tile bits (a permuted store of the relabeled mode may move any bit)
+    s->zmem = s->zmem_next;  // what the pass left unwritten (64: it wrote every chunk)
+    s->zmem_next = 64;
     if (split || flip || tp.xbits || s->zbits >= s->nbits || getenv("QK_NO_ZBOUND")) {
       s->zbits = 64;
     } else {
@@ -4570,6 +4607,10 @@ int run_step(qk_sim* s, size_t i, size_t* first_exec) {
 // this run's per-class device times (ms) to cls and to the kernel stats
 int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
   CUDA_TRY(cudaSetDevice(s->device));
+  if (!s->fresh && s->zmem < s->nbits) {  // a run that never reached the top bits
+    int rc = ensure_full(s);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   int rc = check_peer_error(s);
   if (rc) return rc;
@@ -4856,6 +4897,7 @@ int qk_reset(qk_sim* s) {
   // only the first chunk is written; the rest is filled on demand (ensure_full)
   s->fresh = s->amps >= (2ull << kFreshBits) && !getenv("QK_NO_FRESH");
   s->zbits = s->fresh ? kFreshBits : 64;
+  s->zmem = s->fresh ? kFreshBits : 64;
   int rc = launch_fill_zero_one(s->state, s->fresh ? (1ull << kFreshBits) : s->amps, s->rank_lo == 0,
                                 (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
