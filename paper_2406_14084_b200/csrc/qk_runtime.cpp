@@ -1608,6 +1608,9 @@ struct qk_sim {
   // lazy in-place layout: reference address bit q of the handle's state lives
   // at physical bit lay[q]; qk_run leaves lay_final (the plan's end layout)
   std::vector<int> lay, lay_final;
+  // the plan's layout at its start (identity unless the first-use placement
+  // applies): reference bit q at physical bit plan_lay0[q]; free on |0...0>
+  std::vector<int> plan_lay0;
   std::vector<CUtensorMap> lazy_map1;  // per TMA pass: the strided view of bufs[1] (lazy passes)
   // device plan
   void* blob = nullptr;
@@ -2554,7 +2557,7 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
 // just before it (`xw`), and the next segment's passes see the wires it
 // brought in. A CSQS whose rank bits are all held here is a relabel.
 bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std::vector<InstrH>* out,
-             std::vector<int>* p2w_final, int ntot = -1) {
+             std::vector<int>* p2w_final, int ntot = -1, const std::vector<int>* init_pos = nullptr) {
   if (ntot < nb) ntot = nb;
   if (ntot > 64 || cap > nb) return false;
   std::vector<int> p2w(ntot);
@@ -2678,6 +2681,8 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   };
   std::vector<int> wire_at(nb);  // physical bit -> wire (the layout the passes see)
   for (int q = 0; q < nb; ++q) wire_at[q] = q;
+  if (init_pos)  // initial placement: wire w at physical bit (*init_pos)[w]
+    for (int w = 0; w < nb; ++w) wire_at[(*init_pos)[w]] = w;
   auto choose = [&](uint64_t forced) {
     uint64_t S = forced;
     std::vector<int> pend(ntot, INT32_MAX);
@@ -3014,6 +3019,43 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
       }
       for (auto& ins : rprog) passes += ins.type == QK_INS_BLOCK;
       *reblocked = passes < std::max<size_t>(sweeps, 1) || getenv("QK_REBLOCK");
+    }
+  }
+  // First-use placement: a run from |0...0> may start in any layout, so the
+  // wires go to physical bits in the order the schedule first puts them in a
+  // tile. The zero support then grows from the bottom: each early pass reads
+  // and writes only the prefix its wires span (QFT/BV/H circuits whose first
+  // gates sit on high qubits get the same cheap early passes as QAOA).
+  s->plan_lay0.clear();
+  if (*reblocked && !getenv("QK_NO_ZPLACE")) {
+    std::vector<int> pos(nb, -1), order;
+    for (const InstrH& ins : rprog)
+      if (ins.type == QK_INS_BLOCK)
+        for (int w : ins.tile_w)
+          if (w < nb && pos[w] < 0) {
+            pos[w] = (int)order.size();
+            order.push_back(w);
+          }
+    for (int w = 0; w < nb; ++w)
+      if (pos[w] < 0) {
+        pos[w] = (int)order.size();
+        order.push_back(w);
+      }
+    bool ident_pos = true;
+    for (int w = 0; w < nb; ++w) ident_pos = ident_pos && pos[w] == w;
+    std::vector<InstrH> rprog2;
+    std::vector<int> p2w2;
+    const char* cenv2 = getenv("QK_REBLOCK_CAP");
+    if (!ident_pos && reblock(s->prog, nb, cenv2 ? atoi(cenv2) : 12, 3, &rprog2, &p2w2, s->n, &pos)) {
+      size_t n1 = 0, n2 = 0;
+      for (auto& ins : rprog) n1 += ins.type == QK_INS_BLOCK;
+      for (auto& ins : rprog2) n2 += ins.type == QK_INS_BLOCK;
+      if (n2 <= n1) {
+        rprog.swap(rprog2);
+        rb_p2w.swap(p2w2);
+        s->plan_lay0 = pos;
+        for (int q = 0; q < nb; ++q) sigma[q] = pos[q];
+      }
     }
   }
   // reblocked: sigma is indexed by wire; wires of other shards' rank bits sit outside (-1)
@@ -4566,6 +4608,24 @@ int run_prepare(qk_sim* s, size_t* first_exec) {
   CUDA_TRY(cudaSetDevice(s->device));
   int rc = materialize(s, true);  // the plan starts from the reference layout
   if (rc) return rc;
+  if (!s->plan_lay0.empty() && !lay_identity(s->plan_lay0) && !s->fresh) {
+    // a run that does not start from |0...0>: move the data to the plan's
+    // start layout (two SQS rounds, the inverse of a restore)
+    std::vector<std::pair<int, int>> rounds[2];
+    restore_rounds(s->plan_lay0, rounds);
+    for (int r = 1; r >= 0; --r) {
+      if (rounds[r].empty()) continue;
+      std::vector<int> A, B;
+      for (auto& pr : rounds[r]) {
+        A.push_back(pr.first);
+        B.push_back(pr.second);
+      }
+      HostPlan tmp;
+      compile_sqs(tmp, A, B, s->nbits, true);
+      int rc2 = launch_sqs(s->state, &tmp.sqs[0], nullptr, (CUstream_st*)s->stream);
+      if (rc2) return fail(QK_ECUDA, "layout placement failed: %s", cudaGetErrorString((cudaError_t)rc2));
+    }
+  }
   s->fresh_saved = 0;
   *first_exec = s->iplan.size();  // the instruction whose pass read the fresh state
   s->skipped.assign(s->iplan.size(), 0);
