@@ -2651,6 +2651,7 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   }
   const int N = (int)nd.size();
   int first_open = 0;  // every gate before it is done (closure scans start here)
+  const int kFront = getenv("QK_REBLOCK_FRONT") ? atoi(getenv("QK_REBLOCK_FRONT")) : 64;
   std::vector<int> nseg(N);
   for (int k = 0; k < N; ++k) nseg[k] = seg_of_gate((size_t)nd[k]);
   int cur_seg = 0;
@@ -2690,12 +2691,23 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
       if (nseg[k] == cur_seg && !isdone(done, k))
         for (int w = 0; w < ntot; ++w)
           if (G[nd[k]].wm >> w & 1) pend[w] = k;
+    // candidates: the wires of the first open gates (the frontier); a wire
+    // whose first open gate lies further on cannot unblock more than these
+    uint64_t front = 0;
+    {
+      int seen = 0;
+      for (int k = first_open; k < N && seen < kFront; ++k)
+        if (nseg[k] == cur_seg && !isdone(done, k)) {
+          front |= G[nd[k]].wm;
+          ++seen;
+        }
+    }
     std::vector<uint64_t> tmp;
     while (popc(S) < cap) {
       int best = -1, bc = -1;
       for (int x = 0; x < nb; ++x) {
         const int w = wire_at[x];
-        if ((S >> w & 1) || pend[w] == INT32_MAX) continue;
+        if ((S >> w & 1) || pend[w] == INT32_MAX || !(front >> w & 1)) continue;
         int c = 0;
         closure(S | (1ull << w), tmp, &c);
         if (c > bc || (c == bc && pend[w] < pend[best])) {
