@@ -818,6 +818,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     return 0;
   };
   if (!sched.empty() && sched.size() + extra(sched) < phs.size() + extra(phs)) phs.swap(sched);
+  // (dev, timing only: drops the phases beyond QK_EXP_MAXPH and their gates)
+  if (const char* mx = getenv("QK_EXP_MAXPH"))
+    if ((int)phs.size() > atoi(mx) && atoi(mx) > 0) phs.resize(atoi(mx));
   // Quadratic runs of one phase (allow_quad): the parts of each run that no
   // later gate of the phase needs first — gates whose tile targets are thread
   // bits or slots no later gate of the phase acts on — commute with the rest
