@@ -2945,6 +2945,44 @@ bool reblock(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std:
   return true;
 }
 
+// The schedule is a pure function of the program and its arguments; loading
+// the same circuit again (every end-to-end step does) reuses it, like the
+// generated pass sources. Process-wide, bounded.
+void pack_prog(const std::vector<InstrH>& prog, std::vector<int32_t>* wp, std::vector<double>* pp);
+bool reblock_memo(const std::vector<InstrH>& prog, int nb, int cap, int rowbits, std::vector<InstrH>* out,
+                  std::vector<int>* p2w_final, int ntot, const std::vector<int>* init_pos) {
+  if (getenv("QK_NO_PLAN_MEMO")) return reblock(prog, nb, cap, rowbits, out, p2w_final, ntot, init_pos);
+  std::vector<int32_t> w;
+  std::vector<double> pr;
+  pack_prog(prog, &w, &pr);
+  std::string key(reinterpret_cast<const char*>(w.data()), w.size() * 4);
+  key.append(reinterpret_cast<const char*>(pr.data()), pr.size() * 8);
+  const int args[4] = {nb, cap, rowbits, ntot};
+  key.append(reinterpret_cast<const char*>(args), sizeof args);
+  if (init_pos) key.append(reinterpret_cast<const char*>(init_pos->data()), init_pos->size() * sizeof(int));
+  struct Memo {
+    bool ok;
+    std::vector<InstrH> out;
+    std::vector<int> p2w;
+  };
+  static std::mutex mu;
+  static std::map<std::string, Memo> memo;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) {
+      *out = it->second.out;
+      *p2w_final = it->second.p2w;
+      return it->second.ok;
+    }
+  }
+  const bool ok = reblock(prog, nb, cap, rowbits, out, p2w_final, ntot, init_pos);
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() > 64) memo.clear();
+  memo[key] = Memo{ok, ok ? *out : std::vector<InstrH>(), ok ? *p2w_final : std::vector<int>()};
+  return ok;
+}
+
 int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
   const auto tc0 = std::chrono::steady_clock::now();
   struct PlanTimer {
@@ -3018,7 +3056,7 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     }
     const char* cenv = getenv("QK_REBLOCK_CAP");
     const auto trb = std::chrono::steady_clock::now();
-    const bool rbok = ok && reblock(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n);
+    const bool rbok = ok && reblock_memo(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n, nullptr);
     if (getenv("QK_DUMP_LOAD"))
       fprintf(stderr, "load: reblock %.3f ms\n",
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trb).count());
@@ -3061,7 +3099,7 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     std::vector<InstrH> rprog2;
     std::vector<int> p2w2;
     const char* cenv2 = getenv("QK_REBLOCK_CAP");
-    if (!ident_pos && reblock(s->prog, nb, cenv2 ? atoi(cenv2) : 12, 3, &rprog2, &p2w2, s->n, &pos)) {
+    if (!ident_pos && reblock_memo(s->prog, nb, cenv2 ? atoi(cenv2) : 12, 3, &rprog2, &p2w2, s->n, &pos)) {
       size_t n1 = 0, n2 = 0;
       for (auto& ins : rprog) n1 += ins.type == QK_INS_BLOCK;
       for (auto& ins : rprog2) n2 += ins.type == QK_INS_BLOCK;
