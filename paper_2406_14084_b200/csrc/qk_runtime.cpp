@@ -3117,6 +3117,7 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     for (int w = nb; w < s->n; ++w) sigma[w] = -1;
   }
   const std::vector<InstrH>& prog = *reblocked ? rprog : s->prog;
+  const auto tloop = std::chrono::steady_clock::now();
   auto emit_restore = [&]() {
     std::vector<std::pair<int, int>> rounds[2];
     restore_rounds(sigma, rounds);
@@ -3845,6 +3846,9 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     }
     s->iplan.push_back(std::move(ip));
   }
+  if (getenv("QK_DUMP_LOAD"))
+    fprintf(stderr, "load: pass planning %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tloop).count());
   if (merge_sqs && !lay_identity(sigma) && !emit_restore()) return fail(QK_ESIM, "internal: swap run merge failed");
   // lazy and relabel modes: the handle keeps the end layout (readbacks map
   // through it, writers and the next run restore it); QK_RELABEL_RESTORE
