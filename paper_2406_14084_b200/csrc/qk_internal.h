@@ -27,6 +27,8 @@ bool first_on_device(unsigned long long* mask);
 
 constexpr int kMaxC = 13;        // 2^13 complex128 = 128 KiB of shared memory per CTA
 constexpr int kMaxM = 4;         // register qubits per thread (16 amplitudes)
+constexpr int kMaxTM = 5;        // specialised passes only: 5 register qubits (32 amplitudes)
+constexpr int kMaxNA = 1 << kMaxTM;
 constexpr int kMaxOuter = 48;    // address bits outside the chunk
 constexpr int kSqsW = 5;         // SQS tile: runs of 2^5 amplitudes (512 B)
 
@@ -89,11 +91,11 @@ struct OpDesc {
   int32_t coef;       // offset into the coefficient pool (doubles)
   int64_t table;      // offset (complex entries) into the diagonal table pool
   uint16_t tcontrib[16];  // thread bit k -> table index contribution
-  uint16_t pr[16];        // register amplitude j -> table index contribution
+  uint16_t pr[kMaxNA];    // register amplitude j -> table index contribution
   int32_t nco;            // OP_DIAG over address bits outside the chunk (folded diagonal blocks):
   uint8_t co_k[8];        //   chunk-index bit co_k[i] -> table index contribution co_v[i]
   uint16_t co_v[8];
-  uint16_t unit;          // OP_DIAG: register amplitudes j whose entry is exactly 1 for every
+  uint32_t unit;          // OP_DIAG: register amplitudes j whose entry is exactly 1 for every
                           //   thread and chunk (e.g. CP with a register control at 0)
 };
 
@@ -102,9 +104,9 @@ struct PhaseDesc {
   int32_t tbits;          // C - M
   int32_t pad;
   uint8_t tpos[16];       // thread bit k -> chunk-local position
-  uint16_t rloc[16];      // register amplitude j -> chunk-local index
+  uint16_t rloc[kMaxNA];  // register amplitude j -> chunk-local index
   uint64_t taddr[16];     // thread bit k -> address offset (amplitudes)
-  uint64_t raddr[16];     // register amplitude j -> address offset (amplitudes)
+  uint64_t raddr[kMaxNA]; // register amplitude j -> address offset (amplitudes)
 };
 
 struct PassDesc {
@@ -157,20 +159,20 @@ struct TOp {
   int8_t code, r0, r1, creg;
   int16_t ctrl, coef;
   int32_t table;
-  int8_t st[4];
-  int16_t cf[4];
+  int8_t st[kMaxTM];
+  int16_t cf[kMaxTM];
   uint16_t tcontrib[12];
-  uint16_t pr[16];
+  uint16_t pr[kMaxNA];
   int8_t nco;             // OpDesc::nco / co_k / co_v (specialised kernels only)
   uint8_t co_k[8];
   uint16_t co_v[8];
-  uint16_t unit;          // OpDesc::unit (specialised kernels skip those multiplies)
+  uint32_t unit;          // OpDesc::unit (specialised kernels skip those multiplies)
 };
 
 struct TPhase {
   int16_t op_begin, op_end;
   uint8_t tpos[12];
-  uint16_t rloc[16];
+  uint16_t rloc[kMaxNA];
 };
 
 struct alignas(64) TmaParams {
@@ -193,7 +195,7 @@ struct alignas(64) TmaParams {
   uint8_t xpos[4];              // source address bits of the cluster rank (spectator qubits)
   uint8_t dpos[64];             // destination bit of every source address bit (permuted)
   uint64_t ldst_t[12];          // last phase: thread bit k -> destination offset
-  uint64_t ldst_r[16];          // last phase: register amplitude j -> destination offset
+  uint64_t ldst_r[kMaxNA];      // last phase: register amplitude j -> destination offset
   TPhase ph[kTMaxPh];
   TOp ops[kTMaxOps];
   double coef[kTMaxCoef];

@@ -381,7 +381,7 @@ std::vector<int> slice_plan(const TmaParams& tp, int st) {
       if (op.code != OP_DIAG) continue;
       uint32_t inner = 0;
       for (int k = 0; k < 12; ++k) inner |= op.tcontrib[k];
-      for (int j = 0; j < 16; ++j) inner |= op.pr[j];
+      for (int j = 0; j < (1 << tp.M); ++j) inner |= op.pr[j];
       int ents = 1;
       while ((uint32_t)ents <= inner) ents <<= 1;
       bool outer_top = true;
@@ -452,7 +452,8 @@ bool jit_pairs(const TmaParams& tp) {
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
                 std::vector<double>* coef, int variant, const std::vector<QuadOp>* quad) {
   const int C = tp.C, M = tp.M, T = C - M, NA = 1 << M;
-  if (M != 4 && M != 3) return false;
+  if (M != 4 && M != 3 && M != 5) return false;
+  if (M == 5 && (variant & 2)) return false;  // (the table-group pair factors index 4 slots)
   std::ostringstream b, pro;  // pro: consumer prologue (loop-invariant table values)
   toff->clear();
   coef->clear();
@@ -488,7 +489,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   // (none for 512-thread groups: 120 registers per thread leave no room)
   const int hoist = (variant & 1) ? 0
                                   : std::min<int>((int)toff->size(),
-                                                  hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 ? 0 : (M == 4 ? 1 : 2)));
+                                                  hz ? atoi(hz) : ((1 << (C - M)) * ng > 256 || M == 5 ? 0 : (M == 4 ? 1 : 2)));
   // hoist the first `hoist` tables that have no per-chunk (outer-bit) term
   // and load the first `early` per-chunk tables at the top of the chunk
   // iteration, so their L2 latency overlaps the stage wait and earlier phases
@@ -802,7 +803,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           // E(tid) prod_{active s in j} e_s(tid), times pj[j] where it is not 1
           int q = 0;
           while (qops[q] != o) ++q;
-          const uint32_t act = op.pr[0] & ((1u << M) - 1), pjm = op.pr[1];
+          const uint32_t act = op.pr[0] & ((1u << M) - 1), pjm = op.pr[1] | ((uint32_t)op.pr[3] << 16);
           b << "    { const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";
           if (op.pr[2] == 1) {  // constants per register amplitude
             for (int jj = 0; jj < NA; ++jj)
@@ -861,7 +862,7 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           int q = 0;
           while (qops[q] != o) ++q;
           const int qf = qfac[q];
-          int R[4];
+          int R[kMaxTM];
           for (int sl = 0; sl < M; ++sl) R[sl] = __builtin_ctz(D.rloc[1 << sl]);
           b << "    { const double2* fq = fac + ((u32)s * " << NQ << "u + " << qf << "u) * " << FS << "u;\n";
           b << "      const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";

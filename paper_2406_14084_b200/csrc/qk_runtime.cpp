@@ -497,6 +497,8 @@ struct Item {
   int run;
 };
 
+bool m5_enabled() { return getenv("QK_M5") && jit_available(); }
+
 // Compile the gates of one pass over chunk address bits Q (ascending) of a
 // vector of `nbits` address bits.
 int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const std::vector<int>& Q,
@@ -543,6 +545,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
   const int C = (int)Q.size();
   int M = std::min(kMaxM, C);
   if (C >= 9 && C <= 12 && Q.back() == C - 1 && getenv("QK_M")) M = std::max(3, std::min(4, atoi(getenv("QK_M"))));
+  // five register qubits (32 amplitudes per thread, two 128-thread groups per
+  // CTA): fewer phases for wide passes; specialised kernels only
+  if (allow_quad && C == 12 && m5_enabled()) M = 5;
   int loc[64];
   for (int& x : loc) x = -1;
   for (int l = 0; l < C; ++l) loc[Q[l]] = l;
@@ -762,19 +767,37 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
           b.push_back(best);
         }
         cands.push_back(b);
+        // (c) the store-lane positions with pending work first, so the last
+        // phase can keep them as lanes (no layout-only phase at the end)
+        std::vector<int> c3 = base;
+        for (int q = 0; q < C && (int)c3.size() < M; ++q)
+          if (lane_pos[q] && freq[q] > 0 && !in_r(c3, q)) c3.push_back(q);
+        while ((int)c3.size() < M) {
+          int best = -1;
+          for (int q = 0; q < C; ++q)
+            if (!in_r(c3, q) && freq[q] > 0 && (best < 0 || freq[q] > freq[best])) best = q;
+          if (best < 0) break;
+          c3.push_back(best);
+        }
+        cands.push_back(c3);
       } else {
         cands.push_back({});
       }
-      int best_c = -1, best_n = -1;
+      // ties go to the set with more store-lane positions: their gates run
+      // early and the last phase can keep them as lanes
+      int best_c = -1, best_n = -1, best_l = -1;
       for (size_t c = 0; c < cands.size(); ++c) {
         auto& R = cands[c];
         for (int q : fill_order)
           if ((int)R.size() < M && !in_r(R, q)) R.push_back(q);
         std::vector<char> dn = done;
         const int k = runs_with(R, dn, nullptr);
-        if (k > best_n) {
+        int nl = 0;
+        for (int q : R) nl += lane_pos[q];
+        if (k > best_n || (k == best_n && nl > best_l)) {
           best_n = k;
           best_c = (int)c;
+          best_l = nl;
         }
       }
       PhaseB pb;
@@ -817,6 +840,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
       if (lane_pos[q]) return 1;
     return 0;
   };
+  if (getenv("QK_DUMP_SCHED"))
+    fprintf(stderr, "phase builders: program order %zu+%d, list scheduler %zu+%d\n", phs.size(), extra(phs),
+            sched.size(), extra(sched));
   if (!sched.empty() && sched.size() + extra(sched) < phs.size() + extra(phs)) phs.swap(sched);
   // (dev, timing only: drops the phases beyond QK_EXP_MAXPH and their gates)
   if (const char* mx = getenv("QK_EXP_MAXPH"))
@@ -1116,7 +1142,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
   // term of slot s + pairs with its set thread bits)); pj as for OP_QUAD.
   // masks: slots whose e_s differs from 1 for some thread, j whose pj != 1.
   auto build_qlite = [&](int r, const std::vector<int>& Tth, const std::vector<int>& R, int64_t* out,
-                         uint16_t* slot_mask, uint16_t* pj_mask, uint16_t* flags) -> int {
+                         uint16_t* slot_mask, uint32_t* pj_mask, uint16_t* flags) -> int {
     const int TT = (int)Tth.size();
     std::vector<double> lin(C, 0.0), pr((size_t)C * C, 0.0);
     double ph0 = 0.0;
@@ -1183,7 +1209,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
           for (int sb = sa + 1; sb < M; ++sb)
             if (j >> sb & 1) ap += P2(R[sa], R[sb]);
       ap = wrap_angle(ap);
-      if (ap != 0.0) *pj_mask |= (uint16_t)(1u << j);
+      if (ap != 0.0) *pj_mask |= 1u << j;
       const cplx v = cexpi(ap);
       d[L.pj + 2 * j] = v.real();
       d[L.pj + 2 * j + 1] = v.imag();
@@ -1210,7 +1236,7 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
         f *= cplx(d[L.pj + 2 * j], d[L.pj + 2 * j + 1]);
         d[L.pj + 2 * j] = f.real();
         d[L.pj + 2 * j + 1] = f.imag();
-        if (f != cplx(1.0, 0.0)) *pj_mask |= (uint16_t)(1u << j);
+        if (f != cplx(1.0, 0.0)) *pj_mask |= 1u << j;
       }
     } else if (e_one) {
       *flags = 2;
@@ -1285,13 +1311,15 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
                  !getenv("QK_NO_QLITE")) {
         std::vector<int> Tth(T.begin(), T.end());
         int64_t off = 0;
-        uint16_t sm = 0, pm = 0, fl = 0;
+        uint16_t sm = 0, fl = 0;
+        uint32_t pm = 0;
         int rc = build_qlite(it.run, Tth, pb.R, &off, &sm, &pm, &fl);
         if (rc) return rc;
         op.code = OP_QLITE;
         op.table = off;
         op.pr[0] = sm;
-        op.pr[1] = pm;
+        op.pr[1] = (uint16_t)(pm & 0xffffu);
+        op.pr[3] = (uint16_t)(pm >> 16);  // (32 register amplitudes)
         op.pr[2] = fl;
       } else if (it.type == 1) {
         if (allow_quad && run_quad[it.run]) tile_table_used = true;
@@ -1823,7 +1851,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
               const std::vector<int>* xspec = nullptr, const std::vector<int>* tile = nullptr) {
   if (getenv("QK_NO_TMA")) return false;
   const bool lz = tile && !tile->empty();
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > ((lz || getenv("QK_TMA13")) ? 13 : 12) || pd.nphases > kTMaxPh ||
+  if (pd.M < 3 || pd.M > kMaxTM || pd.C < 9 || pd.C > ((lz || getenv("QK_TMA13")) ? 13 : 12) || pd.nphases > kTMaxPh ||
       s->nbits > 34)
     return false;
   if (pd.nouter != s->nbits - pd.C) return false;
@@ -1911,7 +1939,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
     const PhaseDesc& D = hp.phases[pd.phase0 + ph];
     TPhase& T = tp.ph[ph];
     for (int k = 0; k < 12; ++k) T.tpos[k] = D.tpos[k];
-    for (int j = 0; j < 16; ++j) T.rloc[j] = D.rloc[j];
+    for (int j = 0; j < kMaxNA; ++j) T.rloc[j] = D.rloc[j];
     T.op_begin = (int16_t)nsteps;
     TOp* cur1q = nullptr;  // open STEP_1Q (one-qubit gates on distinct slots commute)
     for (int o = D.op_begin; o < D.op_end; ++o) {
@@ -1936,7 +1964,7 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
           if (op.table > INT32_MAX) return false;
           t.table = (int32_t)op.table;
           for (int k = 0; k < 12; ++k) t.tcontrib[k] = op.tcontrib[k];
-          for (int j = 0; j < 16; ++j) t.pr[j] = op.pr[j];
+          for (int j = 0; j < kMaxNA; ++j) t.pr[j] = op.pr[j];
           t.nco = (int8_t)op.nco;
           t.unit = op.unit;
           for (int k = 0; k < op.nco; ++k) {
@@ -2528,7 +2556,7 @@ bool tma_plan_ok(const HostPlan& hp, int pass, int nbits, int cmax = 12) {
   if (getenv("QK_NO_TMA")) return false;
   const PassDesc& pd = hp.passes[pass];
   if (getenv("QK_TMA13")) cmax = 13;
-  if (pd.M < 3 || pd.M > 4 || pd.C < 9 || pd.C > cmax || pd.nphases > kTMaxPh || nbits > 34) return false;
+  if (pd.M < 3 || pd.M > kMaxTM || pd.C < 9 || pd.C > cmax || pd.nphases > kTMaxPh || nbits > 34) return false;
   if (pd.nouter != nbits - pd.C) return false;
   const int ob = hp.phases[pd.phase0].op_begin, oe = hp.phases[pd.phase0 + pd.nphases - 1].op_end;
   int ncoef = 0;

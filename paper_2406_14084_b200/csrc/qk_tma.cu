@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_block_tma(const __grid_constant
 }  // namespace
 
 static int consumers_for(int C, int M) {
+  if (M == 5) return 2 << (C - 5);  // two groups (specialised kernels only)
   if (M == 4 && C == 12 && getenv("QK_NG2")) return 512;
   if (M == 4 && C <= 11 && getenv("QK_CONS")) return atoi(getenv("QK_CONS"));
   return M == 4 ? kConsumers4 : kConsumers3;
@@ -337,7 +338,7 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax) {
   // Stages are taken in chunk order by whichever group owns the chunk, so a
   // stage's barrier never runs more than one phase ahead of its waiter even
   // when S is not a multiple of NG (QK_NG2: 2 groups of 256 on 3 stages)
-  if (!(NG == 2 && C == 12 && getenv("QK_NG2") && !getenv("QK_NG2_EVEN"))) S = (S / NG) * NG;
+  if (!(NG == 2 && C == 12 && (getenv("QK_NG2") || M == 5) && !getenv("QK_NG2_EVEN"))) S = (S / NG) * NG;
   if (S > 4 * NG) S = 4 * NG;
   if (const char* e = getenv("QK_SMAX")) smax = atoi(e);
   if (smax > 0) S = std::max(std::min(S, smax), NG);
@@ -354,6 +355,7 @@ int launch_block_tma(const TmaParams* p, int num_sms, CUstream_st* stream) {
     cudaFuncSetAttribute(k_block_tma<3, 32 + kConsumers3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_block_tma<4, 32 + 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   }
+  if (p->M > 4) return -1;  // five register qubits: specialised kernels only
   int ng = 0, st = 0;
   const int smem = tma_smem_bytes(p->C, p->M, &ng, &st, p->smax);
   if (smem < 0) return -1;
