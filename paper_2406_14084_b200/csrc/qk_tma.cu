@@ -338,7 +338,10 @@ int tma_smem_bytes(int C, int M, int* ng, int* stages, int smax) {
   // Stages are taken in chunk order by whichever group owns the chunk, so a
   // stage's barrier never runs more than one phase ahead of its waiter even
   // when S is not a multiple of NG (QK_NG2: 2 groups of 256 on 3 stages)
-  if (!(NG == 2 && C == 12 && (getenv("QK_NG2") || M == 5) && !getenv("QK_NG2_EVEN"))) S = (S / NG) * NG;
+  // (with more stages than groups a group may wait for round r of a stage whose
+  // round r - 1 has not completed yet, and the parity wait passes at once: M = 5
+  // keeps one stage per group)
+  if (!(NG == 2 && C == 12 && getenv("QK_NG2") && !getenv("QK_NG2_EVEN"))) S = (S / NG) * NG;
   if (S > 4 * NG) S = 4 * NG;
   if (const char* e = getenv("QK_SMAX")) smax = atoi(e);
   if (smax > 0) S = std::max(std::min(S, smax), NG);
