@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>  // environ
 #include <string>
 #include <mutex>
 #include <unordered_map>
@@ -3011,6 +3012,35 @@ bool reblock_memo(const std::vector<InstrH>& prog, int nb, int cap, int rowbits,
   return ok;
 }
 
+// Whole-plan memo (host side only: the device tables, tensor maps and
+// kernels are still built by upload_plan for every load). Key: the packed
+// program, the handle's shape and every QK_* switch of the environment.
+struct PlanMemo {
+  HostPlan hp;
+  std::vector<InstrPlan> iplan;
+  std::vector<int> plan_lay0, lay_final;
+  bool oop_sqs = false, reblocked = false;
+};
+std::mutex g_plan_mu;
+std::map<std::string, PlanMemo> g_plan_memo;
+
+std::string plan_key(const qk_sim* s, bool try_reblock) {
+  std::vector<int32_t> w;
+  std::vector<double> pr;
+  pack_prog(s->prog, &w, &pr);
+  std::string key(reinterpret_cast<const char*>(w.data()), w.size() * 4);
+  key.append(reinterpret_cast<const char*>(pr.data()), pr.size() * 8);
+  const int shape[12] = {s->n, s->r, s->b, s->L, s->nbits, s->count, s->rank_lo, (int)s->gbg, s->bufs[1] != nullptr,
+                         (int)try_reblock, (int)jit_available(), (int)s->dry};
+  key.append(reinterpret_cast<const char*>(shape), sizeof shape);
+  std::vector<std::string> env;
+  for (char** e = environ; e && *e; ++e)
+    if (!strncmp(*e, "QK_", 3)) env.push_back(*e);
+  std::sort(env.begin(), env.end());
+  for (auto& e : env) key += "|" + e;
+  return key;
+}
+
 int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
   const auto tc0 = std::chrono::steady_clock::now();
   struct PlanTimer {
@@ -3023,6 +3053,29 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
   } plan_timer{tc0};
   s->hp.clear();
   s->iplan.clear();
+  const bool memo_on = !getenv("QK_NO_PLAN_MEMO");
+  const std::string pkey = memo_on ? plan_key(s, try_reblock) : std::string();
+  if (memo_on) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_plan_memo.find(pkey);
+    if (it != g_plan_memo.end()) {
+      s->hp = it->second.hp;
+      s->iplan = it->second.iplan;
+      s->plan_lay0 = it->second.plan_lay0;
+      s->lay_final = it->second.lay_final;
+      s->oop_sqs = it->second.oop_sqs;
+      *reblocked = it->second.reblocked;
+    }
+  }
+  if (!s->iplan.empty() || !s->hp.passes.empty()) {
+    replay_perm(s);
+    const auto tq0 = std::chrono::steady_clock::now();
+    const int urc = upload_plan(s);
+    if (getenv("QK_DUMP_LOAD"))
+      fprintf(stderr, "load: plan memo hit, upload_plan %.3f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
+    return urc;
+  }
   std::string emsg;
   const int nb = s->nbits;
   // Relabeling mode (needs the second buffer): every block runs with the same
@@ -3934,6 +3987,11 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
       ns += ip.type == QK_INS_SQS;
     }
     fprintf(stderr, "relabel=%d Cg=%d fused SQS %d of %d\n", (int)relabel, Cg, nf, ns);
+  }
+  if (memo_on) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    if (g_plan_memo.size() > 32) g_plan_memo.clear();
+    g_plan_memo[pkey] = PlanMemo{s->hp, s->iplan, s->plan_lay0, s->lay_final, s->oop_sqs, *reblocked};
   }
   const auto tq0 = std::chrono::steady_clock::now();
   const int urc = upload_plan(s);
