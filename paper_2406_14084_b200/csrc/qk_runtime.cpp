@@ -16,6 +16,7 @@
 #include <complex>
 #include <deque>
 #include <map>
+#include <memory>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -2050,6 +2051,57 @@ std::vector<QuadOp> quad_ops(const HostPlan& hp, const TmaParams& tp) {
 // (or a program sharing pass structures) reuses the generated source instead
 // of rebuilding ~100 KB of text per pass (3.8 ms for QAOA30's 24 passes).
 // Key: the TmaParams bytes without the tensor map and device pointers.
+// environment switches the generator (and tma_smem_bytes / jit_pairs) reads
+const char* const kGenEnv[] = {"QK_JIT_PREFETCH", "QK_JIT_HOIST", "QK_JIT_EARLY", "QK_JIT_SW128", "QK_NO_CORDER",
+                               "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS",
+                               "QK_EXP_SKIP", "QK_JIT_MAXNREG", "QK_NO_TSTORE", "QK_PAIR", "QK_QHOIST"};
+
+// A pass structure's built kernel variants (process-wide): key = its TMA
+// parameters without pointers and tensor map, its OP_QUAD data, the switches
+std::string tma_key(const TmaParams& tp) {
+  TmaParams k = tp;
+  memset(&k.map, 0, sizeof k.map);
+  k.tabs = nullptr;
+  k.state = nullptr;
+  k.out = nullptr;
+  return std::string(reinterpret_cast<const char*>(&k), sizeof k);
+}
+struct PassJit {
+  int variant;
+  void* kern;
+  std::vector<long long> toff;
+  std::vector<double> coef;
+};
+struct PassJitMemo {
+  std::string tkey;  // tuning key (hash of the structure's first source)
+  std::vector<PassJit> vars;
+};
+std::mutex g_pj_mu;
+std::unordered_map<std::string, std::unique_ptr<PassJitMemo>> g_pass_jit;
+std::string pass_jit_key(const TmaParams& tp, const std::vector<QuadOp>& quad, const char* venv) {
+  std::string key = tma_key(tp);
+  for (const QuadOp& q : quad) key.append(reinterpret_cast<const char*>(&q), sizeof q);
+  for (const char* e : kGenEnv) {
+    const char* v = getenv(e);
+    key.push_back('|');
+    if (v) key.append(v);
+  }
+  key += venv ? std::string("|v") + venv : std::string("|all");
+  return key;
+}
+const PassJitMemo* pass_jit_find(const std::string& key) {
+  if (getenv("QK_JIT_NOCACHE")) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pj_mu);
+  auto it = g_pass_jit.find(key);
+  return it == g_pass_jit.end() ? nullptr : it->second.get();
+}
+const PassJitMemo* pass_jit_store(const std::string& key, PassJitMemo&& m) {
+  std::lock_guard<std::mutex> lk(g_pj_mu);
+  auto& slot = g_pass_jit[key];
+  if (!slot) slot.reset(new PassJitMemo(std::move(m)));  // entries live for the process (kernels do too)
+  return slot.get();
+}
+
 bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long long>* toff,
                        std::vector<double>* coef, int variant = 0, const std::vector<QuadOp>* quad = nullptr) {
   struct Val {
@@ -2060,19 +2112,11 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
   };
   static std::mutex mu;
   static std::unordered_map<std::string, Val> cache;
-  TmaParams k = tp;
-  memset(&k.map, 0, sizeof k.map);
-  k.tabs = nullptr;
-  k.state = nullptr;
-  k.out = nullptr;
-  std::string key(reinterpret_cast<const char*>(&k), sizeof k);
+  std::string key = tma_key(tp);
   key.push_back((char)variant);
   if (quad && (variant & 2))
     for (const QuadOp& q : *quad) key.append(reinterpret_cast<const char*>(&q), sizeof q);
-  // environment switches the generator (and tma_smem_bytes) reads
-  for (const char* e : {"QK_JIT_PREFETCH", "QK_JIT_HOIST", "QK_JIT_EARLY", "QK_JIT_SW128", "QK_NO_CORDER",
-                        "QK_NO_SLICES", "QK_SLICE_RUN", "QK_X_FENCE", "QK_SMAX", "QK_NG2", "QK_CONS",
-                        "QK_EXP_SKIP", "QK_JIT_MAXNREG"}) {
+  for (const char* e : kGenEnv) {
     const char* v = getenv(e);
     key.push_back('|');
     if (v) key.append(v);
@@ -2289,23 +2333,28 @@ int upload_plan(qk_sim* s) {
   }
   if (jit_available() && s->nbits >= jit_min) {
     const auto tj0 = std::chrono::steady_clock::now();
-    std::vector<std::string> srcs;
-    std::vector<int> src_pass, src_var;
-    std::vector<std::vector<long long>> toffs;
-    std::vector<std::vector<double>> coefs;
     // Up to sixteen variants per pass (bit 1: no hoisted table, bit 2: quadratic
     // table groups, bit 4: OP_QUAD factors computed after the stage wait
     // instead of ahead in a pending slot, bit 8: TMA-store epilogue for lazy
-    // passes); identical sources are built once. QK_JIT_VARIANT=v pins
-    // one, otherwise the first runs time every variant and keep the fastest
-    // per pass structure (process-wide, tune_pick / tune_record).
+    // passes); identical sources are built once. QK_JIT_VARIANT=v pins one,
+    // otherwise the first runs time every variant and keep the fastest per
+    // pass structure (process-wide, tune_pick / tune_record). A pass structure
+    // seen before (same parameters, same switches) reuses its kernels.
     const char* venv = getenv("QK_JIT_VARIANT");
     s->tuning.assign(hp.passes.size(), -1);
     s->pass_var.assign(hp.passes.size(), {});
     s->pass_key.assign(hp.passes.size(), std::string());
+    std::vector<std::string> pkeys(hp.passes.size());
+    std::vector<const PassJitMemo*> hits(hp.passes.size(), nullptr);
+    std::vector<std::string> srcs;
+    std::vector<int> src_pass, src_var;
+    std::vector<std::vector<long long>> toffs;
+    std::vector<std::vector<double>> coefs;
     for (size_t p = 0; p < hp.passes.size(); ++p) {
       if (s->pass_tma[p] < 0) continue;
       std::vector<QuadOp> quad = quad_ops(hp, s->tma[s->pass_tma[p]]);
+      pkeys[p] = pass_jit_key(s->tma[s->pass_tma[p]], quad, venv);
+      if ((hits[p] = pass_jit_find(pkeys[p]))) continue;
       std::vector<std::string> seen;
       for (int variant = 0; variant < 16; ++variant) {
         if (venv && variant != atoi(venv)) continue;
@@ -2315,7 +2364,6 @@ int upload_plan(qk_sim* s) {
         if (!jit_source_cached(s->tma[s->pass_tma[p]], &src, &toff, &coef, variant, &quad)) continue;
         if (std::find(seen.begin(), seen.end(), src) != seen.end()) continue;
         seen.push_back(src);
-        if (s->pass_key[p].empty()) s->pass_key[p] = src;  // tuning key: the structure's first source
         if (const char* dd = getenv("QK_JIT_DUMP")) {
           const std::string path = std::string(dd) + "/pass" + std::to_string(p) + "_v" + std::to_string(variant) + ".cu";
           if (FILE* f = fopen(path.c_str(), "w")) {
@@ -2337,25 +2385,36 @@ int upload_plan(qk_sim* s) {
       fprintf(stderr, "load: jit_source %.3f ms (%zu kernels), jit_build %.3f ms\n",
               std::chrono::duration<double, std::milli>(tj1 - tj0).count(), srcs.size(),
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tj1).count());
-    for (size_t i = 0; i < srcs.size(); ++i) {
-      if (!handles[i]) continue;
-      const int p = src_pass[i];
-      // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | split | toff[ntab+1] |
-      // coef[ncoef+1] | smap[16 words] (64-B aligned: the last 16 words of the blob)
-      const size_t smap_off = (16 + 6 + toffs[i].size() + 1 + coefs[i].size() + 1 + 7) & ~(size_t)7;
-      std::vector<uint64_t> blob(smap_off + 16, 0);
-      blob[16] = (uint64_t)(uintptr_t)s->d_pool;
+    {  // new pass structures: their built variants (the tuning key: the first source's hash)
+      std::map<int, PassJitMemo> fresh;
+      for (size_t i = 0; i < srcs.size(); ++i) {
+        PassJitMemo& m = fresh[src_pass[i]];
+        if (m.tkey.empty()) m.tkey = std::to_string(std::hash<std::string>{}(srcs[i])) + "_" + std::to_string(srcs[i].size());
+        if (handles[i]) m.vars.push_back({src_var[i], handles[i], toffs[i], coefs[i]});
+      }
+      for (auto& kv : fresh) hits[kv.first] = pass_jit_store(pkeys[kv.first], std::move(kv.second));
+    }
+    for (size_t p = 0; p < hp.passes.size(); ++p) {
+      if (!hits[p]) continue;
+      s->pass_key[p] = hits[p]->tkey;
       const TmaParams& tq = s->tma[s->pass_tma[p]];
-      blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
-      blob[20] = (uint64_t)(uintptr_t)s->d_nrm;
-      blob[21] = 0;                                                 // split word (launch_pass_part)
-      for (size_t k = 0; k < toffs[i].size(); ++k) blob[22 + k] = (uint64_t)toffs[i][k];
-      const size_t co = 22 + toffs[i].size() + 1;
-      for (size_t k = 0; k < coefs[i].size(); ++k) memcpy(&blob[co + k], &coefs[i][k], 8);
-      s->pass_var[p].push_back({src_var[i], handles[i], std::move(blob)});
-      if (!s->pass_jit[p]) {
-        s->pass_jit[p] = handles[i];
-        s->jit_blob[p] = s->pass_var[p].back().blob;
+      for (const PassJit& v : hits[p]->vars) {
+        // QkJitParams: map[16 words] | tabs | state | out | nchunks | nrm | split | toff[ntab+1] |
+        // coef[ncoef+1] | smap[16 words] (64-B aligned: the last 16 words of the blob)
+        const size_t smap_off = (16 + 6 + v.toff.size() + 1 + v.coef.size() + 1 + 7) & ~(size_t)7;
+        std::vector<uint64_t> blob(smap_off + 16, 0);
+        blob[16] = (uint64_t)(uintptr_t)s->d_pool;
+        blob[19] = tq.xbits ? tq.nchunks >> tq.xbits : tq.nchunks;  // cluster mode: supertiles
+        blob[20] = (uint64_t)(uintptr_t)s->d_nrm;
+        blob[21] = 0;                                                 // split word (launch_pass_part)
+        for (size_t k = 0; k < v.toff.size(); ++k) blob[22 + k] = (uint64_t)v.toff[k];
+        const size_t co = 22 + v.toff.size() + 1;
+        for (size_t k = 0; k < v.coef.size(); ++k) memcpy(&blob[co + k], &v.coef[k], 8);
+        s->pass_var[p].push_back({v.variant, v.kern, std::move(blob)});
+        if (!s->pass_jit[p]) {
+          s->pass_jit[p] = v.kern;
+          s->jit_blob[p] = s->pass_var[p].back().blob;
+        }
       }
     }
     for (size_t p = 0; p < hp.passes.size(); ++p) tune_pick(s, (int)p, false);
