@@ -263,6 +263,41 @@ def test_random_streams_vs_oracle(gpu, engine, seed):
     assert err <= TOL, (seed, n, r, c, err)
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_random_streams_in_the_scheduled_range_vs_oracle(gpu, seed):
+    """Random instruction streams at 17-21 qubits with chunks of 8-12 (QK_JIT=0:
+    the lazy layout and the cross-block schedule apply from 16 address bits),
+    half of them without D<k> gates so the schedule, the quadratic phases, the
+    zero-support reads and chunk skipping and the first-use placement all run;
+    R = 0..2 rank partitions in one handle. Against the oracle."""
+    import os
+    rng = np.random.default_rng(9100 + seed)
+    n = int(rng.integers(17, 22))
+    r = int(rng.integers(0, 3))
+    L = n - r
+    c = int(rng.integers(8, 13))
+    layout = LayoutParams(n=n, c=L, r=r, cl=2, b=L)
+    global KINDS
+    kinds0 = KINDS
+    if seed % 2 == 0:
+        KINDS = [k for k in KINDS if k != "D"]
+    try:
+        ins = _random_stream(rng, n, r, c, int(rng.integers(4, 14)))
+    finally:
+        KINDS = kinds0
+    text = serialize_optimized(OptimizedCircuit(n, layout, ins))
+    os.environ["QK_JIT"] = "0"
+    try:
+        res = simulate(OptimizedCircuit(n, layout, ins), SimConfig(layout))
+        got = res.physical_vector()
+    finally:
+        os.environ.pop("QK_JIT", None)
+    want, perm, _ = orc.simulate_text(text, n, L, r=r, b=L)
+    assert tuple(res.final_permutation) == perm
+    err = float(np.max(np.abs(got - want)))
+    assert err <= TOL, (seed, n, r, c, err)
+
+
 def test_chunk_widths_up_to_13(gpu, engine):
     rng = np.random.default_rng(77)
     for c in (10, 11, 12, 13):
