@@ -73,14 +73,24 @@ def parse_stem(stem: str):
     return fam, int(head[len(fam):]), int(c[1:]), int(r[1:])
 
 
-def analytic_factors(fam: str, n: int):
+def analytic_factors(fam: str, n: int, text: str | None = None):
     """Product-state answer of the families that have one (test_oracle.py:32-42):
-    QFT|0> and H layers uniform, BV |0..0>. None otherwise."""
+    QFT|0> and H layers uniform, BV |0..0>, an RZZ layer |0..0> up to a phase
+    (the fidelity ignores it), a U layer the product of each qubit's U|0>
+    (gate id q acts on logical qubit q, gen_gate_layer). None otherwise."""
     f = np.zeros((n, 2), dtype=np.complex128)
     if fam in ("qft", "h"):
         f[:] = 2 ** -0.5
-    elif fam == "bv":
+    elif fam in ("bv", "rzz"):
         f[:, 0] = 1.0
+    elif fam == "u" and text is not None:
+        from paper_2406_14084_b200 import Gate, GateKind, LayoutParams, gate_matrix, parse_optimized
+        opt = parse_optimized(text, LayoutParams(n=n, c=n))
+        us = [g for ins in opt.instructions for g in getattr(ins, "gates", ()) if g.kind == GateKind.U]
+        if len(us) != n:
+            return None
+        for g in us:
+            f[g.gid] = gate_matrix(Gate(GateKind.U, (0,), 0, g.params))[:, 0]
     else:
         return None
     return f
@@ -395,7 +405,7 @@ def run_single(args):
         except (OSError, ValueError):
             traffic = None
     parity = golden_check(h, name)
-    f = analytic_factors(fam, n)
+    f = analytic_factors(fam, n, text)
     if f is not None and fam != "qaoa":
         fid = res.fidelity_product(f)
         parity = dict(parity or {}, fidelity=fid, fidelity_vs="analytic product state")
@@ -494,7 +504,7 @@ def run_multi(args, world, rank, local):
     achieved_block = bb / (block_ms * 1e-3) / 1e9 if block_ms else 0.0
     xrs_gbs = xb / (xrs_ms * 1e-3) / 1e9 if xrs_ms else 0.0
     # analytic parity after the timed region (device-side fidelity over all shards)
-    f = analytic_factors(fam, n)
+    f = analytic_factors(fam, n, text)
     fid = sim.fidelity_product(perm, f) if f is not None else None
     nrm = sim.norm()
     # e2e through the public API
