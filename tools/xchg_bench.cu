@@ -18,13 +18,16 @@ __global__ void __launch_bounds__(256, 1) k_smem(double2* out, int rounds) {
   for (int r = 0; r < rounds; ++r) {
     // write: thread bits 0..7 -> positions 0..7, registers -> 8..11 (XOR-swizzled)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sm[(t | (j << 8)) ^ ((j & 7) << 0)] = v[j];
+    for (int j = 0; j < 16; ++j) {
+      const unsigned i = t | (j << 8);
+      sm[i ^ ((i >> 4) & 7)] = v[j];  // conflict-free for both access patterns
+    }
     __syncthreads();
     // read: registers -> positions 0..3, thread bits -> 4..11
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const unsigned i = (j | (t << 4));
-      v[j] = sm[i ^ ((i >> 8) & 7)];
+      v[j] = sm[i ^ ((i >> 4) & 7)];
       v[j].x += 1e-9;
     }
     __syncthreads();
