@@ -278,6 +278,11 @@ struct QuadOp {
   bool ok = false;
   double pf[16][2] = {};   // pair (s, s') at index s * 4 + s' (s < s'), complex
   double inv2 = 1.0;       // 1 / |table scale|^2 (f_s / f_0 = f_s conj(f_0) inv2)
+  // OP_QUAD / OP_QLITE: the 2^M register-amplitude constants pj of the op's
+  // data (uniform over threads and chunks), so the kernel takes them as
+  // parameters instead of loading them per chunk (0 entries: not known)
+  int npj = 0;
+  double pj[kMaxNA][2] = {};
 };
 // variant bits: 1 = no hoisted table, 2 = quadratic table groups
 bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* toff, std::vector<double>* coef,

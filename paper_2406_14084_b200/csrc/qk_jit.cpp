@@ -805,9 +805,19 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           while (qops[q] != o) ++q;
           const uint32_t act = op.pr[0] & ((1u << M) - 1), pjm = op.pr[1] | ((uint32_t)op.pr[3] << 16);
           b << "    { const double2* qd = p.tabs + p.toff[" << QT + q << "];\n";
+          // the pj constants: kernel parameters when the planner passed them
+          // (uniform over threads and chunks), else loads from the op's data
+          const QuadOp* qk = (quad && o < (int)quad->size() && (*quad)[o].npj == NA) ? &(*quad)[o] : nullptr;
+          auto pjv = [&](int jj) -> std::string {
+            if (!qk) return "__ldg(qd + " + std::to_string(QL0.pj / 2 + jj) + ")";
+            const int ci = (int)coef->size();
+            coef->push_back(qk->pj[jj][0]);
+            coef->push_back(qk->pj[jj][1]);
+            return "make_double2(p.coef[" + std::to_string(ci) + "], p.coef[" + std::to_string(ci + 1) + "])";
+          };
           if (op.pr[2] == 1) {  // constants per register amplitude
             for (int jj = 0; jj < NA; ++jj)
-              if (pjm >> jj & 1) b << "      v[" << jj << "] = cm(v[" << jj << "], __ldg(qd + " << QL0.pj / 2 + jj << "));\n";
+              if (pjm >> jj & 1) b << "      v[" << jj << "] = cm(v[" << jj << "], " << pjv(jj) << ");\n";
             b << "    }\n";
             break;
           }
@@ -834,9 +844,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
               // every amplitude whose active bits are j (the inactive slots vary freely)
               for (int jj = 0; jj < NA; ++jj) {
                 if ((uint32_t)(jj & (int)act) != (uint32_t)j) continue;
-                const std::string pjv = "__ldg(qd + " + std::to_string(QL0.pj / 2 + jj) + ")";
                 std::string m;
-                if (pjm >> jj & 1) m = f.empty() ? pjv : "cm(" + f + ", " + pjv + ")";
+                if (pjm >> jj & 1) {
+                  const std::string pv = pjv(jj);
+                  m = f.empty() ? pv : "cm(" + f + ", " + pv + ")";
+                }
                 else m = f;
                 if (!m.empty()) b << "      v[" << jj << "] = cm(v[" << jj << "], " << m << ");\n";
               }
@@ -878,9 +890,19 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
             else b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], __ldg(qt + " << 1 + sl << "));\n";
           }
           // depth-first over the slots: a stack of M + 1 partial products
+          const QuadOp* qk = (quad && o < (int)quad->size() && (*quad)[o].npj == NA) ? &(*quad)[o] : nullptr;
           std::function<void(int, int, const std::string&)> visit = [&](int j, int bit, const std::string& f) {
             if (bit < 0) {
-              if (__builtin_popcount((unsigned)j) >= 2)
+              if (__builtin_popcount((unsigned)j) >= 2 && qk) {
+                const int ci = (int)coef->size();
+                coef->push_back(qk->pj[j][0]);
+                coef->push_back(qk->pj[j][1]);
+                if (qk->pj[j][0] == 1.0 && qk->pj[j][1] == 0.0)
+                  b << "      v[" << j << "] = cm(v[" << j << "], " << f << ");\n";
+                else
+                  b << "      v[" << j << "] = cm(v[" << j << "], cm(" << f << ", make_double2(p.coef[" << ci << "], p.coef["
+                    << ci + 1 << "])));\n";
+              } else if (__builtin_popcount((unsigned)j) >= 2)
                 b << "      v[" << j << "] = cm(v[" << j << "], cm(" << f << ", __ldg(qd + " << QL.pj / 2 + j << ")));\n";
               else
                 b << "      v[" << j << "] = cm(v[" << j << "], " << f << ");\n";

@@ -2005,9 +2005,27 @@ std::vector<QuadOp> quad_ops(const HostPlan& hp, const TmaParams& tp) {
   std::vector<QuadOp> out(kTMaxOps);
   std::unordered_map<int64_t, int> by_out;
   for (size_t t = 0; t < hp.tables.size(); ++t) by_out[hp.tables[t].out] = (int)t;
+  std::unordered_map<int64_t, const std::vector<double>*> qdata;
+  for (auto& qc : hp.qcopy) qdata[qc.first] = &qc.second;
   for (int ph = 0; ph < tp.nphases; ++ph)
     for (int o = tp.ph[ph].op_begin; o < tp.ph[ph].op_end; ++o) {
       const TOp& op = tp.ops[o];
+      if ((op.code == OP_QUAD || op.code == OP_QLITE) && !getenv("QK_NO_PJ_CONST")) {
+        auto it = qdata.find(op.table);
+        if (it == qdata.end()) continue;
+        const int NO = op.code == OP_QUAD ? tp.nbits - tp.C : 0;
+        const QuadLayout L = quad_layout(tp.C, tp.M, NO);
+        const std::vector<double>& d = *it->second;
+        if ((size_t)(L.pj + 2 * (1 << tp.M)) > d.size()) continue;
+        QuadOp q;
+        q.npj = 1 << tp.M;
+        for (int j = 0; j < q.npj; ++j) {
+          q.pj[j][0] = d[L.pj + 2 * j];
+          q.pj[j][1] = d[L.pj + 2 * j + 1];
+        }
+        out[o] = q;
+        continue;
+      }
       if (op.code != OP_DIAG) continue;
       auto it = by_out.find(op.table);
       if (it == by_out.end()) continue;
@@ -2114,7 +2132,9 @@ bool jit_source_cached(const TmaParams& tp, std::string* src, std::vector<long l
   static std::unordered_map<std::string, Val> cache;
   std::string key = tma_key(tp);
   key.push_back((char)variant);
-  if (quad && (variant & 2))
+  // (the quadratic ops' data: pair factors for variant bit 2, and the pj
+  // constants every variant passes as parameters)
+  if (quad)
     for (const QuadOp& q : *quad) key.append(reinterpret_cast<const char*>(&q), sizeof q);
   for (const char* e : kGenEnv) {
     const char* v = getenv(e);

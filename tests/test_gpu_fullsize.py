@@ -238,3 +238,32 @@ def test_run_from_a_written_state_matches_oracle(gpu, name, n, c):
     want0, _, _ = orc.simulate_text(text, n, c, r=r)
     assert float(np.max(np.abs(got0 - want0))) <= 1e-10
     sim.release()
+
+
+@pytest.mark.gpu
+def test_same_structure_new_angles_in_one_process(gpu):
+    """QAOA20 (lazy layout, schedule, quadratic phases) and the same circuit
+    with every RZZ and RX angle changed, loaded one after the other in one
+    process: identical pass structures share kernels and memo entries, but the
+    angles and the pair-phase constants (kernel parameters) must be the second
+    circuit's. Against the oracle."""
+    from oracle import quokka_oracle as orc
+    meta = json.load(open(os.path.join(GOLDEN, "golden.json")))
+    case = [c for c in meta["circuits"] if c["name"] == "qaoa20_c12"][0]
+    text = case["text"]
+    lines = []
+    for ln in text.splitlines():
+        tk = ln.split()
+        if tk and tk[0] in ("RZZ", "RX"):
+            tk[-1] = repr(float(tk[-1]) * 1.37 + 0.11)
+        lines.append(" ".join(tk))
+    text2 = "\n".join(lines) + "\n"
+    n, c = case["n"], case["c"]
+    for t in (text, text2, text):
+        sim = Simulator(LayoutParams(n=n, c=n))
+        perm = sim.load_text(t, c)
+        sim.reset()
+        got = sim.run_loaded(perm).physical_vector()
+        want, _, _ = orc.simulate_text(t, n, c)
+        assert float(np.max(np.abs(got - want))) <= TOL
+        sim.release()
