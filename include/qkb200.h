@@ -97,7 +97,9 @@ int qk_create_multi(int n, int r, int b, const int* devs, int ndev, qk_sim** out
 int qk_destroy(qk_sim* sim);
 
 /* Simulator.reset — simulator.py:439-442. Writes |0...0>; only the first 2^13
- * amplitudes go to HBM here, the next pass or reader fills the rest. */
+ * amplitudes go to HBM here. The next run's passes then read and write only
+ * the address prefix that can hold nonzero amplitudes (zero support); a reader
+ * or writer outside a run fills whatever was never written. */
 int qk_reset(qk_sim* sim);
 
 /* Layout queries */
