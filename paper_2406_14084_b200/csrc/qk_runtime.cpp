@@ -1927,7 +1927,10 @@ bool make_tma(qk_sim* s, const PassDesc& pd, TmaParams& tp, const std::vector<in
         nmat += hp.ops[o].code == OP_MAT;
       }
     }
-    const bool l1_tables = ndiag >= 2 || (pd.nphases >= 3 && nmat >= 5);
+    // (the dense-gate cap predates the quadratic phases: with tables replaced
+    // by OP_QUAD / OP_QLITE, QAOA30's passes run 3% faster on three stages;
+    // QK_SMAX_MAT=1 restores it)
+    const bool l1_tables = ndiag >= 2 || (getenv("QK_SMAX_MAT") && pd.nphases >= 3 && nmat >= 5);
     // Narrower chunks with any table keep 128 KiB of stages (QFT30: 38.0 ->
     // 34.9 ms with 8 instead of 12 16-KiB stages; 4 stages starve the loads).
     if (!tp.xbits && !getenv("QK_NO_SMAX")) {
