@@ -462,6 +462,7 @@ def run_single(args):
                       "achieved_all_gbs": achieved_all, "achieved_sqs_gbs": achieved_sqs,
                       "jit": _lib.jit_available(), "cold_load_s": cold_load_s,
                       "autotune_runs": AUTOTUNE_RUNS,
+                      "graph_replays_per_step": st[13] / args.steps,   # CUDA-graph replays (small states)
                       "zero_support": "from |0...0>, passes read and write only the address prefix that "
                                       "can hold nonzero amplitudes (exact; DESIGN.md section 3)",
                       "full_sweeps_s": full_sweeps},

@@ -174,7 +174,11 @@ int qk_program_info(const qk_sim* sim, int* n_instr, int* n_blocks, int* n_sqs,
 /* Simulator.run — simulator.py:529-555. Executes the loaded program against
  * the current state. timings[0..3] = gate, ims, xrs, wall seconds (device
  * event time per instruction class; wall = host time of the whole call).
- * The state is not reset (simulator.py:531). */
+ * The state is not reset (simulator.py:531). A single-shard handle of at
+ * most 2^24 amplitudes (QK_GRAPH_BITS) replays the launches of a run from the
+ * same start state (after qk_reset, say) from a CUDA graph captured on the
+ * second tuned run from that state (a program loaded for one run stays eager); the class times of a replay are its event time split in the
+ * proportions of the last eager run. QK_NO_GRAPH runs every launch eagerly. */
 int qk_run(qk_sim* sim, double* timings);
 
 /* Per-kernel-class device time (ms) and launch count since the last reset of
@@ -184,7 +188,8 @@ int qk_run(qk_sim* sim, double* timings);
  * bytes of the cluster-exchange block passes (block + full chunk swap in one
  * pass), which out[0..1] and out[6] exclude. out[12] = cross-shard exchanges
  * that ran overlapped with their neighbour passes (comm stream; xrs_ms is then
- * the exchange's own span). out must hold 16 doubles. */
+ * the exchange's own span). out[13] = runs replayed from a captured CUDA
+ * graph (small single-shard states; qk_run). out must hold 16 doubles. */
 int qk_kernel_stats(qk_sim* sim, double* out, int reset);
 
 /* Enable per-launch event timing (1) or per-instruction-class timing only (0). */

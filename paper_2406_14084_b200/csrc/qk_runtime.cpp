@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <complex>
@@ -23,6 +24,7 @@
 #include <cstring>
 #include <unistd.h>  // environ
 #include <string>
+#include <string_view>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -1717,6 +1719,31 @@ struct qk_sim {
   // builds; upload_plan stops after writing the generated pass sources
   bool dry = false;
   std::string dry_dir;
+  // CUDA-graph replay of small runs (qk_run, graph_run): the launches of the
+  // steps of a run from one host-side start state, captured once and replayed;
+  // the host state the steps leave is kept with the graph and re-applied
+  struct HostRunState {
+    bool fresh = false;
+    int zbits = 64, zmem = 64, zmem_next = 64, cur = 0, ovl_live = -1;
+    double fresh_saved = 0;
+    std::vector<double> saved_i;
+    std::vector<char> skipped;
+    std::vector<int> lay;
+    size_t first_exec = 0;
+  };
+  struct GraphEnt {
+    std::vector<int64_t> key;  // start state (graph_key) the graph was captured from
+    cudaGraphExec_t exec = nullptr;
+    HostRunState post;         // host state after its steps
+  };
+  std::deque<GraphEnt> graphs;                 // most recent last, at most kGraphs
+  std::deque<std::vector<int64_t>> gseen;      // start states of recent eager runs
+  uint64_t prog_gen = 0;      // identity of the uploaded plan (a graph holds its pointers)
+  bool capturing = false;     // steps record no per-instruction events
+  bool graph_timed = false;   // the run to finish was a replay: events[0..1] bracket it
+  int graph_fails = 0;
+  std::vector<double> last_ms;  // per instruction, the last eager run (replay time attribution)
+  double stat_graph = 0;        // runs replayed from a graph
 };
 
 constexpr size_t kFlagBytes = 4096;  // 64 shards x 8 B, padded
@@ -2251,6 +2278,8 @@ void plan_overlap(qk_sim* s);
 
 int upload_plan_dry(qk_sim* s);
 
+std::atomic<uint64_t> g_plan_gen{1};
+
 int upload_plan(qk_sim* s) {
   if (s->dry) return upload_plan_dry(s);
   HostPlan& hp = s->hp;
@@ -2273,6 +2302,10 @@ int upload_plan(qk_sim* s) {
   }
   char* base = (char*)s->blob;
   CUDA_TRY(cudaMemcpyAsync(base, buf.data(), buf.size(), cudaMemcpyHostToDevice, s->stream));
+  // plan identity for the graph replay (graph_key): the same plan uploaded
+  // again to the same addresses keeps a captured graph valid
+  s->prog_gen = s->nbits <= 24 ? (uint64_t)std::hash<std::string_view>()(std::string_view(buf.data(), buf.size()))
+                               : ++g_plan_gen;
   s->d_pass = (PassDesc*)(base + o_pass);
   s->d_phase = (PhaseDesc*)(base + o_phase);
   s->d_ops = (OpDesc*)(base + o_ops);
@@ -4875,7 +4908,7 @@ int run_prepare(qk_sim* s, size_t* first_exec) {
 
 int run_step(qk_sim* s, size_t i, size_t* first_exec) {
   CUDA_TRY(cudaSetDevice(s->device));
-  CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
+  if (!s->capturing) CUDA_TRY(cudaEventRecord(s->events[2 * i], s->stream));
   const bool was_fresh = s->fresh;
   const double saved0 = s->fresh_saved;
   bool skipped = false;
@@ -4886,7 +4919,7 @@ int run_step(qk_sim* s, size_t i, size_t* first_exec) {
   s->saved_i[i] = s->fresh_saved - saved0;
   if (was_fresh && !s->fresh && s->fresh_saved > 0) *first_exec = i;
   // (an overlapped exchange brackets itself on the comm stream)
-  if (!overlapped) CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
+  if (!overlapped && !s->capturing) CUDA_TRY(cudaEventRecord(s->events[2 * i + 1], s->stream));
   else s->stat_overlapped += 1;
   return QK_OK;
 }
@@ -4913,9 +4946,25 @@ int run_finish(qk_sim* s, size_t first_exec, double cls[3]) {
       s->tuning[p] = -1;
     }
   const size_t ni = s->iplan.size();
+  // a replay is timed as a whole and attributed to its instructions in the
+  // proportions of the last eager run
+  float g_ms = 0;
+  double g_sum = 0;
+  const bool replay = s->graph_timed;
+  s->graph_timed = false;
+  if (replay) {
+    CUDA_TRY(cudaEventElapsedTime(&g_ms, s->events[0], s->events[1]));
+    s->last_ms.resize(ni, 0.0);
+    for (size_t i = 0; i < ni; ++i) g_sum += s->last_ms[i];
+    s->stat_graph += 1;
+  } else {
+    s->last_ms.assign(ni, 0.0);
+  }
   for (size_t i = 0; i < ni; ++i) {
     float ms = 0;
-    CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
+    if (replay) ms = g_sum > 0 ? (float)(g_ms * s->last_ms[i] / g_sum) : (i == 0 ? g_ms : 0.f);
+    else CUDA_TRY(cudaEventElapsedTime(&ms, s->events[2 * i], s->events[2 * i + 1]));
+    if (!replay) s->last_ms[i] = ms;
     const int c = s->iplan[i].type;
     if (getenv("QK_DUMP_TIMES"))
       fprintf(stderr, "instr %zu type %d pass0 %d passes %d permuted %d fused %d: %.3f ms\n", i, c, s->iplan[i].pass0, s->iplan[i].npass,
@@ -5011,6 +5060,165 @@ int group_csqs(qk_sim* g, const int32_t* local_set, const int32_t* rank_set, int
     CUDA_TRY(cudaStreamSynchronize(m->stream));
     int rc = check_peer_error(m);
     if (rc) return rc;
+  }
+  return QK_OK;
+}
+
+// ---- CUDA-graph replay of small runs
+//
+// A run of a small state is launch-bound (QFT20: two passes of ~15 us between
+// host-side planning of zero-support views, tensor-map encodes and launches).
+// Its launch sequence is a pure function of the loaded plan, the tuned
+// variant picks and the host-side start state (fresh / zero-support bounds /
+// buffer / layout), so the steps of the first run from a start state are
+// captured into a graph (their host logic runs as in an eager run, the
+// launches go into the graph) and later runs from the same start state replay
+// it and re-apply the host state the steps left. Eligible: single-shard
+// handles of at most 2^QK_GRAPH_BITS amplitudes (default 24), tuning complete,
+// the same start state seen by the previous (eager) run,
+// reference layout at the start, no per-launch profiling; QK_NO_GRAPH turns
+// it off. Anything that fails during capture (a host sync, an unsupported
+// call) restores the start state and runs eagerly.
+
+bool tuning_pending(qk_sim* s) {
+  if (getenv("QK_NO_TUNE")) return false;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  for (size_t p = 0; p < s->pass_var.size(); ++p) {
+    if (s->pass_var[p].size() < 2) continue;
+    auto it = g_tune.find(s->pass_key[p]);
+    if (it == g_tune.end() || it->second.best < 0) return true;
+  }
+  return false;
+}
+
+bool graph_eligible(qk_sim* s) {
+  static const int max_bits = getenv("QK_GRAPH_BITS") ? atoi(getenv("QK_GRAPH_BITS")) : 24;
+  if (s->dry || s->nshards != 1 || s->per_launch || s->iplan.empty() || s->graph_fails > 2) return false;
+  if (s->nbits > max_bits || getenv("QK_NO_GRAPH") || getenv("QK_DUMP_TIMES")) return false;
+  if (!s->lay.empty() && !lay_identity(s->lay)) return false;  // a restore would sync
+  for (auto& ip : s->iplan)
+    if (ip.type == QK_INS_CSQS && ip.sqs == -2) return false;
+  return !tuning_pending(s);
+}
+
+std::vector<int64_t> graph_key(const qk_sim* s) {
+  std::string env;  // launch-time QK_* switches (QK_NO_FRESH, QK_SQS_INPLACE, ...)
+  for (char** e = environ; e && *e; ++e)
+    if (!strncmp(*e, "QK_", 3)) (env += *e) += '|';
+  // the launches' kernels and their parameter blocks as built (jit_blob is
+  // patched at launch from the run's state, which the key holds already)
+  uint64_t kh = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) { kh = (kh ^ v) * 1099511628211ull; };
+  for (size_t p = 0; p < s->pass_jit.size(); ++p) {
+    mix((uint64_t)(uintptr_t)s->pass_jit[p]);
+    if (p < s->pass_var.size())
+      for (auto& v : s->pass_var[p]) {
+        mix((uint64_t)(uintptr_t)v.kern);
+        for (uint64_t w : v.blob) mix(w);
+      }
+  }
+  for (int t : s->pass_tma) mix((uint64_t)(int64_t)t);
+  return {(int64_t)s->prog_gen, s->fresh, s->zbits,  s->zmem, s->zmem_next, s->cur, s->allow_tma,
+          (int64_t)(uintptr_t)s->d_scratch, (int64_t)s->iplan.size(), (int64_t)std::hash<std::string>()(env),
+          (int64_t)(uintptr_t)s->blob, (int64_t)(uintptr_t)s->d_pool, (int64_t)kh};
+}
+
+qk_sim::HostRunState host_state(const qk_sim* s) {
+  qk_sim::HostRunState h;
+  h.fresh = s->fresh;
+  h.zbits = s->zbits;
+  h.zmem = s->zmem;
+  h.zmem_next = s->zmem_next;
+  h.cur = s->cur;
+  h.ovl_live = s->ovl_live;
+  h.fresh_saved = s->fresh_saved;
+  h.saved_i = s->saved_i;
+  h.skipped = s->skipped;
+  h.lay = s->lay;
+  return h;
+}
+
+void set_host_state(qk_sim* s, const qk_sim::HostRunState& h) {
+  s->fresh = h.fresh;
+  s->zbits = h.zbits;
+  s->zmem = h.zmem;
+  s->zmem_next = h.zmem_next;
+  s->cur = h.cur;
+  s->state = s->bufs[s->cur];
+  s->ovl_live = h.ovl_live;
+  s->fresh_saved = h.fresh_saved;
+  s->saved_i = h.saved_i;
+  s->skipped = h.skipped;
+  s->lay = h.lay;
+}
+
+// 1: not taken (run eagerly); otherwise the run's status
+constexpr size_t kGraphs = 8;
+
+int graph_run(qk_sim* s, double* timings) {
+  if (!graph_eligible(s)) return 1;
+  const auto t0 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaSetDevice(s->device));
+  const std::vector<int64_t> key = graph_key(s);
+  qk_sim::GraphEnt* ent = nullptr;
+  for (auto& g : s->graphs)
+    if (g.key == key) ent = &g;
+  if (ent) {
+    s->norm_valid = false;  // (run_prepare's materialize)
+    set_host_state(s, ent->post);
+  } else {
+    // capture on the second run from a start state: a program loaded for one
+    // run from one state stays eager
+    if (std::find(s->gseen.begin(), s->gseen.end(), key) == s->gseen.end()) {
+      s->gseen.push_back(key);
+      if (s->gseen.size() > kGraphs) s->gseen.pop_front();
+      return 1;
+    }
+    const qk_sim::HostRunState pre = host_state(s);
+    const bool nv = s->norm_valid;
+    size_t first_exec = 0;
+    int rc = ensure_events(s, 2 * s->iplan.size() + 2);
+    if (rc) return rc;
+    s->capturing = true;
+    cudaError_t e = cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+      rc = run_prepare(s, &first_exec);
+      for (size_t i = 0; !rc && i < s->iplan.size(); ++i) rc = run_step(s, i, &first_exec);
+    }
+    cudaGraph_t g = nullptr;
+    const cudaError_t e2 = e == cudaSuccess ? cudaStreamEndCapture(s->stream, &g) : e;
+    s->capturing = false;
+    cudaGraphExec_t ex = nullptr;
+    if (!rc && e2 == cudaSuccess && g && cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) ex = nullptr;
+    if (g) cudaGraphDestroy(g);
+    if (!ex) {
+      cudaGetLastError();
+      set_host_state(s, pre);
+      s->norm_valid = nv;
+      s->graph_fails += 1;
+      return 1;
+    }
+    if (s->graphs.size() >= kGraphs) {
+      cudaGraphExecDestroy(s->graphs.front().exec);
+      s->graphs.pop_front();
+    }
+    s->graphs.push_back({key, ex, host_state(s)});
+    ent = &s->graphs.back();
+    ent->post.first_exec = first_exec;
+  }
+  CUDA_TRY(cudaEventRecord(s->events[0], s->stream));
+  CUDA_TRY(cudaGraphLaunch(ent->exec, s->stream));
+  CUDA_TRY(cudaEventRecord(s->events[1], s->stream));
+  s->graph_timed = true;
+  double cls[3] = {0, 0, 0};
+  int rc = run_finish(s, ent->post.first_exec, cls);
+  if (rc) return rc;
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (timings) {
+    timings[0] = cls[0] * 1e-3;
+    timings[1] = cls[1] * 1e-3;
+    timings[2] = cls[2] * 1e-3;
+    timings[3] = wall;
   }
   return QK_OK;
 }
@@ -5143,6 +5351,7 @@ int qk_destroy(qk_sim* s) {
   }
   cudaSetDevice(s->device);
   if (s->stream) cudaStreamSynchronize(s->stream);
+  for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
   for (auto e : s->events) cudaEventDestroy(e);
   for (auto e : s->tune_ev) cudaEventDestroy(e);
   for (auto e : s->marks)
@@ -5189,8 +5398,7 @@ int qk_reset(qk_sim* s) {
   int rc = launch_fill_zero_one(s->state, s->fresh ? (1ull << kFreshBits) : s->amps, s->rank_lo == 0,
                                 (CUstream_st*)s->stream);
   if (rc) return fail(QK_ECUDA, "reset failed");
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  return QK_OK;
+  return QK_OK;  // stream-ordered: every later entry point uses this stream
 }
 
 int qk_layout(const qk_sim* s, int* n, int* r, int* b, int* rank_lo, int* count) {
@@ -5315,6 +5523,10 @@ int qk_set_profiling(qk_sim* s, int per_launch) {
 int qk_run(qk_sim* s, double* timings) {
   if (!s) return fail(QK_EINVAL, "null handle");
   if (is_group(s)) return group_run(s, timings);
+  {
+    const int g = graph_run(s, timings);
+    if (g != 1) return g;
+  }
   const auto t0 = std::chrono::steady_clock::now();
   size_t first_exec = 0;
   int rc = run_prepare(s, &first_exec);
@@ -5354,11 +5566,13 @@ int qk_kernel_stats(qk_sim* s, double* out, int reset) {
     out[10] = s->stat_launch[3];
     out[11] = s->stat_bytes[3];
     out[12] = s->stat_overlapped;
-    out[13] = out[14] = out[15] = 0;
+    out[13] = s->stat_graph;
+    out[14] = out[15] = 0;
   }
   if (reset) {
     for (int c = 0; c < 4; ++c) s->stat_ms[c] = s->stat_launch[c] = s->stat_bytes[c] = 0;
     s->stat_overlapped = 0;
+    s->stat_graph = 0;
   }
   return QK_OK;
 }
