@@ -545,10 +545,12 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
       budget -= regs;
       qhoisted[q] = 1;
       pro << "  double2 qw" << q << ", qv" << q << "[" << M << "];\n";
-      pro << "  { const double2* qt = p.tabs + p.toff[" << QT + q << "] + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
+      // per-thread columns (qk_internal.h QuadLayout): entry k of thread tid at k * 2^T + tid
+      pro << "  { const double2* qt = p.tabs + p.toff[" << QT + q << "] + " << QL.thr / 2 << " + tid;\n";
       pro << "    qw" << q << " = __ldg(qt);\n";
       for (int sl = 0; sl < M; ++sl)
-        if (op.code == OP_QUAD || (op.pr[0] >> sl & 1)) pro << "    qv" << q << "[" << sl << "] = __ldg(qt + " << 1 + sl << ");\n";
+        if (op.code == OP_QUAD || (op.pr[0] >> sl & 1))
+          pro << "    qv" << q << "[" << sl << "] = __ldg(qt + " << (1 + sl) * (1 << (C - M)) << ");\n";
       pro << "  }\n";
     }
   }
@@ -826,17 +828,17 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
             for (int sl = 0; sl < M; ++sl)
               if (act >> sl & 1) {
                 if (qhoisted[q]) b << "      const double2 e" << sl << " = qv" << q << "[" << sl << "];\n";
-                else b << "      const double2 e" << sl << " = __ldg(qd + " << QL0.thr / 2 << " + tid * " << 1 + M << "u + " << 1 + sl << ");\n";
+                else b << "      const double2 e" << sl << " = __ldg(qd + " << QL0.thr / 2 + (1 + sl) * (1 << (C - M)) << " + tid);\n";
               }
           } else if (qhoisted[q]) {
             b << "      const double2 E = qw" << q << ";\n";
             for (int sl = 0; sl < M; ++sl)
               if (act >> sl & 1) b << "      const double2 e" << sl << " = qv" << q << "[" << sl << "];\n";
           } else {
-            b << "      const double2* qt = qd + " << QL0.thr / 2 << " + tid * " << 1 + M << "u;\n";
+            b << "      const double2* qt = qd + " << QL0.thr / 2 << " + tid;\n";
             b << "      const double2 E = __ldg(qt);\n";
             for (int sl = 0; sl < M; ++sl)
-              if (act >> sl & 1) b << "      const double2 e" << sl << " = __ldg(qt + " << 1 + sl << ");\n";
+              if (act >> sl & 1) b << "      const double2 e" << sl << " = __ldg(qt + " << (1 + sl) * (1 << (C - M)) << ");\n";
           }
           // partial products over the active slots, depth-first ("" = exactly 1)
           std::function<void(int, int, const std::string&)> visit = [&](int j, int bit, const std::string& f) {
@@ -882,12 +884,12 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
           if (qhoisted[q]) {
             b << "      double2 E = cm(Bt, qw" << q << ");\n";
           } else {
-            b << "      const double2* qt = qd + " << QL.thr / 2 << " + tid * " << 1 + M << "u;\n";
+            b << "      const double2* qt = qd + " << QL.thr / 2 << " + tid;\n";
             b << "      double2 E = cm(Bt, __ldg(qt));\n";
           }
           for (int sl = 0; sl < M; ++sl) {
             if (qhoisted[q]) b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], qv" << q << "[" << sl << "]);\n";
-            else b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], __ldg(qt + " << 1 + sl << "));\n";
+            else b << "      const double2 e" << sl << " = cm(fq[" << R[sl] << "], __ldg(qt + " << (1 + sl) * (1 << (C - M)) << "));\n";
           }
           // depth-first over the slots: a stack of M + 1 partial products
           const QuadOp* qk = (quad && o < (int)quad->size() && (*quad)[o].npj == NA) ? &(*quad)[o] : nullptr;

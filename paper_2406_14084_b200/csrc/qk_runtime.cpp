@@ -1107,16 +1107,17 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
           for (int k2 = k + 1; k2 < TT; ++k2)
             if (tid >> k2 & 1) aw += P2(Tth[k], Tth[k2]);
       const cplx w = sc * cexpi(wrap_angle(aw));
-      double* row = &d[L.thr + (size_t)tid * (1 + M) * 2];
-      row[0] = w.real();
-      row[1] = w.imag();
+      // per-thread columns: entry k of thread tid at k * 2^(C-M) + tid (coalesced loads)
+      auto cell = [&](int k) { return &d[L.thr + 2 * ((size_t)k * ((size_t)1 << (C - M)) + tid)]; };
+      cell(0)[0] = w.real();
+      cell(0)[1] = w.imag();
       for (int sl = 0; sl < M; ++sl) {
         double av = 0.0;
         for (int k = 0; k < TT; ++k)
           if (tid >> k & 1) av += P2(Tth[k], R[sl]);
         const cplx v = cexpi(wrap_angle(av));
-        row[2 + 2 * sl] = v.real();
-        row[3 + 2 * sl] = v.imag();
+        cell(1 + sl)[0] = v.real();
+        cell(1 + sl)[1] = v.imag();
       }
     }
     for (int j = 0; j < (1 << M); ++j) {
@@ -1192,9 +1193,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
             if (tid >> k2 & 1) ae += P2(Tth[k], Tth[k2]);
         }
       const cplx e = sc * cexpi(wrap_angle(ae));
-      double* row = &d[L.thr + (size_t)tid * (1 + M) * 2];
-      row[0] = e.real();
-      row[1] = e.imag();
+      auto cell = [&](int k) { return &d[L.thr + 2 * ((size_t)k * ((size_t)1 << (C - M)) + tid)]; };
+      cell(0)[0] = e.real();
+      cell(0)[1] = e.imag();
       for (int sl = 0; sl < M; ++sl) {
         double av = lin[R[sl]];
         for (int k = 0; k < TT; ++k)
@@ -1202,8 +1203,8 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
         av = wrap_angle(av);
         if (av != 0.0) *slot_mask |= (uint16_t)(1u << sl);
         const cplx v = cexpi(av);
-        row[2 + 2 * sl] = v.real();
-        row[3 + 2 * sl] = v.imag();
+        cell(1 + sl)[0] = v.real();
+        cell(1 + sl)[1] = v.imag();
       }
     }
     for (int j = 0; j < (1 << M); ++j) {
@@ -1222,11 +1223,12 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
     // products become constants in pj (flag 1); otherwise flag 2 when E is
     // exactly 1 for every thread (no thread-only or global phase)
     bool same = true, e_one = true;
-    const size_t rl = (size_t)(1 + M) * 2;
+    const size_t NT = (size_t)1 << (C - M);
+    auto at = [&](int tid, int k) { return &d[L.thr + 2 * ((size_t)k * NT + tid)]; };
     for (int tid = 0; tid < (1 << TT); ++tid) {
-      const double* row = &d[L.thr + (size_t)tid * rl];
-      same = same && std::equal(row, row + rl, &d[L.thr]);
-      e_one = e_one && row[0] == 1.0 && row[1] == 0.0;
+      for (int k = 0; k <= M; ++k)
+        same = same && at(tid, k)[0] == at(0, k)[0] && at(tid, k)[1] == at(0, k)[1];
+      e_one = e_one && at(tid, 0)[0] == 1.0 && at(tid, 0)[1] == 0.0;
     }
     *flags = 0;
     if (same) {
@@ -1234,9 +1236,9 @@ int compile_pass(HostPlan& hp, const std::vector<const GateH*>& gates_in, const 
       *pj_mask = 0;
       *slot_mask = 0;
       for (int j = 0; j < (1 << M); ++j) {
-        cplx f(d[L.thr], d[L.thr + 1]);
+        cplx f(at(0, 0)[0], at(0, 0)[1]);
         for (int sl = 0; sl < M; ++sl)
-          if (j >> sl & 1) f *= cplx(d[L.thr + 2 + 2 * sl], d[L.thr + 3 + 2 * sl]);
+          if (j >> sl & 1) f *= cplx(at(0, 1 + sl)[0], at(0, 1 + sl)[1]);
         f *= cplx(d[L.pj + 2 * j], d[L.pj + 2 * j + 1]);
         d[L.pj + 2 * j] = f.real();
         d[L.pj + 2 * j + 1] = f.imag();
@@ -3252,7 +3254,9 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     }
     const char* cenv = getenv("QK_REBLOCK_CAP");
     const auto trb = std::chrono::steady_clock::now();
-    const bool rbok = ok && reblock_memo(s->prog, nb, cenv ? atoi(cenv) : 12, 3, &rprog, &rb_p2w, s->n, nullptr);
+    // row bits forced into every tile: 3 (128-B rows); QK_ROWBITS=4 (dev) gives 256-B row segments
+    const int rowb = getenv("QK_ROWBITS") ? atoi(getenv("QK_ROWBITS")) : 3;
+    const bool rbok = ok && reblock_memo(s->prog, nb, cenv ? atoi(cenv) : 12, rowb, &rprog, &rb_p2w, s->n, nullptr);
     if (getenv("QK_DUMP_LOAD"))
       fprintf(stderr, "load: reblock %.3f ms\n",
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - trb).count());
@@ -3295,7 +3299,8 @@ int compile_program_impl(qk_sim* s, bool try_reblock, bool* reblocked) {
     std::vector<InstrH> rprog2;
     std::vector<int> p2w2;
     const char* cenv2 = getenv("QK_REBLOCK_CAP");
-    if (!ident_pos && reblock_memo(s->prog, nb, cenv2 ? atoi(cenv2) : 12, 3, &rprog2, &p2w2, s->n, &pos)) {
+    const int rowb2 = getenv("QK_ROWBITS") ? atoi(getenv("QK_ROWBITS")) : 3;
+    if (!ident_pos && reblock_memo(s->prog, nb, cenv2 ? atoi(cenv2) : 12, rowb2, &rprog2, &p2w2, s->n, &pos)) {
       size_t n1 = 0, n2 = 0;
       for (auto& ins : rprog) n1 += ins.type == QK_INS_BLOCK;
       for (auto& ins : rprog2) n2 += ins.type == QK_INS_BLOCK;
