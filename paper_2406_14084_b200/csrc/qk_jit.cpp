@@ -535,8 +535,11 @@ bool jit_source(const TmaParams& tp, std::string* src, std::vector<long long>* t
   std::vector<char> qhoisted(qops.size(), 0);
   {
     // (measured spill-free: one OP_QUAD hoisted; with many OP_QLITE only ~8)
+    // (variant bit 4 orders OP_QUAD factors, so a pass without OP_QUAD reuses
+    // it for a larger budget: QFT's OP_QLITE-heavy passes, 48 registers)
     const char* qb = getenv("QK_QHOIST");
     int budget = qb ? atoi(qb) : ((int)qops.size() > NQ ? 8 : 20);
+    if (!qb && !NQ && !qops.empty() && (variant & 4)) budget = 48;
     for (size_t q = 0; q < qops.size(); ++q) {
       const TOp& op = tp.ops[qops[q]];
       const int act = op.code == OP_QUAD ? M : __builtin_popcount(op.pr[0] & ((1u << M) - 1));

@@ -2393,7 +2393,8 @@ int upload_plan(qk_sim* s) {
     const auto tj0 = std::chrono::steady_clock::now();
     // Up to sixteen variants per pass (bit 1: no hoisted table, bit 2: quadratic
     // table groups, bit 4: OP_QUAD factors computed after the stage wait
-    // instead of ahead in a pending slot, bit 8: TMA-store epilogue for lazy
+    // instead of ahead in a pending slot (passes without OP_QUAD: more
+    // OP_QLITE factors hoisted into registers), bit 8: TMA-store epilogue for lazy
     // passes); identical sources are built once. QK_JIT_VARIANT=v pins one,
     // otherwise the first runs time every variant and keep the fastest per
     // pass structure (process-wide, tune_pick / tune_record). A pass structure
