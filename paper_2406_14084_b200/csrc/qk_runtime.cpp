@@ -2536,16 +2536,41 @@ int upload_plan(qk_sim* s) {
       }
     }
   plan_overlap(s);
+  // OP_QUAD / OP_QLITE data: one H2D copy of the pool span they occupy (the
+  // gaps are table regions, which the table build below writes), instead of
+  // one pageable copy per op (QFT20: 18 copies)
+  const auto tq0 = std::chrono::steady_clock::now();
+  bool qdone = hp.qcopy.empty();
+  if (!qdone) {
+    size_t lo = SIZE_MAX, hi = 0, tot = 0;
+    for (auto& q : hp.qcopy) {
+      lo = std::min(lo, (size_t)(2 * q.first));
+      hi = std::max(hi, (size_t)(2 * q.first) + q.second.size());
+      tot += q.second.size();
+    }
+    if ((hi - lo) * sizeof(double) <= ((size_t)4 << 20) && hi - lo <= 2 * tot + 8192) {
+      std::vector<double> img(hi - lo, 0.0);
+      for (auto& q : hp.qcopy) std::copy(q.second.begin(), q.second.end(), img.begin() + (2 * q.first - lo));
+      CUDA_TRY(cudaMemcpyAsync(s->d_pool + lo, img.data(), img.size() * sizeof(double), cudaMemcpyHostToDevice,
+                               s->stream));
+      qdone = true;
+    }
+  }
   if (!hp.tables.empty()) {
     int rc = launch_build_tables((const TableDesc*)(base + o_tab), (int)hp.tables.size(),
                                  (const TableGate*)(base + o_tg), (const double*)(base + o_ent),
                                  s->d_pool, (CUstream_st*)s->stream);
     if (rc) return fail(QK_ECUDA, "table build launch failed: %s", cudaGetErrorString((cudaError_t)rc));
   }
-  for (auto& q : hp.qcopy)
-    CUDA_TRY(cudaMemcpyAsync(s->d_pool + 2 * q.first, q.second.data(), q.second.size() * sizeof(double),
-                             cudaMemcpyHostToDevice, s->stream));
+  if (!qdone)
+    for (auto& q : hp.qcopy)
+      CUDA_TRY(cudaMemcpyAsync(s->d_pool + 2 * q.first, q.second.data(), q.second.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (getenv("QK_DUMP_LOAD"))
+    fprintf(stderr, "load: quad data %zu ops (%s), tables and sync %.3f ms\n", hp.qcopy.size(),
+            hp.qcopy.empty() ? "none" : "one copy or per op",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
   return QK_OK;
 }
 
